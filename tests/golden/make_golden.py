@@ -1,0 +1,124 @@
+"""Generates the golden vectors in tests/golden/ from the UNMODIFIED reference.
+
+Run in the build container (needs /root/reference and ``make -C oracle ref``):
+
+    python tests/golden/make_golden.py
+
+Every vector below is produced by oracle/_ref/libspecpar_ref.so, i.e. the reference sources
+/root/reference/proj/src compiled as they lie, driven through oracle/ref_shim.cpp.  Nothing here is
+computed by our own code, so the fixtures pin both the oracle restatement and the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+import os
+import random
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle.pyoracle import Oracle, Reference  # noqa: E402
+
+CFG1 = "/root/reference/proj/configs/ceiling_break.cfg"
+METHODS = ["vanilla_ar", "sd", "psd", "target_retrieval", "draft_retrieval", "double"]
+METRIC_KEYS = ["tokens", "rounds", "clock", "m", "amt", "speedup", "hit_rate", "lookups"]
+
+
+def sha(s: str) -> str:
+    return hashlib.sha256(s.encode()).hexdigest()
+
+
+def criterion1_configs(orc: Oracle):
+    """The acceptance.cpp:62-89 configuration set (Rng(20240817) picks), as key=value texts."""
+    class MT(C.Structure):
+        _fields_ = [("mt", C.c_uint64 * 312), ("idx", C.c_int)]
+    g = MT()
+    orc.lib.orc_mt64_seed.argtypes = [C.POINTER(MT), C.c_uint64]
+    orc.lib.orc_uniform.argtypes = [C.POINTER(MT)]
+    orc.lib.orc_uniform.restype = C.c_double
+    orc.lib.orc_mt64_seed(C.byref(g), 20240817)
+
+    def pick(arr):
+        return arr[int(orc.lib.orc_uniform(C.byref(g)) * len(arr))]
+    out = []
+    for i in range(100):
+        vocab = pick([16, 64])
+        dorder = pick([1, 2])
+        torder = pick([1, 2])
+        rho = pick([0.0, 0.5, 0.9])
+        gamma = pick([2, 4])
+        depth = pick([4, 10])
+        out.append(dict(vocab=vocab, draft_order=dorder, target_order=torder, rho=rho, gamma=gamma,
+                        depth=depth, corpus_len=2048, max_new_tokens=256, seed=1000 + i,
+                        method="double", engine="serial"))
+    return out
+
+
+def cfg_text(d: dict) -> str:
+    return "".join(f"{k}={v}\n" for k, v in d.items())
+
+
+def main():
+    ref = Reference()
+    orc = Oracle()
+    # ---- config 1 (ceiling_break.cfg) -------------------------------------------------------
+    text = open(CFG1).read()
+    draft_v1, target_v1, prior_v1, prompt = ref.export_setup(text)
+    open(os.path.join(HERE, "config1_draft.model-v1"), "w").write(draft_v1)
+    open(os.path.join(HERE, "config1_target.model-v1"), "w").write(target_v1)
+    open(os.path.join(HERE, "config1_prior.dstore-v1"), "w").write(prior_v1)
+    c1 = {"config": text, "prompt": prompt, "sha256": {
+        "draft_model_v1": sha(draft_v1), "target_model_v1": sha(target_v1),
+        "prior_dstore_v1": sha(prior_v1)}, "methods": {}}
+    for m in METHODS:
+        out, js, met = ref.run_config(text, m)
+        c1["methods"][m] = {"output": out, "jsonl_sha256": sha(js),
+                            "metrics": dict(zip(METRIC_KEYS, met))}
+        if m in ("double", "psd", "target_retrieval"):
+            c1["methods"][m]["jsonl"] = js
+    json.dump(c1, open(os.path.join(HERE, "config1.json"), "w"), indent=1)
+
+    # ---- acceptance criterion-1 set (100 randomized Double configs) ------------------------
+    acc = []
+    for d in criterion1_configs(orc):
+        t = cfg_text(d)
+        out, js, met = ref.run_config(t, "double")
+        ar, _, _ = ref.run_config(t, "vanilla_ar")
+        acc.append({"config": d, "output_sha256": sha(" ".join(map(str, out))),
+                    "ar_output_sha256": sha(" ".join(map(str, ar))),
+                    "n_output": len(out), "jsonl_sha256": sha(js),
+                    "metrics": dict(zip(METRIC_KEYS, met))})
+    json.dump(acc, open(os.path.join(HERE, "acceptance100.json"), "w"), indent=0)
+
+    # ---- retrieval: random stores x contexts (layers, steps incl. ties and non-monotone) ---
+    rng = random.Random(20261017)
+    cases = []
+    for case in range(60):
+        max_order = rng.choice([1, 2, 3, 3, 3, 4, 5])
+        vocab = rng.choice([3, 4, 6, 8, 16])
+        inserts = []
+        for _ in range(rng.randint(0, 12)):
+            layer = rng.choice([0, 1, 2])
+            toks = [rng.randrange(vocab) for _ in range(rng.randint(1, 24))]
+            step = rng.choice([rng.randint(0, 5), rng.randint(0, 1000)])
+            inserts.append((layer, toks, step))
+        queries = []
+        for _ in range(rng.randint(1, 12)):
+            ctx = [rng.randrange(vocab) for _ in range(rng.randint(1, 30))]
+            queries.append((ctx, rng.choice([1, 2, 3, 5, 10, 10, 40])))
+        rej = rng.random() < 0.8
+        res, stats = ref.lookup_batch(max_order, inserts, queries, rejected_enabled=rej)
+        cases.append({"max_order": max_order, "rejected_enabled": rej,
+                      "inserts": [[l, t, s] for l, t, s in inserts],
+                      "queries": [[c, d] for c, d in queries],
+                      "results": [[c, s, o] for c, s, o in res], "stats": stats})
+    json.dump(cases, open(os.path.join(HERE, "lookups.json"), "w"))
+    print("golden vectors written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
