@@ -1,0 +1,156 @@
+/* double_b200.h — the C-ABI drop-in boundary of the B200-native DOUBLE decode loop.
+ *
+ * The reference (arXiv 2601.05524 artifact, /root/reference/proj) exposes its decode path as C++ free
+ * functions and structs in proj/include/specpar/*.hpp.  This header is the thin C layer the C++ host
+ * code (include/double_b200.hpp, namespace specpar) calls; every entry point below names the
+ * reference interface it replaces.  Conventions:
+ *   - plain pointers + sizes, no C++ or torch types; host buffers unless a name says "_dev";
+ *   - every call returns a dbl_status; dbl_last_error() returns the thread's last message;
+ *   - errors map 1:1 onto the reference's exception types (std::invalid_argument ->
+ *     DBL_INVALID_ARGUMENT, std::runtime_error -> DBL_RUNTIME_ERROR, std::logic_error ->
+ *     DBL_LOGIC_ERROR), so the C++ shim rethrows the same types (pipeline.cpp:18-22, 210-217);
+ *   - there is no CPU fallback: without a usable sm_100 device every compute entry point fails with
+ *     DBL_CUDA_ERROR.
+ */
+#ifndef DOUBLE_B200_H
+#define DOUBLE_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+    DBL_OK = 0,
+    DBL_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    DBL_RUNTIME_ERROR = 2,    /* std::runtime_error    */
+    DBL_LOGIC_ERROR = 3,      /* std::logic_error      */
+    DBL_CUDA_ERROR = 4,
+    DBL_NCCL_ERROR = 5
+} dbl_status;
+
+/* LookupSource (datastore.hpp:29) — same order */
+typedef enum { DBL_SRC_PRIOR = 0, DBL_SRC_DYNAMIC = 1, DBL_SRC_REJECTED = 2, DBL_SRC_CONTEXT = 3, DBL_SRC_MISS = 4 } dbl_source;
+/* datastore layers */
+typedef enum { DBL_LAYER_PRIOR = 0, DBL_LAYER_DYNAMIC = 1, DBL_LAYER_REJECTED = 2 } dbl_layer;
+
+typedef struct dbl_store_s* dbl_store_t;     /* device-resident HierarchicalDatastore */
+typedef struct dbl_model_s* dbl_model_t;     /* device model: table (config 1) or transformer */
+
+const char* dbl_last_error(void);
+int dbl_version(void);
+/* 1 when a CUDA device of compute capability 10.x is visible and the kernels load */
+int dbl_device_ok(void);
+
+/* ===================================================================== datastore
+ * Replaces specpar::HierarchicalDatastore / NGramIndex (datastore.hpp:19-95, datastore.cpp:9-147).
+ * Layers are append-only token arrays in HBM; an n-gram occurrence is any (sequence, end) whose last
+ * n tokens match, found by a warp-cooperative suffix-match scan (no host index). */
+int dbl_store_create(int max_order, int depth, int device, dbl_store_t* out);   /* HierarchicalDatastore(n, d), datastore.hpp:75-79 */
+int dbl_store_destroy(dbl_store_t s);
+int dbl_store_set_rejected_enabled(dbl_store_t s, int enabled);                  /* rejected_enabled, datastore.hpp:80 */
+int dbl_store_set_layer_order(dbl_store_t s, int layer, int max_order);          /* NGramIndex::max_order, datastore.hpp:20 */
+int dbl_store_insert(dbl_store_t s, int layer, const int32_t* tokens, int n, int64_t step); /* NGramIndex::insert, datastore.cpp:9-20 */
+int dbl_store_record(dbl_store_t s, int layer, const int32_t* tokens, int n);    /* record_accepted / record_rejected, datastore.cpp:134-142 */
+int dbl_store_flush_session(dbl_store_t s);                                      /* flush_session, datastore.cpp:144-147 */
+int dbl_store_clear_layer(dbl_store_t s, int layer);                             /* NGramIndex::clear, datastore.cpp:28-31 */
+int dbl_store_get_step(dbl_store_t s, int64_t* step);                            /* step_counter, datastore.hpp:79 */
+int dbl_store_set_step(dbl_store_t s, int64_t step);
+/* per-layer sizes; occurrences == NGramIndex::occurrence_count (datastore.cpp:22-26) */
+int dbl_store_layer_info(dbl_store_t s, int layer, int64_t* n_seqs, int64_t* n_tokens, int64_t* occurrences);
+/* copies back the layer's sequences (dstore-v1 content, datastore.cpp:149-159) */
+int dbl_store_layer_read(dbl_store_t s, int layer, int32_t* tokens, int64_t tok_cap, int32_t* seq_lens, int64_t* steps, int64_t seq_cap);
+/* HierarchicalDatastore::lookup (datastore.cpp:82-132): one query, host in / host out */
+int dbl_store_lookup(dbl_store_t s, const int32_t* ctx, int L, int d, int32_t* cands, int cap,
+                     int* n_cands, int* source, int* matched_order);
+/* n_q independent queries in ONE launch (one CTA per query); stats accumulate as n_q lookups.
+ * q_offsets[n_q+1] index q_tokens; out_cands is n_q x d_cap. */
+int dbl_store_lookup_batch(dbl_store_t s, int n_q, const int64_t* q_offsets, const int32_t* q_tokens,
+                           const int32_t* depths, int d_cap, int32_t* out_cands, int32_t* out_n,
+                           int32_t* out_source, int32_t* out_order);
+/* LookupStats (datastore.hpp:39-67): lookups, prior, dynamic, rejected, fallback, misses */
+int dbl_store_stats(dbl_store_t s, int64_t out[6]);
+
+/* ===================================================================== models
+ * Replaces specpar::TableModel + forward / forward_batch / argmax_token (model.hpp:18-48,
+ * model.cpp:13-81).  Greedy decoding consumes a distribution only through argmax_token (lowest id on
+ * ties), so device models return per-row argmax ids; logits/probabilities are available for checks. */
+/* TableModel (config 1): n_rows windows of `order` tokens with vocab-wide fp64 rows + fallback row */
+int dbl_table_create(int order, int vocab, int64_t n_rows, const int32_t* windows, const double* probs,
+                     const double* fallback, int device, dbl_model_t* out);
+
+/* Random-init bf16 decoder-only transformer (Qwen3 / Llama shapes).  No reference counterpart: it
+ * stands in for the paper's LLMs behind the same forward_batch contract. */
+typedef struct {
+    int n_layers, hidden, ffn, n_heads, n_kv_heads, head_dim, vocab;
+    int tied_embeddings; /* LM head = embedding matrix */
+    int qk_norm;         /* Qwen3 per-head RMSNorm on q and k */
+    float rope_theta, rms_eps, init_std;
+    int max_seq;         /* KV capacity in tokens */
+    uint64_t seed;       /* weights are a pure function of (seed, tensor, index) */
+    int tp_rank, tp_size;/* tensor parallel shard (1 = unsharded) */
+} dbl_transformer_config;
+/* nccl_comm: an ncclComm_t for tp_size > 1 (else NULL) */
+int dbl_transformer_create(const dbl_transformer_config* cfg, int device, void* nccl_comm, dbl_model_t* out);
+int dbl_model_destroy(dbl_model_t m);
+int dbl_model_vocab(dbl_model_t m, int* vocab);
+/* bytes of weights streamed per forward on this rank (the roofline numerator's static part) */
+int dbl_model_weight_bytes(dbl_model_t m, int64_t* bytes);
+
+/* forward_batch (model.cpp:37-53): |cands|+1 rows, row k = next-token distribution after
+ * ctx ⊕ cands[0..k); stateless (transformers recompute the whole context into a scratch KV). */
+int dbl_forward_argmax(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, int32_t* out_argmax);
+/* same rows as fp32 logits (transformer) or fp64 probabilities cast to fp32 (table), (c+1) x vocab */
+int dbl_forward_logits(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, float* out);
+/* copies a named weight tensor to host (bf16 bits as uint16); for the fp32 torch reference in tests */
+int dbl_transformer_get_weight(dbl_model_t m, const char* name, int layer, uint16_t* out, int64_t numel);
+
+/* ===================================================================== decode loop
+ * Replaces specpar::run / run_round / compute_metrics / traces_to_jsonl (pipeline.hpp:93-115,
+ * pipeline.cpp:15-400) and the harness's run_vanilla_ar (harness.cpp:233-258). */
+typedef struct {
+    int gamma, depth;
+    int draft_retrieval, target_retrieval;
+    int concurrent;          /* Engine::Concurrent; the device loop always overlaps draft and target */
+    double t_target, t_draft, t_lookup, t_sync; /* LatencyConfig, pipeline.hpp:15-29 */
+    int use_graphs;          /* capture the draft chain / target forward in CUDA graphs */
+} dbl_pipeline_options;
+
+typedef struct { /* RunMetrics (pipeline.hpp:73-82) + device timing */
+    int64_t tokens, rounds;
+    double clock, m, amt, speedup, hit_rate;
+    int64_t lookups;
+    double device_ms;        /* CUDA-event time of the decode loop (prefill excluded) */
+    double prefill_ms;       /* CUDA-event time of the prompt prefill */
+    double target_fwd_ms;    /* summed CUDA-event time of target verify forwards */
+    int64_t target_fwd_count;
+    int64_t target_rows;     /* summed verify rows */
+    int64_t kernel_launches; /* device kernels launched by the loop (graph nodes counted) */
+} dbl_run_metrics;
+
+/* run (pipeline.cpp:264-323).  out: committed tokens after the prompt, truncated to max_new.
+ * jsonl: traces_to_jsonl text (may be NULL); jsonl_len receives the full length. */
+int dbl_run(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
+            int n_prompt, int max_new, const dbl_pipeline_options* opts, int32_t* out, int cap,
+            int* n_out, dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len);
+/* run_vanilla_ar (harness.cpp:233-258), greedy: target-only, one forward per token */
+int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
+               int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
+               int64_t jsonl_cap, int64_t* jsonl_len);
+/* run_serial_sd (harness.cpp:264-369): draft-then-verify, use_retrieval = draft_retrieval method */
+int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
+                      int n_prompt, int max_new, const dbl_pipeline_options* opts, int use_retrieval,
+                      int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
+                      int64_t jsonl_cap, int64_t* jsonl_len);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOUBLE_B200_H */

@@ -1,0 +1,132 @@
+"""ctypes prototypes for the C-ABI in include/double_b200.h (libdouble_b200.so, built in-tree).
+
+There is no fallback: importing this module without the built library raises, and every compute
+entry point fails with DBL_CUDA_ERROR when no sm_100 device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libdouble_b200.so")
+
+I32P = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+F64P = C.POINTER(C.c_double)
+F32P = C.POINTER(C.c_float)
+U16P = C.POINTER(C.c_uint16)
+VP = C.c_void_p
+
+OK, INVALID_ARGUMENT, RUNTIME_ERROR, LOGIC_ERROR, CUDA_ERROR, NCCL_ERROR = range(6)
+
+
+class TransformerConfig(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("hidden", C.c_int), ("ffn", C.c_int), ("n_heads", C.c_int),
+                ("n_kv_heads", C.c_int), ("head_dim", C.c_int), ("vocab", C.c_int),
+                ("tied_embeddings", C.c_int), ("qk_norm", C.c_int), ("rope_theta", C.c_float),
+                ("rms_eps", C.c_float), ("init_std", C.c_float), ("max_seq", C.c_int),
+                ("seed", C.c_uint64), ("tp_rank", C.c_int), ("tp_size", C.c_int)]
+
+
+class PipelineOptions(C.Structure):
+    _fields_ = [("gamma", C.c_int), ("depth", C.c_int), ("draft_retrieval", C.c_int),
+                ("target_retrieval", C.c_int), ("concurrent", C.c_int), ("t_target", C.c_double),
+                ("t_draft", C.c_double), ("t_lookup", C.c_double), ("t_sync", C.c_double),
+                ("use_graphs", C.c_int)]
+
+
+class RunMetrics(C.Structure):
+    _fields_ = [("tokens", C.c_int64), ("rounds", C.c_int64), ("clock", C.c_double),
+                ("m", C.c_double), ("amt", C.c_double), ("speedup", C.c_double),
+                ("hit_rate", C.c_double), ("lookups", C.c_int64), ("device_ms", C.c_double),
+                ("prefill_ms", C.c_double), ("target_fwd_ms", C.c_double),
+                ("target_fwd_count", C.c_int64), ("target_rows", C.c_int64),
+                ("kernel_launches", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+# name -> argtypes (all return int status unless listed in _RESTYPE)
+PROTOTYPES = {
+    "dbl_last_error": [],
+    "dbl_version": [],
+    "dbl_device_ok": [],
+    "dbl_store_create": [C.c_int, C.c_int, C.c_int, C.POINTER(VP)],
+    "dbl_store_destroy": [VP],
+    "dbl_store_set_rejected_enabled": [VP, C.c_int],
+    "dbl_store_set_layer_order": [VP, C.c_int, C.c_int],
+    "dbl_store_insert": [VP, C.c_int, I32P, C.c_int, C.c_int64],
+    "dbl_store_record": [VP, C.c_int, I32P, C.c_int],
+    "dbl_store_flush_session": [VP],
+    "dbl_store_clear_layer": [VP, C.c_int],
+    "dbl_store_get_step": [VP, I64P],
+    "dbl_store_set_step": [VP, C.c_int64],
+    "dbl_store_layer_info": [VP, C.c_int, I64P, I64P, I64P],
+    "dbl_store_layer_read": [VP, C.c_int, I32P, C.c_int64, I32P, I64P, C.c_int64],
+    "dbl_store_lookup": [VP, I32P, C.c_int, C.c_int, I32P, C.c_int, C.POINTER(C.c_int),
+                         C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "dbl_store_lookup_batch": [VP, C.c_int, I64P, I32P, I32P, C.c_int, I32P, I32P, I32P, I32P],
+    "dbl_store_stats": [VP, I64P],
+    "dbl_table_create": [C.c_int, C.c_int, C.c_int64, I32P, F64P, F64P, C.c_int, C.POINTER(VP)],
+    "dbl_transformer_create": [C.POINTER(TransformerConfig), C.c_int, VP, C.POINTER(VP)],
+    "dbl_model_destroy": [VP],
+    "dbl_model_vocab": [VP, C.POINTER(C.c_int)],
+    "dbl_model_weight_bytes": [VP, I64P],
+    "dbl_forward_argmax": [VP, I32P, C.c_int, I32P, C.c_int, I32P],
+    "dbl_forward_logits": [VP, I32P, C.c_int, I32P, C.c_int, F32P],
+    "dbl_transformer_get_weight": [VP, C.c_char_p, C.c_int, U16P, C.c_int64],
+    "dbl_run": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), I32P, C.c_int,
+                C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
+    "dbl_run_ar": [VP, I32P, C.c_int, C.c_int, C.c_double, I32P, C.c_int, C.POINTER(C.c_int),
+                   C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
+    "dbl_run_serial_sd": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), C.c_int,
+                          I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p,
+                          C.c_int64, I64P],
+}
+_RESTYPE = {"dbl_last_error": C.c_char_p}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdouble_b200.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing — run `python -m paper_2601_05524_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, args in PROTOTYPES.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _RESTYPE.get(name, C.c_int)
+        _lib = L
+    return _lib
+
+
+class DoubleError(RuntimeError):
+    status = RUNTIME_ERROR
+
+
+class InvalidArgument(DoubleError, ValueError):  # std::invalid_argument
+    status = INVALID_ARGUMENT
+
+
+class LogicError(DoubleError):  # std::logic_error
+    status = LOGIC_ERROR
+
+
+class CudaError(DoubleError):
+    status = CUDA_ERROR
+
+
+_EXC = {INVALID_ARGUMENT: InvalidArgument, RUNTIME_ERROR: DoubleError, LOGIC_ERROR: LogicError,
+        CUDA_ERROR: CudaError, NCCL_ERROR: DoubleError}
+
+
+def check(status: int):
+    if status != OK:
+        msg = lib().dbl_last_error().decode(errors="replace")
+        raise _EXC.get(status, DoubleError)(msg)

@@ -1,0 +1,277 @@
+// The extern "C" boundary (include/double_b200.h): status codes + thread-local last error; the
+// C++ exceptions of the engine never cross it.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "decoder.cuh"
+#include "store.cuh"
+#include "table_model.cuh"
+#include "transformer.cuh"
+
+struct dbl_store_s {
+    std::unique_ptr<dbl::DeviceStore> impl;
+};
+struct dbl_model_s {
+    std::unique_ptr<dbl::Model> impl;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return DBL_OK;
+    } catch (const dbl::Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("out of memory: ") + e.what();
+        return DBL_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return DBL_RUNTIME_ERROR;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) dbl::throw_invalid(std::string("null ") + what);
+}
+
+int copy_run(const dbl::RunOutput& r, int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics,
+             char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len) {
+    if (static_cast<int>(r.output.size()) > cap) dbl::throw_invalid("output buffer too small");
+    if (out && !r.output.empty()) std::memcpy(out, r.output.data(), r.output.size() * 4);
+    if (n_out) *n_out = static_cast<int>(r.output.size());
+    if (metrics) *metrics = r.metrics;
+    if (jsonl || jsonl_len) {
+        const std::string js = dbl::traces_to_jsonl(r.traces);
+        if (jsonl_len) *jsonl_len = static_cast<int64_t>(js.size());
+        if (jsonl) {
+            if (static_cast<int64_t>(js.size()) + 1 > jsonl_cap) dbl::throw_invalid("jsonl buffer too small");
+            std::memcpy(jsonl, js.c_str(), js.size() + 1);
+        }
+    }
+    return 0;
+}
+}  // namespace
+
+namespace dbl {
+void require_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        throw Error(DBL_CUDA_ERROR, "no CUDA device visible (libdouble_b200 has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) throw Error(DBL_INVALID_ARGUMENT, "device index out of range");
+    cudaDeviceProp p{};
+    CUDA_CHECK(cudaGetDeviceProperties(&p, device));
+    if (p.major != 10) throw Error(DBL_CUDA_ERROR, "libdouble_b200 is built for sm_100a (B200) only");
+}
+}  // namespace dbl
+
+extern "C" {
+
+const char* dbl_last_error(void) { return g_last_error.c_str(); }
+int dbl_version(void) { return 1; }
+int dbl_device_ok(void) {
+    try {
+        dbl::require_device(0);
+        return 1;
+    } catch (...) {
+        return 0;
+    }
+}
+
+// ------------------------------------------------------------------------------- datastore
+int dbl_store_create(int max_order, int depth, int device, dbl_store_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        auto* s = new dbl_store_s;
+        try {
+            s->impl = std::make_unique<dbl::DeviceStore>(max_order, depth, device);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+int dbl_store_destroy(dbl_store_t s) {
+    return guarded([&] { delete s; });
+}
+int dbl_store_set_rejected_enabled(dbl_store_t s, int enabled) {
+    return guarded([&] { need(s, "store"); s->impl->set_rejected_enabled(enabled != 0, 0); });
+}
+int dbl_store_set_layer_order(dbl_store_t s, int layer, int max_order) {
+    return guarded([&] { need(s, "store"); s->impl->set_layer_order(layer, max_order, 0); });
+}
+int dbl_store_insert(dbl_store_t s, int layer, const int32_t* tokens, int n, int64_t step) {
+    return guarded([&] {
+        need(s, "store");
+        if (n > 0) need(tokens, "tokens");
+        s->impl->insert(layer, tokens, n, step, 0);
+    });
+}
+int dbl_store_record(dbl_store_t s, int layer, const int32_t* tokens, int n) {
+    return guarded([&] {
+        need(s, "store");
+        if (layer != DBL_LAYER_DYNAMIC && layer != DBL_LAYER_REJECTED)
+            dbl::throw_invalid("record: layer must be dynamic or rejected");
+        if (n > 0) need(tokens, "tokens");
+        s->impl->record(layer, tokens, n, 0);
+    });
+}
+int dbl_store_flush_session(dbl_store_t s) {
+    return guarded([&] { need(s, "store"); s->impl->flush_session(0); });
+}
+int dbl_store_clear_layer(dbl_store_t s, int layer) {
+    return guarded([&] { need(s, "store"); s->impl->clear_layer(layer, 0); });
+}
+int dbl_store_get_step(dbl_store_t s, int64_t* step) {
+    return guarded([&] { need(s, "store"); need(step, "step"); *step = s->impl->step(); });
+}
+int dbl_store_set_step(dbl_store_t s, int64_t step) {
+    return guarded([&] { need(s, "store"); s->impl->set_step(step); });
+}
+int dbl_store_layer_info(dbl_store_t s, int layer, int64_t* n_seqs, int64_t* n_tokens, int64_t* occ) {
+    return guarded([&] { need(s, "store"); s->impl->layer_info(layer, n_seqs, n_tokens, occ); });
+}
+int dbl_store_layer_read(dbl_store_t s, int layer, int32_t* tokens, int64_t tok_cap, int32_t* seq_lens,
+                         int64_t* steps, int64_t seq_cap) {
+    return guarded([&] {
+        need(s, "store");
+        s->impl->layer_read(layer, tokens, tok_cap, seq_lens, steps, seq_cap, 0);
+    });
+}
+int dbl_store_lookup(dbl_store_t s, const int32_t* ctx, int L, int d, int32_t* cands, int cap,
+                     int* n_cands, int* source, int* matched_order) {
+    return guarded([&] {
+        need(s, "store");
+        if (L <= 0) dbl::throw_invalid("lookup: empty context");
+        need(ctx, "ctx");
+        const int dcap = std::max(d, 1);
+        std::vector<int32_t> c(dcap);
+        const int64_t off[2] = {0, L};
+        int32_t n = 0, src = 0, ord = 0;
+        s->impl->lookup_batch(1, off, ctx, &d, dcap, c.data(), &n, &src, &ord, 0);
+        if (n > cap) dbl::throw_invalid("candidate buffer too small");
+        if (n) std::memcpy(cands, c.data(), n * 4);
+        if (n_cands) *n_cands = n;
+        if (source) *source = src;
+        if (matched_order) *matched_order = ord;
+    });
+}
+int dbl_store_lookup_batch(dbl_store_t s, int n_q, const int64_t* q_offsets, const int32_t* q_tokens,
+                           const int32_t* depths, int d_cap, int32_t* out_cands, int32_t* out_n,
+                           int32_t* out_source, int32_t* out_order) {
+    return guarded([&] {
+        need(s, "store");
+        s->impl->lookup_batch(n_q, q_offsets, q_tokens, depths, d_cap, out_cands, out_n, out_source,
+                              out_order, 0);
+    });
+}
+int dbl_store_stats(dbl_store_t s, int64_t out[6]) {
+    return guarded([&] { need(s, "store"); s->impl->stats(out, 0); });
+}
+
+// ---------------------------------------------------------------------------------- models
+int dbl_table_create(int order, int vocab, int64_t n_rows, const int32_t* windows, const double* probs,
+                     const double* fallback, int device, dbl_model_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        need(fallback, "fallback");
+        if (n_rows > 0) { need(windows, "windows"); need(probs, "probs"); }
+        auto m = std::make_unique<dbl_model_s>();
+        m->impl = std::make_unique<dbl::TableModel>(order, vocab, n_rows, windows, probs, fallback, device);
+        *out = m.release();
+    });
+}
+int dbl_transformer_create(const dbl_transformer_config* cfg, int device, void* nccl_comm, dbl_model_t* out) {
+    return guarded([&] {
+        need(cfg, "config");
+        need(out, "out");
+        auto m = std::make_unique<dbl_model_s>();
+        m->impl = std::make_unique<dbl::Transformer>(*cfg, device, nccl_comm);
+        *out = m.release();
+    });
+}
+int dbl_model_destroy(dbl_model_t m) {
+    return guarded([&] { delete m; });
+}
+int dbl_model_vocab(dbl_model_t m, int* vocab) {
+    return guarded([&] { need(m, "model"); need(vocab, "vocab"); *vocab = m->impl->vocab(); });
+}
+int dbl_model_weight_bytes(dbl_model_t m, int64_t* bytes) {
+    return guarded([&] { need(m, "model"); need(bytes, "bytes"); *bytes = m->impl->weight_bytes(); });
+}
+int dbl_forward_argmax(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, int32_t* out) {
+    return guarded([&] {
+        need(m, "model");
+        need(out, "out");
+        dbl::forward_stateless(*m->impl, ctx, L, cands, c, out, nullptr);
+    });
+}
+int dbl_forward_logits(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, float* out) {
+    return guarded([&] {
+        need(m, "model");
+        need(out, "out");
+        std::vector<int32_t> am(c + 1);
+        dbl::forward_stateless(*m->impl, ctx, L, cands, c, am.data(), out);
+    });
+}
+int dbl_transformer_get_weight(dbl_model_t m, const char* name, int layer, uint16_t* out, int64_t numel) {
+    return guarded([&] {
+        need(m, "model");
+        need(name, "name");
+        auto* t = dynamic_cast<dbl::Transformer*>(m->impl.get());
+        if (!t) dbl::throw_invalid("not a transformer model");
+        t->get_weight(name, layer, out, numel);
+    });
+}
+
+// ------------------------------------------------------------------------------ decode loop
+int dbl_run(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt, int n_prompt,
+            int max_new, const dbl_pipeline_options* opts, int32_t* out, int cap, int* n_out,
+            dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len) {
+    return guarded([&] {
+        need(draft, "draft");
+        need(target, "target");
+        need(store, "store");
+        need(opts, "options");
+        if (n_prompt > 0) need(prompt, "prompt");
+        const dbl::RunOutput r = dbl::run_double(*draft->impl, *target->impl, *store->impl, prompt,
+                                                 n_prompt, max_new, *opts);
+        copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
+               int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
+               int64_t jsonl_cap, int64_t* jsonl_len) {
+    return guarded([&] {
+        need(target, "target");
+        if (n_prompt > 0) need(prompt, "prompt");
+        const dbl::RunOutput r = dbl::run_ar(*target->impl, prompt, n_prompt, max_new, t_target);
+        copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
+                      int n_prompt, int max_new, const dbl_pipeline_options* opts, int use_retrieval,
+                      int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
+                      int64_t jsonl_cap, int64_t* jsonl_len) {
+    return guarded([&] {
+        need(draft, "draft");
+        need(target, "target");
+        need(store, "store");
+        need(opts, "options");
+        if (n_prompt > 0) need(prompt, "prompt");
+        const dbl::RunOutput r = dbl::run_serial_sd(*draft->impl, *target->impl, *store->impl, prompt,
+                                                    n_prompt, max_new, *opts, use_retrieval != 0);
+        copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Shared host/device plumbing for libdouble_b200: status/exception mapping, CUDA checks, small
+// device helpers.  Host code throws dbl::Error (carrying a dbl_status); the C-ABI boundary in
+// capi.cu converts it to a status + thread-local message.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "double_b200.h"
+
+namespace dbl {
+
+struct Error : std::runtime_error {
+    dbl_status status;
+    Error(dbl_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void throw_invalid(const std::string& m) { throw Error(DBL_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void throw_runtime(const std::string& m) { throw Error(DBL_RUNTIME_ERROR, m); }
+[[noreturn]] inline void throw_logic(const std::string& m) { throw Error(DBL_LOGIC_ERROR, m); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        throw Error(DBL_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file +
+                                        ":" + std::to_string(line) + ")");
+    }
+}
+#define CUDA_CHECK(x) ::dbl::cuda_check((x), #x, __FILE__, __LINE__)
+#define CUDA_LAUNCH_CHECK() ::dbl::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// RAII device buffer
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void zero(cudaStream_t s = 0) { if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// RAII pinned host buffer
+template <class T>
+struct PinBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    PinBuf() = default;
+    explicit PinBuf(size_t count) { alloc(count); }
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    ~PinBuf() { if (p) cudaFreeHost(p); }
+    void alloc(size_t count) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        if (count) CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&p), count * sizeof(T),
+                                            cudaHostAllocMapped | cudaHostAllocPortable));
+        n = count;
+    }
+    T* dev() const {  // device alias of the mapped pinned allocation
+        void* d = nullptr;
+        CUDA_CHECK(cudaHostGetDevicePointer(&d, p, 0));
+        return static_cast<T*>(d);
+    }
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CUDA_CHECK(cudaGetDevice(&prev));
+        if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+void require_device(int device);  // throws DBL_CUDA_ERROR unless an sm_100 device is usable
+
+constexpr int kMaxOrder = 8;      // datastore n-gram order bound (reference default N = 3)
+
+}  // namespace dbl

@@ -1,0 +1,721 @@
+// The DOUBLE decode loop, B200 edition.
+//
+// Per round (run_round, pipeline.cpp:223-262) the draft and target lanes run concurrently on two
+// CUDA streams over the same frozen datastore snapshot (the reference's Engine::Concurrent contract,
+// pipeline.cpp:239-261):
+//   draft stream : gamma x [lookup -> draft forward -> accept]  (no host round trip inside the chain)
+//   target stream: lookup -> ONE verify forward over committed[kv..] ⊕ spec ⊕ cands -> accept/pre-verify
+// Both write their results into mapped pinned memory; the host joins, applies finish_round
+// (pipeline.cpp:91-206) exactly as the reference, enqueues the <= 3 datastore appends and the lane
+// cursor updates, and starts the next round.  KV "rollback" is a length update: kv_len := LCP of what
+// the device processed and the new committed ⊕ speculative context.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "accept.cuh"
+#include "decoder.cuh"
+
+namespace dbl {
+
+// ------------------------------------------------------------------------------------ Lane
+namespace {
+__global__ void set_lane_state_kernel(LaneState* st, int L, int c, int kv, int row0) {
+    st->L = L;
+    st->c = c;
+    st->kv_len = kv;
+    st->row0 = row0;
+    st->src = DBL_SRC_MISS;
+    st->order = 0;
+    st->start = min(kv, row0);
+}
+}  // namespace
+
+Lane::Lane(Model& m, int cap) : model(m), capacity(cap) {
+    DeviceGuard g(m.device());
+    buf.alloc(cap);
+    argmax.alloc(cap);
+    buf.zero();
+    CUDA_CHECK(cudaMalloc(&state, sizeof(LaneState)));
+    CUDA_CHECK(cudaMemset(state, 0, sizeof(LaneState)));
+    cache = m.make_cache(cap);
+}
+Lane::~Lane() {
+    if (state) cudaFree(state);
+}
+void Lane::set_state(int L, int c, int kv, int row0, cudaStream_t s) {
+    set_lane_state_kernel<<<1, 1, 0, s>>>(state, L, c, kv, row0);
+    CUDA_LAUNCH_CHECK();
+}
+
+namespace {
+
+// pinned mirror used to upload lane tokens: stage[pos] == token at pos
+struct LaneIO {
+    Lane* lane;
+    PinBuf<int32_t> stage;
+    explicit LaneIO(Lane* l) : lane(l), stage(l->capacity) {}
+    // make the device buffer hold X in [0, |X|) given the mirror; returns the LCP
+    int sync_tokens(const std::vector<int32_t>& X, cudaStream_t s) {
+        if (static_cast<int>(X.size()) > lane->capacity) throw_runtime("lane capacity exceeded");
+        const auto& mi = lane->mirror;
+        size_t l = 0;
+        const size_t lim = std::min(mi.size(), X.size());
+        while (l < lim && mi[l] == X[l]) ++l;
+        if (l < X.size()) {
+            std::memcpy(stage.p + l, X.data() + l, (X.size() - l) * 4);
+            CUDA_CHECK(cudaMemcpyAsync(lane->buf.p + l, stage.p + l, (X.size() - l) * 4,
+                                       cudaMemcpyHostToDevice, s));
+        }
+        lane->mirror = X;
+        return static_cast<int>(l);
+    }
+};
+
+constexpr int kPrefillChunk = 256;
+
+// advance the lane's KV to `upto` (positions [kv_len, upto) processed), in forward-sized chunks
+void catch_up(Lane& lane, int upto, cudaStream_t s) {
+    if (!lane.model.has_kv()) return;
+    const int chunk = std::min(kPrefillChunk, lane.model.max_forward_tokens());
+    while (lane.kv_len < upto) {
+        const int end = std::min(upto, lane.kv_len + chunk);
+        // process [kv_len, end): L = end, c = 0, row0 = end - 1 >= kv_len
+        lane.set_state(end, 0, lane.kv_len, end - 1, s);
+        lane.model.forward(lane, end - lane.kv_len, s);
+        lane.kv_len = end;
+    }
+}
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timer() {
+        CUDA_CHECK(cudaEventCreate(&a));
+        CUDA_CHECK(cudaEventCreate(&b));
+    }
+    ~Timer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+    float ms() const {
+        float m = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&m, a, b));
+        return m;
+    }
+};
+
+struct Streams {
+    cudaStream_t main = nullptr, draft = nullptr, target = nullptr;
+    cudaEvent_t ready = nullptr, tf0 = nullptr, tf1 = nullptr;
+    Streams() {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&draft, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaStreamCreateWithFlags(&target, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreate(&tf0));
+        CUDA_CHECK(cudaEventCreate(&tf1));
+    }
+    ~Streams() {
+        cudaStreamSynchronize(main);
+        cudaStreamSynchronize(draft);
+        cudaStreamSynchronize(target);
+        cudaStreamDestroy(main);
+        cudaStreamDestroy(draft);
+        cudaStreamDestroy(target);
+        cudaEventDestroy(ready);
+        cudaEventDestroy(tf0);
+        cudaEventDestroy(tf1);
+    }
+    void fork() {  // lanes start after everything enqueued on main
+        CUDA_CHECK(cudaEventRecord(ready, main));
+        CUDA_CHECK(cudaStreamWaitEvent(draft, ready, 0));
+        CUDA_CHECK(cudaStreamWaitEvent(target, ready, 0));
+    }
+};
+
+const char* source_name(int s) {  // to_string(LookupSource), datastore.cpp:33-42
+    static const char* n[] = {"prior", "dynamic", "rejected", "context", "miss"};
+    return (s >= 0 && s <= 4) ? n[s] : "?";
+}
+
+void validate_opts(const dbl_pipeline_options& o) {  // pipeline.cpp:267-272, pipeline.hpp:24-28
+    if (o.gamma < 1) throw_invalid("gamma must be >= 1");
+    if (o.depth < 1) throw_invalid("depth must be >= 1");
+    if (o.depth > 65535) throw_invalid("depth must be <= 65535");
+    if (o.gamma > kMaxSegs) throw_invalid("gamma exceeds the device chain record");
+    if (o.t_target < 0.0 || o.t_draft <= 0.0 || o.t_lookup < 0.0 || o.t_sync < 0.0)
+        throw_invalid("latency values out of range");
+}
+
+// record_accepted_run / record_rejected_run (pipeline.cpp:72-89)
+void record_run(DeviceStore& st, int layer, const std::vector<int32_t>& before, const int32_t* add,
+                size_t na, cudaStream_t s) {
+    if (na == 0) return;
+    const size_t pre = std::min<size_t>(layer == 1 ? static_cast<size_t>(st.max_order()) - 1 : 3,
+                                        before.size());
+    std::vector<int32_t> rec(before.end() - static_cast<long>(pre), before.end());
+    rec.insert(rec.end(), add, add + na);
+    st.record(layer, rec.data(), static_cast<int>(rec.size()), s);
+}
+
+void device_counts(DeviceStore& st, cudaStream_t s, long* lookups, long* hits) {
+    int64_t v[6];
+    st.stats(v, s);
+    *lookups = v[0];
+    *hits = v[1] + v[2] + v[3] + v[4];
+}
+
+void finish_output(const std::vector<int32_t>& committed, size_t n_prompt, int max_new,
+                   RunOutput& r) {
+    r.output.assign(committed.begin() + static_cast<long>(n_prompt), committed.end());
+    if (r.output.size() > static_cast<size_t>(max_new)) r.output.resize(max_new);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ metrics / jsonl
+void compute_metrics(const std::vector<Trace>& traces, double t_target, dbl_run_metrics* m) {
+    // compute_metrics, pipeline.cpp:325-371
+    long tokens = 0, cur = 0, matched_sum = 0, matched_n = 0, seg_total = 0, seg_n = 0;
+    double clock = 0.0;
+    for (const Trace& t : traces) {
+        tokens += t.committed_count;
+        clock += t.clock_delta;
+        if (t.pending_reject) {
+            seg_total += cur + t.accepted_pending;
+            ++seg_n;
+            cur = t.committed_count - t.accepted_pending;
+        } else if (t.rejected) {
+            seg_total += cur + t.committed_count;
+            ++seg_n;
+            cur = 0;
+        } else {
+            cur += t.committed_count;
+        }
+        for (int v : t.draft_matched) { matched_sum += v; ++matched_n; }
+        if (t.target_matched >= 0) { matched_sum += t.target_matched; ++matched_n; }
+    }
+    if (cur > 0) { seg_total += cur; ++seg_n; }
+    m->tokens = tokens;
+    m->rounds = static_cast<int64_t>(traces.size());
+    m->clock = clock;
+    m->m = seg_n ? static_cast<double>(seg_total) / static_cast<double>(seg_n) : 0.0;
+    m->amt = matched_n ? static_cast<double>(matched_sum) / static_cast<double>(matched_n) : 0.0;
+    m->speedup = clock > 0.0 ? static_cast<double>(tokens) * t_target / clock : 0.0;
+    m->hit_rate = 0.0;
+    m->lookups = 0;
+}
+
+namespace {
+// nlohmann::json's double rendering (shortest round-trip digits; fixed notation for decimal
+// exponents in (-4, 15], else d.ddde+XX; always a '.' or 'e')
+std::string json_double(double x) {
+    if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
+    char tmp[64];
+    int prec = 1;
+    for (; prec <= 17; ++prec) {
+        std::snprintf(tmp, sizeof tmp, "%.*e", prec - 1, x);
+        if (std::strtod(tmp, nullptr) == x) break;
+    }
+    std::string s(tmp);
+    bool neg = false;
+    size_t i = 0;
+    if (s[0] == '-') { neg = true; i = 1; }
+    std::string digits;
+    for (; i < s.size() && s[i] != 'e'; ++i)
+        if (s[i] != '.') digits += s[i];
+    const int e10 = std::atoi(s.c_str() + i + 1);
+    while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+    const int k = static_cast<int>(digits.size()), n = e10 + 1;
+    std::string out = neg ? "-" : "";
+    if (k <= n && n <= 15) {
+        out += digits + std::string(n - k, '0') + ".0";
+    } else if (0 < n && n <= 15) {
+        out += digits.substr(0, n) + "." + digits.substr(n);
+    } else if (-4 < n && n <= 0) {
+        out += "0." + std::string(-n, '0') + digits;
+    } else {
+        out += digits.substr(0, 1);
+        if (k > 1) out += "." + digits.substr(1);
+        const int e = n - 1;
+        char eb[16];
+        std::snprintf(eb, sizeof eb, "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+        out += eb;
+    }
+    return out;
+}
+}  // namespace
+
+std::string traces_to_jsonl(const std::vector<Trace>& traces) {  // pipeline.cpp:373-394
+    std::string out;
+    for (const Trace& t : traces) {
+        out += "{\"round\":" + std::to_string(t.round);
+        out += ",\"mode\":\"" + t.mode + "\"";
+        out += ",\"pending\":" + std::to_string(t.pending);
+        out += ",\"draft_len\":" + std::to_string(t.draft_len);
+        out += ",\"draft_matched\":[";
+        for (size_t k = 0; k < t.draft_matched.size(); ++k) {
+            if (k) out += ",";
+            out += std::to_string(t.draft_matched[k]);
+        }
+        out += "],\"target_matched\":" + std::to_string(t.target_matched);
+        out += ",\"target_source\":\"" + t.target_source + "\"";
+        out += ",\"accepted_pending\":" + std::to_string(t.accepted_pending);
+        out += std::string(",\"pending_reject\":") + (t.pending_reject ? "true" : "false");
+        out += std::string(",\"rejected\":") + (t.rejected ? "true" : "false");
+        out += ",\"committed\":" + std::to_string(t.committed_count);
+        out += ",\"kind\":\"" + t.kind + "\"";
+        out += ",\"clock_delta\":" + json_double(t.clock_delta) + "}\n";
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------------------- run (DOUBLE)
+RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* prompt, int n_prompt,
+                     int max_new, const dbl_pipeline_options& o) {
+    if (max_new < 1) throw_invalid("max_new_tokens must be >= 1");
+    if (n_prompt <= 0) throw_invalid("prompt must be nonempty");
+    validate_opts(o);
+    if (dm.device() != st.device() || tm.device() != st.device())
+        throw_invalid("draft, target and datastore must live on the same device");
+    DeviceGuard g(st.device());
+    const int d = o.depth, gamma = o.gamma;
+    const int cap = n_prompt + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
+    Streams S;
+    Lane dl(dm, cap), tl(tm, cap);
+    LaneIO dio(&dl), tio(&tl);
+    PinBuf<RoundResult> rr_buf(1);
+    RoundResult* rr = rr_buf.p;
+    RoundResult* rr_dev = rr_buf.dev();
+
+    long base_lookups, base_hits;
+    device_counts(st, S.main, &base_lookups, &base_hits);
+
+    std::vector<int32_t> committed(prompt, prompt + n_prompt), spec;
+    int mode = 0, prev_tokens = gamma;  // PipelineState, pipeline.hpp:46-55
+    long round = 0, last_committed_len = n_prompt;
+    st.record(1, prompt, n_prompt, S.main);  // store.record_accepted(prompt), pipeline.cpp:282
+
+    // lanes hold the prompt; transformers prefill KV for positions [0, P-1)
+    dio.sync_tokens(committed, S.main);
+    tio.sync_tokens(committed, S.main);
+    Timer pre;
+    CUDA_CHECK(cudaEventRecord(pre.a, S.main));
+    S.fork();
+    catch_up(dl, n_prompt - 1, S.draft);
+    catch_up(tl, n_prompt - 1, S.target);
+    CUDA_CHECK(cudaEventRecord(S.ready, S.draft));
+    CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
+    CUDA_CHECK(cudaEventRecord(S.ready, S.target));
+    CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
+    CUDA_CHECK(cudaEventRecord(pre.b, S.main));
+    dl.set_state(n_prompt, 0, dl.kv_len, n_prompt - 1, S.main);
+    tl.set_state(n_prompt, 0, tl.kv_len, n_prompt - 1, S.main);
+
+    RunOutput res;
+    Timer loop;
+    CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    double tfwd_ms = 0.0;
+    int64_t tfwd_n = 0, trows = 0;
+    const int32_t eos = tm.vocab() - 1;
+    size_t scanned = n_prompt;
+    bool done = false;
+    while (!done) {
+        // check_state, pipeline.cpp:208-219
+        if (mode == 0 && !spec.empty()) throw_logic("pre-verify mode with a speculative tail");
+        if (mode == 1 && prev_tokens != static_cast<int>(spec.size()))
+            throw_logic("prev_tokens out of sync with speculative tail");
+        const int nc = static_cast<int>(committed.size()), ns = static_cast<int>(spec.size());
+        const int L = nc + ns;
+        rr->draft_L0 = L;
+        rr->draft_L = L;
+        rr->n_segs = 0;
+        rr->draft_error = rr->target_error = 0;
+        S.fork();
+        // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
+        for (int j = 0; j < gamma; ++j) {
+            if (o.draft_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.draft);
+            const int c_max = o.draft_retrieval ? d : 0;
+            const int bound = j == 0 ? L + c_max - std::min(dl.kv_len, L - 1) : 1 + c_max;
+            dm.forward(dl, bound, S.draft);
+            launch_draft_accept(dl, rr_dev, j, S.draft);
+        }
+        // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
+        if (o.target_retrieval) st.lookup_lane(tl.buf.p, tl.state, d, S.target);
+        CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
+        const int tc_max = o.target_retrieval ? d : 0;
+        tm.forward(tl, L + tc_max - std::min(tl.kv_len, nc - 1), S.target);
+        CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
+        launch_target_accept(tl, nc, rr_dev, S.target);
+        CUDA_CHECK(cudaStreamSynchronize(S.draft));
+        CUDA_CHECK(cudaStreamSynchronize(S.target));
+        {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, S.tf0, S.tf1));
+            tfwd_ms += ms;
+            ++tfwd_n;
+        }
+        if (rr->draft_error == 2) throw_runtime("draft chain exceeds the round record");
+        if (rr->draft_error || rr->target_error) throw_runtime("degenerate distribution");
+        const int c_t = rr->ext_c;
+        trows += L + c_t - (nc - 1);
+
+        // ---- finish_round (pipeline.cpp:91-206)
+        const int n_chain = rr->draft_L - rr->draft_L0;
+        const int32_t* chain = rr->draft_tokens;
+        const int ne = rr->ext_matched + 1;
+        const int32_t* ext = rr->ext_emitted;
+        Trace tr;
+        tr.round = round;
+        tr.mode = mode ? "post_verify" : "pre_verify";
+        tr.pending = ns;
+        tr.draft_len = n_chain;
+        if (o.draft_retrieval)
+            for (int j = 0; j < rr->n_segs; ++j) tr.draft_matched.push_back(rr->segs[j].matched);
+        tr.target_matched = o.target_retrieval ? rr->ext_matched : -1;
+        tr.target_source = source_name(rr->ext_source);
+
+        const std::vector<int32_t> committed_before = committed;
+        std::vector<int32_t> add, new_spec;
+        if (rr->tgt_rej >= 0) {
+            const int k = rr->tgt_rej;
+            tr.accepted_pending = k;
+            tr.pending_reject = tr.rejected = true;
+            tr.kind = "pending_reject";
+            add.assign(spec.begin(), spec.begin() + k);
+            add.push_back(rr->tgt_correction);
+            std::vector<int32_t> pre_k = committed_before;
+            pre_k.insert(pre_k.end(), spec.begin(), spec.begin() + k);
+            record_run(st, 2, pre_k, spec.data() + k, spec.size() - k, S.main);
+            std::vector<int32_t> pre_d = committed_before;
+            pre_d.insert(pre_d.end(), spec.begin(), spec.end());
+            record_run(st, 2, pre_d, chain, n_chain, S.main);
+        } else {
+            tr.accepted_pending = ns;
+            add = spec;
+            add.insert(add.end(), ext, ext + ne);
+            const int cmp = std::min(n_chain, ne);
+            int j = 0;
+            while (j < cmp && chain[j] == ext[j]) ++j;
+            if (j == ne && n_chain > ne) {
+                tr.kind = "extend_keep_draft";
+                new_spec.assign(chain + ne, chain + n_chain);
+            } else if (j == cmp) {
+                tr.kind = "extend_draft_subsumed";
+            } else {
+                tr.kind = "extend_drop_draft";
+                tr.rejected = true;
+                std::vector<int32_t> pre_j = committed_before;
+                pre_j.insert(pre_j.end(), spec.begin(), spec.end());
+                pre_j.insert(pre_j.end(), chain, chain + j);
+                record_run(st, 2, pre_j, chain + j, n_chain - j, S.main);
+            }
+        }
+        tr.committed_count = static_cast<int>(add.size());
+        record_run(st, 1, committed_before, add.data(), add.size(), S.main);
+        committed.insert(committed.end(), add.begin(), add.end());
+        // rollback(state, |committed|) (pipeline.cpp:15-30)
+        if (static_cast<long>(committed.size()) < last_committed_len)
+            throw_logic("rollback: keep_len below committed boundary");
+        spec = std::move(new_spec);
+        mode = spec.empty() ? 0 : 1;
+        prev_tokens = spec.empty() ? gamma : static_cast<int>(spec.size());
+        last_committed_len = static_cast<long>(committed.size());
+        ++round;
+        const double draft_time = gamma * (o.t_draft + (o.draft_retrieval ? o.t_lookup : 0.0));
+        const double target_time = o.t_target + (o.target_retrieval ? o.t_lookup : 0.0);
+        tr.clock_delta = std::max(draft_time, target_time) + o.t_sync;
+        res.traces.push_back(std::move(tr));
+
+        // ---- lane cursors for the next round (KV commit by length)
+        std::vector<int32_t> X = committed;
+        X.insert(X.end(), spec.begin(), spec.end());
+        {
+            // the draft lane holds committed_before ⊕ spec ⊕ chain; KV valid below its last token
+            dl.mirror.resize(L);
+            dl.mirror.insert(dl.mirror.end(), chain, chain + n_chain);
+            const int dev_kv = L + n_chain - 1;
+            const int lcp = dio.sync_tokens(X, S.main);
+            dl.kv_len = std::min(dev_kv, lcp);
+            dl.set_state(static_cast<int>(X.size()), 0, dl.kv_len, static_cast<int>(X.size()) - 1, S.main);
+        }
+        {
+            tl.mirror.resize(L);
+            tl.mirror.insert(tl.mirror.end(), rr->ext_cands, rr->ext_cands + c_t);
+            const int dev_kv = L + c_t;
+            const int lcp = tio.sync_tokens(X, S.main);
+            tl.kv_len = std::min(dev_kv, lcp);
+            tl.set_state(static_cast<int>(X.size()), 0, tl.kv_len,
+                         static_cast<int>(committed.size()) - 1, S.main);
+        }
+
+        // ---- EOS / budget (pipeline.cpp:290-306)
+        for (; scanned < committed.size(); ++scanned) {
+            if (committed[scanned] == eos) {
+                committed.resize(scanned + 1);
+                done = true;
+                break;
+            }
+        }
+        if (committed.size() - static_cast<size_t>(n_prompt) >= static_cast<size_t>(max_new)) done = true;
+        if (round > 1000000) throw_runtime("round limit exceeded; pipeline stalled");
+    }
+    CUDA_CHECK(cudaEventRecord(loop.b, S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+
+    finish_output(committed, n_prompt, max_new, res);
+    compute_metrics(res.traces, o.t_target, &res.metrics);
+    long lk, hits;
+    device_counts(st, S.main, &lk, &hits);
+    res.metrics.lookups = lk - base_lookups;
+    res.metrics.hit_rate = res.metrics.lookups == 0
+                               ? 0.0
+                               : static_cast<double>(hits - base_hits) / static_cast<double>(res.metrics.lookups);
+    res.metrics.device_ms = loop.ms();
+    res.metrics.prefill_ms = pre.ms();
+    res.metrics.target_fwd_ms = tfwd_ms;
+    res.metrics.target_fwd_count = tfwd_n;
+    res.metrics.target_rows = trows;
+    st.flush_session(S.main);  // pipeline.cpp:321
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    return res;
+}
+
+// ----------------------------------------------------------------------------------- run (AR)
+namespace {
+__global__ void ar_append_kernel(const int32_t* __restrict__ argmax, int32_t* buf, LaneState* lane,
+                                 int32_t* out_host, int i) {
+    const int L = lane->L;
+    const int tok = argmax[L - 1];
+    buf[L] = tok;
+    out_host[i] = tok;
+    if (tok < 0) lane->error = 1;
+    lane->L = L + 1;
+    lane->c = 0;
+    lane->kv_len = L;
+    lane->row0 = L;
+}
+}  // namespace
+
+RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, double t_target) {
+    // run_vanilla_ar, harness.cpp:233-258 (greedy).  The device runs ahead in blocks of kBlock
+    // tokens between EOS checks; tokens past an EOS are discarded exactly as the reference never
+    // produces them.
+    if (n_prompt <= 0) throw_invalid("prompt must be nonempty");
+    if (max_new < 0) throw_invalid("max_new_tokens must be >= 0");
+    DeviceGuard g(tm.device());
+    constexpr int kBlock = 16;
+    const int cap = n_prompt + max_new + kBlock + 8;
+    Streams S;
+    Lane tl(tm, cap);
+    LaneIO tio(&tl);
+    PinBuf<int32_t> outp(std::max(max_new + kBlock, 1));
+    int32_t* out_dev = outp.dev();
+    std::vector<int32_t> ctx(prompt, prompt + n_prompt);
+    tio.sync_tokens(ctx, S.main);
+    Timer pre, loop;
+    CUDA_CHECK(cudaEventRecord(pre.a, S.main));
+    catch_up(tl, n_prompt - 1, S.main);
+    CUDA_CHECK(cudaEventRecord(pre.b, S.main));
+    tl.set_state(n_prompt, 0, tl.kv_len, n_prompt - 1, S.main);
+    CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    RunOutput res;
+    const int32_t eos = tm.vocab() - 1;
+    int produced = 0;
+    bool done = max_new == 0;
+    while (!done) {
+        const int n = std::min(kBlock, max_new - produced);
+        for (int i = 0; i < n; ++i) {
+            tm.forward(tl, 1, S.main);
+            ar_append_kernel<<<1, 1, 0, S.main>>>(tl.argmax.p, tl.buf.p, tl.state, out_dev, produced + i);
+            CUDA_LAUNCH_CHECK();
+        }
+        CUDA_CHECK(cudaStreamSynchronize(S.main));
+        for (int i = 0; i < n; ++i) {
+            const int32_t tok = outp.p[produced + i];
+            if (tok < 0) throw_runtime("degenerate distribution");
+            res.output.push_back(tok);
+            Trace t;
+            t.round = produced + i;
+            t.mode = "ar";
+            t.committed_count = 1;
+            t.kind = "ar_step";
+            t.clock_delta = t_target;
+            res.traces.push_back(std::move(t));
+            if (tok == eos) { done = true; break; }
+        }
+        produced += n;
+        if (produced >= max_new) done = true;
+    }
+    CUDA_CHECK(cudaEventRecord(loop.b, S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    compute_metrics(res.traces, t_target, &res.metrics);
+    res.metrics.clock = static_cast<double>(res.metrics.tokens) * t_target;  // harness.cpp:254-256
+    res.metrics.speedup = 1.0;
+    res.metrics.device_ms = loop.ms();
+    res.metrics.prefill_ms = pre.ms();
+    res.metrics.target_fwd_count = produced;
+    res.metrics.target_rows = produced;
+    return res;
+}
+
+// ---------------------------------------------------------------------------- run (serial SD)
+RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* prompt, int n_prompt,
+                        int max_new, const dbl_pipeline_options& o, bool use_retrieval) {
+    // run_serial_sd, harness.cpp:264-369 (greedy): draft chain over committed, one target forward
+    // over committed ⊕ chain, accept prefix + correction or all + bonus token.
+    if (n_prompt <= 0) throw_invalid("prompt must be nonempty");
+    validate_opts(o);
+    DeviceGuard g(st.device());
+    const int d = o.depth, gamma = o.gamma;
+    const int cap = n_prompt + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
+    Streams S;
+    Lane dl(dm, cap), tl(tm, cap);
+    LaneIO dio(&dl), tio(&tl);
+    PinBuf<RoundResult> rr_buf(1);
+    RoundResult* rr = rr_buf.p;
+    RoundResult* rr_dev = rr_buf.dev();
+    long base_lookups, base_hits;
+    device_counts(st, S.main, &base_lookups, &base_hits);
+    st.record(1, prompt, n_prompt, S.main);
+    std::vector<int32_t> committed(prompt, prompt + n_prompt);
+    dio.sync_tokens(committed, S.main);
+    tio.sync_tokens(committed, S.main);
+    catch_up(dl, n_prompt - 1, S.main);
+    catch_up(tl, n_prompt - 1, S.main);
+    RunOutput res;
+    Timer loop;
+    CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    const int32_t eos = tm.vocab() - 1;
+    long round = 0;
+    size_t scanned = n_prompt;
+    bool done = false;
+    while (!done) {
+        const int nc = static_cast<int>(committed.size());
+        dl.set_state(nc, 0, dl.kv_len, nc - 1, S.main);
+        rr->draft_L0 = rr->draft_L = nc;
+        rr->n_segs = 0;
+        rr->draft_error = rr->target_error = 0;
+        for (int j = 0; j < gamma; ++j) {
+            if (use_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.main);
+            const int c_max = use_retrieval ? d : 0;
+            dm.forward(dl, j == 0 ? nc + c_max - std::min(dl.kv_len, nc - 1) : 1 + c_max, S.main);
+            launch_draft_accept(dl, rr_dev, j, S.main);
+        }
+        CUDA_CHECK(cudaStreamSynchronize(S.main));
+        if (rr->draft_error) throw_runtime(rr->draft_error == 2 ? "draft chain too long" : "degenerate distribution");
+        const int n_chain = rr->draft_L - rr->draft_L0;
+        std::vector<int32_t> chain(rr->draft_tokens, rr->draft_tokens + n_chain);
+        // target lane: chain as the "speculative" tail, no candidates
+        std::vector<int32_t> X = committed;
+        X.insert(X.end(), chain.begin(), chain.end());
+        const int lcp = tio.sync_tokens(X, S.main);
+        tl.kv_len = std::min(tl.kv_len, lcp);
+        tl.set_state(nc + n_chain, 0, tl.kv_len, nc - 1, S.main);
+        tm.forward(tl, nc + n_chain - std::min(tl.kv_len, nc - 1), S.main);
+        launch_target_accept(tl, nc, rr_dev, S.main);
+        CUDA_CHECK(cudaStreamSynchronize(S.main));
+        if (rr->target_error) throw_runtime("degenerate distribution");
+        tl.kv_len = nc + n_chain;
+        dl.mirror.resize(nc);
+        dl.mirror.insert(dl.mirror.end(), chain.begin(), chain.end());
+        dl.kv_len = nc + n_chain - 1;  // set by the last draft_accept on the device
+
+        Trace t;
+        t.round = round;
+        t.mode = "serial";
+        t.draft_len = n_chain;
+        if (use_retrieval)
+            for (int j = 0; j < rr->n_segs; ++j) t.draft_matched.push_back(rr->segs[j].matched);
+        std::vector<int32_t> add;
+        if (rr->tgt_rej >= 0) {
+            const int k = rr->tgt_rej;
+            t.accepted_pending = k;
+            t.pending_reject = t.rejected = true;
+            t.kind = "reject";
+            add.assign(chain.begin(), chain.begin() + k);
+            add.push_back(rr->tgt_correction);
+            std::vector<int32_t> pre = committed;
+            pre.insert(pre.end(), chain.begin(), chain.begin() + k);
+            record_run(st, 2, pre, chain.data() + k, chain.size() - k, S.main);
+        } else {
+            t.accepted_pending = n_chain;
+            t.kind = "all_accepted";
+            add = chain;
+            add.push_back(rr->ext_emitted[0]);  // sample(dists.back()), greedy
+        }
+        t.committed_count = static_cast<int>(add.size());
+        t.clock_delta = gamma * (o.t_draft + (use_retrieval ? o.t_lookup : 0.0)) + o.t_target + o.t_sync;
+        record_run(st, 1, committed, add.data(), add.size(), S.main);
+        committed.insert(committed.end(), add.begin(), add.end());
+        res.traces.push_back(std::move(t));
+        ++round;
+        // both lanes now must hold `committed`
+        const int l1 = dio.sync_tokens(committed, S.main);
+        dl.kv_len = std::min(dl.kv_len, l1);
+        const int l2 = tio.sync_tokens(committed, S.main);
+        tl.kv_len = std::min(tl.kv_len, l2);
+        for (; scanned < committed.size(); ++scanned) {
+            if (committed[scanned] == eos) {
+                committed.resize(scanned + 1);
+                done = true;
+                break;
+            }
+        }
+        if (committed.size() - static_cast<size_t>(n_prompt) >= static_cast<size_t>(max_new)) done = true;
+        if (round > 1000000) throw_runtime("round limit exceeded; decoder stalled");
+    }
+    CUDA_CHECK(cudaEventRecord(loop.b, S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    finish_output(committed, n_prompt, max_new, res);
+    compute_metrics(res.traces, o.t_target, &res.metrics);
+    long lk, hits;
+    device_counts(st, S.main, &lk, &hits);
+    res.metrics.lookups = lk - base_lookups;
+    res.metrics.hit_rate = res.metrics.lookups == 0
+                               ? 0.0
+                               : static_cast<double>(hits - base_hits) / static_cast<double>(res.metrics.lookups);
+    res.metrics.device_ms = loop.ms();
+    return res;
+}
+
+// ------------------------------------------------------------------------ stateless forward
+namespace {
+__global__ void gather_rows_kernel(const int32_t* argmax, int from, int n, int32_t* out) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = argmax[from + i];
+}
+}  // namespace
+
+void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,
+                       int32_t* out_argmax, float* out_logits) {
+    if (L <= 0) throw_invalid("forward_batch: empty context");  // model.cpp:41
+    if (c < 0) throw_invalid("negative candidate count");
+    DeviceGuard g(m.device());
+    Streams S;
+    Lane lane(m, L + c + 16);
+    LaneIO io(&lane);
+    std::vector<int32_t> X(ctx, ctx + L);
+    X.insert(X.end(), cands, cands + c);
+    io.sync_tokens(X, S.main);
+    catch_up(lane, L - 1, S.main);
+    lane.set_state(L, c, lane.kv_len, L - 1, S.main);
+    DevBuf<float> lg;
+    if (out_logits) {
+        lg.alloc(static_cast<size_t>(c + 1) * m.vocab());
+        m.logits(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), lg.p, S.main);
+    } else {
+        m.forward(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), S.main);
+    }
+    DevBuf<int32_t> rows(c + 1);
+    gather_rows_kernel<<<1, 256, 0, S.main>>>(lane.argmax.p, L - 1, c + 1, rows.p);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaMemcpyAsync(out_argmax, rows.p, (c + 1) * 4, cudaMemcpyDeviceToHost, S.main));
+    if (out_logits)
+        CUDA_CHECK(cudaMemcpyAsync(out_logits, lg.p, lg.bytes(), cudaMemcpyDeviceToHost, S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    for (int i = 0; i <= c; ++i)
+        if (out_argmax[i] < 0) throw_runtime("degenerate distribution");
+}
+
+}  // namespace dbl

@@ -1,0 +1,45 @@
+// Host orchestrator of the device decode loop (replaces specpar::run / run_round / finish_round,
+// pipeline.cpp:15-323; run_vanilla_ar / run_serial_sd, harness.cpp:233-369).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "model.cuh"
+#include "store.cuh"
+
+namespace dbl {
+
+struct Trace {  // RoundTrace, pipeline.hpp:57-71
+    long round = 0;
+    std::string mode;
+    int pending = 0, draft_len = 0;
+    std::vector<int> draft_matched;
+    int target_matched = -1;
+    std::string target_source;
+    int accepted_pending = 0;
+    bool pending_reject = false, rejected = false;
+    int committed_count = 0;
+    std::string kind;
+    double clock_delta = 0.0;
+};
+
+struct RunOutput {
+    std::vector<int32_t> output;
+    std::vector<Trace> traces;
+    dbl_run_metrics metrics{};
+};
+
+std::string traces_to_jsonl(const std::vector<Trace>& traces);
+void compute_metrics(const std::vector<Trace>& traces, double t_target, dbl_run_metrics* m);
+
+RunOutput run_double(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
+                     int n_prompt, int max_new, const dbl_pipeline_options& o);
+RunOutput run_ar(Model& target, const int32_t* prompt, int n_prompt, int max_new, double t_target);
+RunOutput run_serial_sd(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
+                        int n_prompt, int max_new, const dbl_pipeline_options& o, bool use_retrieval);
+
+// forward_batch as a stateless call (fresh lane / KV): argmax rows (c+1) and optionally logits
+void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,
+                       int32_t* out_argmax, float* out_logits);
+
+}  // namespace dbl

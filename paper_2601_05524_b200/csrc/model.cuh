@@ -1,0 +1,56 @@
+// Device model interface shared by the table model (config 1) and the transformer (configs 2-5).
+// A model's forward reads a lane's token buffer and writes per-position argmax rows — the
+// forward_batch contract (model.cpp:37-53) with greedy consumption (argmax_token, model.cpp:70-81).
+#pragma once
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "lane.cuh"
+
+namespace dbl {
+
+// Per-(model, lane) mutable device state (KV cache for transformers; empty for tables).
+struct LaneCache {
+    virtual ~LaneCache() = default;
+};
+
+class Lane;
+
+class Model {
+  public:
+    virtual ~Model() = default;
+    virtual int device() const = 0;
+    virtual int vocab() const = 0;
+    virtual bool has_kv() const = 0;
+    virtual int64_t weight_bytes() const { return 0; }
+    virtual std::unique_ptr<LaneCache> make_cache(int capacity) = 0;
+    // Enqueue one forward on stream s: process positions [min(kv_len,row0), L+c) of the lane, write
+    // lane.argmax[p] for those positions and set lane.start / lane.kv_len = L+c.  `max_tokens` is a
+    // host-side upper bound of L+c-start (kernel shape bucket); the exact count is read on device.
+    virtual void forward(Lane& lane, int max_tokens, cudaStream_t s) = 0;
+    // Like forward, and also write fp32 logits (tables: probabilities) of rows [row0, L+c), in
+    // order, to out_dev ((L+c-row0) x vocab).
+    virtual void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) = 0;
+    virtual int max_forward_tokens() const { return 1 << 30; }
+    virtual std::string kind() const = 0;
+};
+
+// A model's working buffers for one decode role.
+class Lane {
+  public:
+    Lane(Model& m, int capacity);
+    ~Lane();
+    Model& model;
+    int capacity;                 // token capacity of buf / argmax
+    DevBuf<int32_t> buf, argmax;
+    LaneState* state = nullptr;   // device
+    std::unique_ptr<LaneCache> cache;
+    // host-side mirror (kept exact by the orchestrator)
+    std::vector<int32_t> mirror;  // tokens the device buffer holds in [0, mirror.size())
+    int kv_len = 0;               // host view of the valid KV prefix
+    void set_state(int L, int c, int kv, int row0, cudaStream_t s);
+};
+
+}  // namespace dbl

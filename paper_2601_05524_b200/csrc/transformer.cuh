@@ -1,0 +1,29 @@
+// Random-init bf16 decoder-only transformer on sm_100a (configs 2-5): see transformer.cu.
+#pragma once
+#include "model.cuh"
+
+namespace dbl {
+
+class Transformer final : public Model {
+  public:
+    Transformer(const dbl_transformer_config& cfg, int device, void* nccl_comm);
+    ~Transformer() override;
+    int device() const override { return device_; }
+    int vocab() const override { return cfg_.vocab; }
+    bool has_kv() const override { return true; }
+    int64_t weight_bytes() const override;
+    std::unique_ptr<LaneCache> make_cache(int capacity) override;
+    void forward(Lane& lane, int max_tokens, cudaStream_t s) override;
+    void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
+    int max_forward_tokens() const override;
+    std::string kind() const override { return "transformer"; }
+    void get_weight(const std::string& name, int layer, uint16_t* out, int64_t numel);
+
+  private:
+    struct Impl;
+    Impl* impl_ = nullptr;
+    dbl_transformer_config cfg_;
+    int device_;
+};
+
+}  // namespace dbl

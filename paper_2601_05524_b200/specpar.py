@@ -1,0 +1,425 @@
+"""Python mirror of the reference's ``specpar`` decode-path API (proj/include/specpar/*.hpp), backed by
+the B200 C-ABI (include/double_b200.h).  Same names, argument meaning and error types:
+
+=========================================  =====================================================
+reference (C++)                            here
+=========================================  =====================================================
+HierarchicalDatastore(n, d)                HierarchicalDatastore(n, d, device=0)
+  .prior/.dynamic/.rejected .insert(s, k)    .prior/.dynamic/.rejected .insert(s, k)
+  .lookup(ctx, d) -> LookupResult            .lookup(ctx, d) -> LookupResult
+  .record_accepted / .record_rejected        same
+  .flush_session(), .rejected_enabled        same; .stats -> LookupStats
+build_prior(corpora, N, K)                 build_prior(store, corpora, K)   (fills store.prior)
+TableModel + forward_batch / argmax_token  TableModel.from_model_v1(text) ; forward_batch(m, ctx, c)
+run(draft, target, store, prompt, n, opts) run(draft, target, store, prompt, n, opts)
+run_vanilla_ar / run_serial_sd (harness)   run_vanilla_ar / run_serial_sd
+=========================================  =====================================================
+
+std::invalid_argument -> InvalidArgument (a ValueError), std::runtime_error -> DoubleError,
+std::logic_error -> LogicError.  Nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._capi import (DoubleError, InvalidArgument, LogicError, PipelineOptions as _Opts, RunMetrics,
+                    TransformerConfig, check, lib)
+
+SOURCES = ["prior", "dynamic", "rejected", "context", "miss"]
+PRIOR, DYNAMIC, REJECTED = 0, 1, 2
+
+__all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer",
+           "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "run", "run_vanilla_ar",
+           "run_serial_sd", "build_prior", "DoubleError", "InvalidArgument", "LogicError",
+           "parse_model_v1", "parse_dstore_v1"]
+
+
+def _i32(xs) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(list(xs) if not isinstance(xs, np.ndarray) else xs,
+                                           dtype=np.int32).reshape(-1))
+
+
+def _p32(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+@dataclass
+class LookupResult:  # datastore.hpp:33-37
+    candidates: list
+    source: str = "miss"
+    matched_order: int = 0
+
+
+@dataclass
+class LookupStats:  # datastore.hpp:39-67
+    lookups: int = 0
+    prior_hits: int = 0
+    dynamic_hits: int = 0
+    rejected_hits: int = 0
+    fallback_hits: int = 0
+    misses: int = 0
+
+    def hits(self):
+        return self.prior_hits + self.dynamic_hits + self.rejected_hits + self.fallback_hits
+
+    def hit_rate(self):
+        return 0.0 if self.lookups == 0 else self.hits() / self.lookups
+
+
+class _Layer:
+    """One NGramIndex layer of a device store (datastore.hpp:19-27)."""
+
+    def __init__(self, store: "HierarchicalDatastore", layer: int):
+        self._s, self._l = store, layer
+
+    def insert(self, tokens, step: int):  # NGramIndex::insert, datastore.cpp:9-20
+        a = _i32(tokens)
+        check(lib().dbl_store_insert(self._s._h, self._l, _p32(a), len(a), int(step)))
+
+    def clear(self):
+        check(lib().dbl_store_clear_layer(self._s._h, self._l))
+
+    def _info(self):
+        n_s, n_t, occ = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().dbl_store_layer_info(self._s._h, self._l, C.byref(n_s), C.byref(n_t),
+                                         C.byref(occ)))
+        return n_s.value, n_t.value, occ.value
+
+    def occurrence_count(self) -> int:
+        return self._info()[2]
+
+    @property
+    def max_order(self):
+        return self._s._orders[self._l]
+
+    @max_order.setter
+    def max_order(self, v):
+        check(lib().dbl_store_set_layer_order(self._s._h, self._l, int(v)))
+        self._s._orders[self._l] = int(v)
+
+    def read(self):
+        """(sequences, steps) copied back from HBM."""
+        n_s, n_t, _ = self._info()
+        toks = np.zeros(max(n_t, 1), np.int32)
+        lens = np.zeros(max(n_s, 1), np.int32)
+        steps = np.zeros(max(n_s, 1), np.int64)
+        check(lib().dbl_store_layer_read(self._s._h, self._l, _p32(toks), len(toks), _p32(lens),
+                                         steps.ctypes.data_as(C.POINTER(C.c_int64)), len(lens)))
+        out, at = [], 0
+        for i in range(n_s):
+            out.append(toks[at:at + lens[i]].tolist())
+            at += lens[i]
+        return out, steps[:n_s].tolist()
+
+    @property
+    def sequences(self):
+        return self.read()[0]
+
+
+class HierarchicalDatastore:
+    """Device-resident three-layer n-gram store (datastore.hpp:72-95)."""
+
+    def __init__(self, n: int = 3, d: int = 10, device: int = 0):
+        h = C.c_void_p()
+        check(lib().dbl_store_create(int(n), int(d), int(device), C.byref(h)))
+        self._h = h
+        self.max_order, self.depth, self.device = n, d, device
+        self._orders = [n, n, n]
+        self._rej = True
+        self.prior, self.dynamic, self.rejected = _Layer(self, 0), _Layer(self, 1), _Layer(self, 2)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().dbl_store_destroy(h)
+            self._h = None
+
+    @property
+    def rejected_enabled(self) -> bool:
+        return self._rej
+
+    @rejected_enabled.setter
+    def rejected_enabled(self, on: bool):
+        check(lib().dbl_store_set_rejected_enabled(self._h, int(bool(on))))
+        self._rej = bool(on)
+
+    @property
+    def step_counter(self) -> int:
+        v = C.c_int64()
+        check(lib().dbl_store_get_step(self._h, C.byref(v)))
+        return v.value
+
+    @step_counter.setter
+    def step_counter(self, v: int):
+        check(lib().dbl_store_set_step(self._h, int(v)))
+
+    def lookup(self, context, d: int) -> LookupResult:  # datastore.cpp:82-132
+        a = _i32(context)
+        cap = max(int(d), 1)
+        out = np.zeros(cap, np.int32)
+        n, src, order = C.c_int(), C.c_int(), C.c_int()
+        check(lib().dbl_store_lookup(self._h, _p32(a), len(a), int(d), _p32(out), cap,
+                                     C.byref(n), C.byref(src), C.byref(order)))
+        return LookupResult(out[:n.value].tolist(), SOURCES[src.value], order.value)
+
+    def lookup_batch(self, contexts, depths):
+        """Many independent lookups in one kernel launch (one CTA per query)."""
+        ctxs = [_i32(c) for c in contexts]
+        for c in ctxs:
+            if len(c) == 0:
+                raise InvalidArgument("lookup: empty context")
+        offs = np.zeros(len(ctxs) + 1, np.int64)
+        offs[1:] = np.cumsum([len(c) for c in ctxs])
+        toks = np.concatenate(ctxs) if ctxs else np.zeros(1, np.int32)
+        deps = _i32(depths)
+        dcap = max(int(deps.max()) if len(deps) else 1, 1)
+        nq = len(ctxs)
+        oc = np.zeros(nq * dcap, np.int32)
+        on, osrc, oord = (np.zeros(nq, np.int32) for _ in range(3))
+        check(lib().dbl_store_lookup_batch(self._h, nq, offs.ctypes.data_as(C.POINTER(C.c_int64)),
+                                           _p32(toks), _p32(deps), dcap, _p32(oc), _p32(on),
+                                           _p32(osrc), _p32(oord)))
+        return [LookupResult(oc[q * dcap:q * dcap + on[q]].tolist(), SOURCES[osrc[q]], int(oord[q]))
+                for q in range(nq)]
+
+    def record_accepted(self, tokens):  # datastore.cpp:134-137
+        a = _i32(tokens)
+        check(lib().dbl_store_record(self._h, DYNAMIC, _p32(a), len(a)))
+
+    def record_rejected(self, tokens):  # datastore.cpp:139-142
+        a = _i32(tokens)
+        check(lib().dbl_store_record(self._h, REJECTED, _p32(a), len(a)))
+
+    def flush_session(self):  # datastore.cpp:144-147
+        check(lib().dbl_store_flush_session(self._h))
+
+    @property
+    def stats(self) -> LookupStats:
+        v = np.zeros(6, np.int64)
+        check(lib().dbl_store_stats(self._h, v.ctypes.data_as(C.POINTER(C.c_int64))))
+        return LookupStats(*[int(x) for x in v])
+
+
+def build_prior(store: HierarchicalDatastore, corpora, rounds: int):
+    """build_prior (datastore.cpp:149-159): the first K sequences, step = index, into store.prior."""
+    if rounds < 0:
+        raise InvalidArgument("build_prior: rounds must be >= 0")
+    for i, seq in enumerate(list(corpora)[:rounds]):
+        store.prior.insert(seq, i)
+    return store
+
+
+def parse_dstore_v1(text: str):
+    """dstore-v1 (datastore.cpp:161-187) -> (max_order, [sequences])."""
+    lines = text.split("\n")
+    head = lines[0].split()
+    if len(head) < 3 or head[0] != "dstore-v1":
+        raise DoubleError("dstore-v1: bad header")
+    n = int(head[2])
+    if len(lines) - 1 < n:
+        raise DoubleError("dstore-v1: truncated")
+    return int(head[1]), [[int(t) for t in lines[1 + i].split()] for i in range(n)]
+
+
+def parse_model_v1(text: str):
+    """model-v1 (model.cpp:199-228) -> (order, vocab, windows[n,order], probs[n,vocab], fallback)."""
+    lines = text.split("\n")
+    head = lines[0].split()
+    if len(head) < 4 or head[0] != "model-v1":
+        raise DoubleError("model-v1: bad header")
+    vocab, order = int(head[1]), int(head[2])
+    windows, rows, fallback = [], [], None
+    for ln in lines[1:]:
+        if not ln.strip():
+            continue
+        left, right = ln.split(":", 1)
+        probs = np.array(right.split(), dtype=np.float64)
+        if len(probs) != vocab:
+            raise DoubleError("model-v1: truncated probability row")
+        if left.strip() == "fallback":
+            fallback = probs
+            continue
+        w = [int(t) for t in left.split()]
+        if len(w) != order:
+            raise DoubleError("model-v1: window length mismatch")
+        windows.append(w)
+        rows.append(probs)
+    if fallback is None:
+        raise DoubleError("model-v1: missing fallback row")
+    return (order, vocab, np.array(windows, np.int32).reshape(-1, order),
+            np.array(rows, np.float64).reshape(-1, vocab), fallback)
+
+
+class _Model:
+    _h = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().dbl_model_destroy(h)
+            self._h = None
+
+    @property
+    def vocab_size(self) -> int:
+        v = C.c_int()
+        check(lib().dbl_model_vocab(self._h, C.byref(v)))
+        return v.value
+
+    @property
+    def weight_bytes(self) -> int:
+        v = C.c_int64()
+        check(lib().dbl_model_weight_bytes(self._h, C.byref(v)))
+        return v.value
+
+
+class TableModel(_Model):
+    """Device TableModel (model.hpp:18-25): order-m windows -> fp64 next-token rows."""
+
+    def __init__(self, order, vocab, windows, probs, fallback, device: int = 0):
+        w = np.ascontiguousarray(windows, np.int32).reshape(-1)
+        p = np.ascontiguousarray(probs, np.float64).reshape(-1)
+        f = np.ascontiguousarray(fallback, np.float64)
+        n_rows = len(w) // order if order else 0
+        h = C.c_void_p()
+        check(lib().dbl_table_create(int(order), int(vocab), n_rows, _p32(w),
+                                     p.ctypes.data_as(C.POINTER(C.c_double)),
+                                     f.ctypes.data_as(C.POINTER(C.c_double)), int(device), C.byref(h)))
+        self._h = h
+        self.order = order
+
+    @classmethod
+    def from_model_v1(cls, text: str, device: int = 0) -> "TableModel":
+        order, vocab, w, p, f = parse_model_v1(text)
+        return cls(order, vocab, w, p, f, device)
+
+
+class Transformer(_Model):
+    """Random-init bf16 transformer on the device (shapes: models.py presets)."""
+
+    def __init__(self, cfg: TransformerConfig, device: int = 0, nccl_comm: int | None = None):
+        h = C.c_void_p()
+        check(lib().dbl_transformer_create(C.byref(cfg), int(device),
+                                           C.c_void_p(nccl_comm) if nccl_comm else None, C.byref(h)))
+        self._h = h
+        self.cfg = cfg
+
+    def weight(self, name: str, layer: int = -1, shape=None) -> np.ndarray:
+        """bf16 weight -> np.float32 (for the torch fp32 reference in tests)."""
+        numel = int(np.prod(shape))
+        out = np.zeros(numel, np.uint16)
+        check(lib().dbl_transformer_get_weight(self._h, name.encode(), int(layer),
+                                               out.ctypes.data_as(C.POINTER(C.c_uint16)), numel))
+        return (out.astype(np.uint32) << 16).view(np.float32).reshape(shape)
+
+
+def forward_batch(model: _Model, context, candidates) -> list:
+    """forward_batch (model.cpp:37-53) consumed greedily: argmax of each of the |cands|+1 rows."""
+    ctx, cands = _i32(context), _i32(candidates)
+    out = np.zeros(len(cands) + 1, np.int32)
+    check(lib().dbl_forward_argmax(model._h, _p32(ctx), len(ctx), _p32(cands), len(cands), _p32(out)))
+    return out.tolist()
+
+
+def forward_logits(model: _Model, context, candidates) -> np.ndarray:
+    """(|cands|+1) x vocab fp32 logits (tables: the fp64 probabilities rounded to fp32)."""
+    ctx, cands = _i32(context), _i32(candidates)
+    out = np.zeros((len(cands) + 1, model.vocab_size), np.float32)
+    check(lib().dbl_forward_logits(model._h, _p32(ctx), len(ctx), _p32(cands), len(cands),
+                                   out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
+@dataclass
+class PipelineOptions:  # pipeline.hpp:36-44 (+ LatencyConfig, :15-29)
+    gamma: int = 4
+    depth: int = 10
+    draft_retrieval: bool = True
+    target_retrieval: bool = True
+    engine: str = "serial"  # serial|concurrent: identical results; the device always overlaps
+    t_target: float = 1.0
+    t_draft: float = 0.25
+    t_lookup: float = 0.0
+    t_sync: float = 0.0
+    use_graphs: bool = True
+
+    def _c(self) -> _Opts:
+        return _Opts(self.gamma, self.depth, int(self.draft_retrieval), int(self.target_retrieval),
+                     int(self.engine == "concurrent"), self.t_target, self.t_draft, self.t_lookup,
+                     self.t_sync, int(self.use_graphs))
+
+
+@dataclass
+class RunResult:  # pipeline.hpp:84-88
+    output: list
+    metrics: dict
+    jsonl: str = ""
+    traces: list = field(default_factory=list)
+
+
+def _finish(rc, out, n, m, js, jl, want_jsonl) -> RunResult:
+    check(rc)
+    import json
+    text = js.value.decode() if want_jsonl else ""
+    return RunResult(out[:n.value].tolist(), m.as_dict(), text,
+                     [json.loads(x) for x in text.splitlines()] if want_jsonl else [])
+
+
+def _jsonl_buf(max_new, gamma=1):
+    return C.create_string_buffer(max(1 << 16, 512 * (max_new + 8)))
+
+
+def run(draft: _Model, target: _Model, store: HierarchicalDatastore, prompt, max_new_tokens: int,
+        opts: PipelineOptions | None = None, want_jsonl: bool = True) -> RunResult:
+    """run (pipeline.cpp:264-323): the DOUBLE loop on the device."""
+    opts = opts or PipelineOptions()
+    p = _i32(prompt)
+    cap = max(int(max_new_tokens), 1)
+    out = np.zeros(cap, np.int32)
+    n = C.c_int()
+    m = RunMetrics()
+    js = _jsonl_buf(max_new_tokens) if want_jsonl else None
+    jl = C.c_int64()
+    o = opts._c()
+    rc = lib().dbl_run(draft._h, target._h, store._h, _p32(p), len(p), int(max_new_tokens),
+                       C.byref(o), _p32(out), cap, C.byref(n), C.byref(m), js,
+                       len(js) if js is not None else 0, C.byref(jl))
+    return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float = 1.0,
+                   want_jsonl: bool = True) -> RunResult:
+    """run_vanilla_ar (harness.cpp:233-258), greedy."""
+    p = _i32(prompt)
+    cap = max(int(max_new_tokens), 1)
+    out = np.zeros(cap, np.int32)
+    n = C.c_int()
+    m = RunMetrics()
+    js = _jsonl_buf(max_new_tokens) if want_jsonl else None
+    jl = C.c_int64()
+    rc = lib().dbl_run_ar(target._h, _p32(p), len(p), int(max_new_tokens), float(t_target), _p32(out),
+                          cap, C.byref(n), C.byref(m), js, len(js) if js is not None else 0,
+                          C.byref(jl))
+    return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+def run_serial_sd(draft: _Model, target: _Model, store: HierarchicalDatastore, prompt,
+                  max_new_tokens: int, opts: PipelineOptions | None = None,
+                  use_retrieval: bool = False, want_jsonl: bool = True) -> RunResult:
+    """run_serial_sd (harness.cpp:264-369): methods ``sd`` / ``draft_retrieval``."""
+    opts = opts or PipelineOptions()
+    p = _i32(prompt)
+    cap = max(int(max_new_tokens), 1)
+    out = np.zeros(cap, np.int32)
+    n = C.c_int()
+    m = RunMetrics()
+    js = _jsonl_buf(max_new_tokens) if want_jsonl else None
+    jl = C.c_int64()
+    o = opts._c()
+    rc = lib().dbl_run_serial_sd(draft._h, target._h, store._h, _p32(p), len(p),
+                                 int(max_new_tokens), C.byref(o), int(use_retrieval), _p32(out), cap,
+                                 C.byref(n), C.byref(m), js, len(js) if js is not None else 0,
+                                 C.byref(jl))
+    return _finish(rc, out, n, m, js, jl, want_jsonl)
