@@ -147,6 +147,14 @@ int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, 
                       int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
                       int64_t jsonl_cap, int64_t* jsonl_len);
 
+/* ===================================================================== kernel-level checks
+ * Debug entry points used by the parity tests to exercise one kernel against a host reference.
+ * dbl_debug_gemm: W [n_out x K] bf16 bits, X [T x K] bf16 bits, padded to tp token columns.
+ *   epi 0 StoreBF16 / 4 StoreF32 -> io[T x n_out]; 1 ResidAdd -> io[T x n_out] += W X^T;
+ *   2 SiluMul (16 gate | 16 up rows per 32) -> io[T x n_out/2]; 3 Argmax -> argmax[T], io = logits. */
+int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,
+                   int n_valid, float* io, int32_t* argmax);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

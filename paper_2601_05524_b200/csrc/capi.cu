@@ -8,6 +8,9 @@
 #include "store.cuh"
 #include "table_model.cuh"
 #include "transformer.cuh"
+#include "gemm.cuh"
+#include "lane.cuh"
+#include <cuda_bf16.h>
 
 struct dbl_store_s {
     std::unique_ptr<dbl::DeviceStore> impl;
@@ -271,6 +274,54 @@ int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, 
         const dbl::RunOutput r = dbl::run_serial_sd(*draft->impl, *target->impl, *store->impl, prompt,
                                                     n_prompt, max_new, *opts, use_retrieval != 0);
         copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+
+// --------------------------------------------------------------------------- kernel checks
+int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,
+                   int n_valid, float* io, int32_t* argmax) {
+    return guarded([&] {
+        need(W, "W");
+        need(X, "X");
+        if (T < 1 || T > tp) dbl::throw_invalid("need 1 <= T <= tp");
+        dbl::require_device(0);
+        using namespace dbl;
+        DevBuf<uint16_t> dW(static_cast<size_t>(n_out) * K), dX(static_cast<size_t>(tp) * K);
+        CUDA_CHECK(cudaMemcpy(dW.p, W, dW.bytes(), cudaMemcpyHostToDevice));
+        dX.zero();
+        CUDA_CHECK(cudaMemcpy(dX.p, X, static_cast<size_t>(T) * K * 2, cudaMemcpyHostToDevice));
+        const CUtensorMap tW = make_tmap_bf16_2d(dW.p, n_out, K, 128);
+        const CUtensorMap tX = make_tmap_bf16_2d(dX.p, tp, K, 16);
+        GemmWorkspace ws;
+        const int n_tiles = (n_out + 127) / 128;
+        ws.ensure(num_sms(0), tp, n_tiles);
+        const int out_cols = epi == 2 ? n_out / 2 : n_out;
+        DevBuf<float> o32(static_cast<size_t>(tp) * out_cols);
+        DevBuf<__nv_bfloat16> o16(static_cast<size_t>(tp) * out_cols);
+        o32.zero();
+        if (epi == 1) CUDA_CHECK(cudaMemcpy(o32.p, io, static_cast<size_t>(T) * out_cols * 4, cudaMemcpyHostToDevice));
+        void* out = (epi == 0 || epi == 2) ? static_cast<void*>(o16.p) : static_cast<void*>(o32.p);
+        gemm_launch(static_cast<Epi>(epi), tW, tX, n_out, K, tp, n_valid, out, out_cols,
+                    epi == 3 ? o32.p : nullptr, out_cols, ws, 0);
+        if (epi == 3) {
+            LaneState st{};
+            st.L = T; st.c = 0; st.start = 0;
+            LaneState* dst = nullptr;
+            CUDA_CHECK(cudaMalloc(&dst, sizeof st));
+            CUDA_CHECK(cudaMemcpy(dst, &st, sizeof st, cudaMemcpyHostToDevice));
+            DevBuf<int32_t> am(tp);
+            argmax_finish(ws, n_tiles, tp, dst, am.p, 0);
+            CUDA_CHECK(cudaMemcpy(argmax, am.p, T * 4, cudaMemcpyDeviceToHost));
+            cudaFree(dst);
+        }
+        CUDA_CHECK(cudaDeviceSynchronize());
+        if (epi == 0 || epi == 2) {
+            std::vector<__nv_bfloat16> h(static_cast<size_t>(T) * out_cols);
+            CUDA_CHECK(cudaMemcpy(h.data(), o16.p, h.size() * 2, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < h.size(); ++i) io[i] = __bfloat162float(h[i]);
+        } else {
+            CUDA_CHECK(cudaMemcpy(io, o32.p, static_cast<size_t>(T) * out_cols * 4, cudaMemcpyDeviceToHost));
+        }
     });
 }
 

@@ -1,0 +1,368 @@
+// tcgen05 swap-AB stream-K GEMM (see gemm.cuh for the design).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "gemm.cuh"
+#include "lane.cuh"
+#include "sm100.cuh"
+
+namespace dbl {
+
+namespace {
+
+constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps 2..5 epilogue
+constexpr int kBlockM = 128, kBlockK = 64;
+constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KiB
+
+__device__ __forceinline__ long long range_begin(long long c, long long U, long long G) { return c * U / G; }
+// CTA whose range contains unit u: largest c with floor(cU/G) <= u
+__device__ __forceinline__ long long cta_of(long long u, long long U, long long G) {
+    return ((u + 1) * G - 1) / U;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmArgs a) {
+    using namespace sm100;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = a.stages, tp = a.tp;
+    const int b_bytes = tp * kBlockK * 2;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + S * kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * b_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+    int* sflag = reinterpret_cast<int*>(tslot + 1);
+    float* sval = reinterpret_cast<float*>(sflag + 4);  // [4][32]
+    int* sidx = reinterpret_cast<int*>(sval + 128);     // [4][32]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long U = a.units, G = gridDim.x, c = blockIdx.x;
+    const long long b0 = range_begin(c, U, G), b1 = range_begin(c + 1, U, G);
+    if (b0 >= b1) return;
+    const int KB = a.kb_total;
+    const uint32_t ncols = tp <= 32 ? 32 : tp <= 64 ? 64 : tp <= 128 ? 128 : 256;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 128);
+        fence_barrier_init();
+        tma_prefetch_desc(&tmW);
+        tma_prefetch_desc(&tmX);
+    }
+    if (warp == 1) tmem_alloc(tslot, ncols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ------------------------------------------------ TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long u = b0; u < b1;) {
+                const int m = static_cast<int>(u / KB), kb0 = static_cast<int>(u % KB);
+                const int kb1 = static_cast<int>(std::min<long long>(KB, kb0 + (b1 - u)));
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
+                    tma_load_2d(sA + stage * kABytes, &tmW, &full[stage], kb * kBlockK, m * kBlockM, kEvictFirst);
+                    for (int j = 0; j < tp / 16; ++j)
+                        tma_load_2d(sB + stage * b_bytes + j * 2048, &tmX, &full[stage], kb * kBlockK, j * 16,
+                                    kEvictLast);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                u += kb1 - kb0;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------------ MMA issuer
+            const uint32_t idesc = idesc_bf16_m128(tp);
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (long long u = b0; u < b1;) {
+                const int kb0 = static_cast<int>(u % KB);
+                const int kb1 = static_cast<int>(std::min<long long>(KB, kb0 + (b1 - u)));
+                mbar_wait(tempty, acc_phase ^ 1);
+                tc_fence_after();
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ad = umma_desc_sw128(smem_u32(sA + stage * kABytes));
+                    const uint64_t bd = umma_desc_sw128(smem_u32(sB + stage * b_bytes));
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    mma_commit(&empty[stage]);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(tfull);
+                acc_phase ^= 1;
+                u += kb1 - kb0;
+            }
+        }
+    } else {  // ------------------------------------------------------------ epilogue (128 threads)
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        const int r = q * 32 + lane;
+        const int et = threadIdx.x - 64;  // 0..127
+        const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        uint32_t acc_phase = 0;
+        for (long long u = b0; u < b1;) {
+            const int m = static_cast<int>(u / KB), kb0 = static_cast<int>(u % KB);
+            const int kb1 = static_cast<int>(std::min<long long>(KB, kb0 + (b1 - u)));
+            const long long tile_u0 = static_cast<long long>(m) * KB, tile_u1 = tile_u0 + KB;
+            const long long first = cta_of(tile_u0, U, G), last = cta_of(tile_u1 - 1, U, G);
+            const int n_contrib = static_cast<int>(last - first + 1);
+            const int my = static_cast<int>(c - first);
+            mbar_wait(tfull, acc_phase);
+            tc_fence_after();
+            bool finisher = true;
+            if (n_contrib > 1) {
+                const int slot = static_cast<int>(2 * c + (u == b0 ? 0 : 1));
+                float* P = a.ws + static_cast<long long>(slot) * tp * kBlockM;
+                for (int ch = 0; ch < tp; ch += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + ch, v);
+                    const int nc = min(32, tp - ch);
+                    for (int i = 0; i < nc; ++i) __stcg(P + (ch + i) * kBlockM + r, v[i]);
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (et == 0) sflag[0] = atomicAdd(&a.counters[m], 1) == n_contrib - 1;
+                named_bar_sync(1, 128);
+                finisher = sflag[0] != 0;
+                if (finisher) {
+                    __threadfence();
+                    if (et == 0) a.counters[m] = 0;  // reusable by the next launch
+                }
+            }
+            if (finisher) {
+                for (int ch = 0; ch < tp; ch += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + ch, v);
+                    const int nc = min(32, tp - ch);
+                    if (n_contrib > 1) {  // ordered sum p_0 + p_1 + ... (fixed for every token count)
+                        float acc[32];
+                        for (int j = 0; j < n_contrib; ++j) {
+                            const long long cj = first + j;
+                            const long long bj = range_begin(cj, U, G);
+                            const int slot = static_cast<int>(2 * cj + (std::max(bj, tile_u0) == bj ? 0 : 1));
+                            const float* P = a.ws + static_cast<long long>(slot) * tp * kBlockM;
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const float x = (j == my || i >= nc) ? v[i] : __ldcg(P + (ch + i) * kBlockM + r);
+                                acc[i] = j == 0 ? x : acc[i] + x;
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = acc[i];
+                    }
+                    const int n = m * kBlockM + r;
+                    if constexpr (EPI == static_cast<int>(Epi::StoreBF16)) {
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out);
+                        for (int i = 0; i < nc; ++i) o[static_cast<long long>(ch + i) * a.ld_out + n] = __float2bfloat16_rn(v[i]);
+                    } else if constexpr (EPI == static_cast<int>(Epi::StoreF32)) {
+                        float* o = static_cast<float*>(a.out);
+                        for (int i = 0; i < nc; ++i) o[static_cast<long long>(ch + i) * a.ld_out + n] = v[i];
+                    } else if constexpr (EPI == static_cast<int>(Epi::ResidAdd)) {
+                        float* o = static_cast<float*>(a.out);
+                        for (int i = 0; i < nc; ++i) o[static_cast<long long>(ch + i) * a.ld_out + n] += v[i];
+                    } else if constexpr (EPI == static_cast<int>(Epi::SiluMul)) {
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out);
+                        const int f = m * 64 + q * 16 + lane;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const float up = __shfl_down_sync(0xffffffffu, v[i], 16);
+                            if (lane < 16 && i < nc) {
+                                const float g = v[i];
+                                o[static_cast<long long>(ch + i) * a.ld_out + f] =
+                                    __float2bfloat16_rn(g / (1.0f + __expf(-g)) * up);
+                            }
+                        }
+                    } else {  // Argmax
+                        const bool ok = n < a.n_valid;
+                        if (a.logits && ok)
+                            for (int i = 0; i < nc; ++i) a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            float bv = ok ? v[i] : -INFINITY;
+                            int bi = ok ? n : 0x7fffffff;
+#pragma unroll
+                            for (int off = 16; off > 0; off >>= 1) {
+                                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                            }
+                            if (lane == i) { sval[q * 32 + i] = bv; sidx[q * 32 + i] = bi; }
+                        }
+                        named_bar_sync(1, 128);
+                        if (et < 32 && et < nc) {
+                            float bv = sval[et];
+                            int bi = sidx[et];
+                            for (int qq = 1; qq < 4; ++qq) {
+                                const float ov = sval[qq * 32 + et];
+                                const int oi = sidx[qq * 32 + et];
+                                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                            }
+                            a.amax_ws[static_cast<long long>(m) * tp + ch + et] = make_float2(bv, __int_as_float(bi));
+                        }
+                        named_bar_sync(1, 128);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty);
+            acc_phase ^= 1;
+            u += kb1 - kb0;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, ncols);
+    }
+}
+
+// one warp per token row: reduce the per-tile (max, lowest idx) partials in tile order
+__global__ void argmax_finish_kernel(const float2* __restrict__ ws, int n_tiles, int tp, const LaneState* lane,
+                                     int32_t* __restrict__ argmax) {
+    const int start = lane->start;
+    const int T = lane->L + lane->c - start;
+    const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int ln = threadIdx.x & 31;
+    if (t >= T || t >= tp) return;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int m = ln; m < n_tiles; m += 32) {
+        const float2 p = ws[static_cast<long long>(m) * tp + t];
+        const int pi = __float_as_int(p.y);
+        if (p.x > bv || (p.x == bv && pi < bi)) { bv = p.x; bi = pi; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (ln == 0) argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw Error(DBL_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+template <int EPI>
+void set_smem_attr() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    });
+}
+
+}  // namespace
+
+int num_sms(int device) {
+    int n = 0;
+    CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    return n;
+}
+
+CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockK), static_cast<cuuint32_t>(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    if (cols % kBlockK) throw_invalid("GEMM K must be a multiple of 64");
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(DBL_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+void GemmWorkspace::ensure(int g, int mtp, int mtiles) {
+    if (g <= grid && mtp <= max_tp && mtiles <= max_tiles) return;
+    grid = std::max(grid, g);
+    max_tp = std::max(max_tp, mtp);
+    max_tiles = std::max(max_tiles, mtiles);
+    partials.alloc(static_cast<size_t>(2) * grid * max_tp * kBlockM);
+    counters.alloc(max_tiles);
+    counters.zero();
+    amax.alloc(static_cast<size_t>(max_tiles) * max_tp);
+    CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_out, int K, int tp, int n_valid,
+                 void* out, int ld_out, float* logits, int ld_logits, GemmWorkspace& ws, cudaStream_t s) {
+    if (tp < 16 || tp > 256 || tp % 16) throw_invalid("GEMM token tile must be a multiple of 16 in [16, 256]");
+    if (K % kBlockK) throw_invalid("GEMM K must be a multiple of 64");
+    GemmArgs a{};
+    a.n_out = n_out;
+    a.K = K;
+    a.tp = tp;
+    a.n_valid = n_valid;
+    a.n_tiles = (n_out + kBlockM - 1) / kBlockM;
+    a.kb_total = K / kBlockK;
+    a.units = static_cast<long long>(a.n_tiles) * a.kb_total;
+    const int stage_bytes = kABytes + tp * kBlockK * 2;
+    const int budget = 227 * 1024 - 1024 - 1024;  // alignment slack + barriers/scratch
+    a.stages = std::max(2, std::min(12, budget / stage_bytes));
+    const size_t smem = 1024 + static_cast<size_t>(a.stages) * stage_bytes + 1024;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    const int grid = static_cast<int>(std::min<long long>(num_sms(dev), a.units));
+    if (ws.grid < grid || ws.max_tp < tp || ws.max_tiles < a.n_tiles)
+        throw_runtime("GEMM workspace too small (call GemmWorkspace::ensure)");
+    a.out = out;
+    a.ld_out = ld_out;
+    a.logits = logits;
+    a.ld_logits = ld_logits;
+    a.amax_ws = ws.amax.p;
+    a.ws = ws.partials.p;
+    a.counters = ws.counters.p;
+    switch (epi) {
+#define DBL_GEMM_CASE(E)                                                                   \
+    case E:                                                                                \
+        set_smem_attr<static_cast<int>(E)>();                                              \
+        gemm_kernel<static_cast<int>(E)><<<grid, kThreads, smem, s>>>(tmW, tmX, a);        \
+        break;
+        DBL_GEMM_CASE(Epi::StoreBF16)
+        DBL_GEMM_CASE(Epi::ResidAdd)
+        DBL_GEMM_CASE(Epi::SiluMul)
+        DBL_GEMM_CASE(Epi::Argmax)
+        DBL_GEMM_CASE(Epi::StoreF32)
+#undef DBL_GEMM_CASE
+    }
+    CUDA_LAUNCH_CHECK();
+}
+
+void argmax_finish(const GemmWorkspace& ws, int n_tiles, int tp, const LaneState* lane, int32_t* argmax,
+                   cudaStream_t s) {
+    argmax_finish_kernel<<<(tp + 7) / 8, 256, 0, s>>>(ws.amax.p, n_tiles, tp, lane, argmax);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace dbl
