@@ -191,8 +191,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     } else {  // Argmax
                         const bool ok = n < a.n_valid;
-                        if (a.logits && ok)
-                            for (int i = 0; i < nc; ++i) a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
+                        if (a.logits && ok) {  // only the forward's valid rows (the buffer holds no padding)
+                            const int nrow = a.lane ? a.lane->L + a.lane->c - a.lane->start : tp;
+                            for (int i = 0; i < nc && ch + i < nrow; ++i)
+                                a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
+                        }
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
                             float bv = ok ? v[i] : -INFINITY;
@@ -316,7 +319,8 @@ void GemmWorkspace::ensure(int g, int mtp, int mtiles) {
 }
 
 void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_out, int K, int tp, int n_valid,
-                 void* out, int ld_out, float* logits, int ld_logits, GemmWorkspace& ws, cudaStream_t s) {
+                 void* out, int ld_out, float* logits, int ld_logits, GemmWorkspace& ws, cudaStream_t s,
+                 const LaneState* lane) {
     if (tp < 16 || tp > 256 || tp % 16) throw_invalid("GEMM token tile must be a multiple of 16 in [16, 256]");
     if (K % kBlockK) throw_invalid("GEMM K must be a multiple of 64");
     GemmArgs a{};
@@ -328,9 +332,9 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
     a.kb_total = K / kBlockK;
     a.units = static_cast<long long>(a.n_tiles) * a.kb_total;
     const int stage_bytes = kABytes + tp * kBlockK * 2;
-    const int budget = 227 * 1024 - 1024 - 1024;  // alignment slack + barriers/scratch
+    const int budget = 227 * 1024 - 1024 - 2048;  // alignment slack + barriers/scratch (<= 1.3 KB)
     a.stages = std::max(2, std::min(12, budget / stage_bytes));
-    const size_t smem = 1024 + static_cast<size_t>(a.stages) * stage_bytes + 1024;
+    const size_t smem = 1024 + static_cast<size_t>(a.stages) * stage_bytes + 2048;
     int dev = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
     const int grid = static_cast<int>(std::min<long long>(num_sms(dev), a.units));
@@ -340,6 +344,7 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
     a.ld_out = ld_out;
     a.logits = logits;
     a.ld_logits = ld_logits;
+    a.lane = lane;
     a.amax_ws = ws.amax.p;
     a.ws = ws.partials.p;
     a.counters = ws.counters.p;

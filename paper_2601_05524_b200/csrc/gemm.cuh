@@ -18,6 +18,8 @@
 
 namespace dbl {
 
+struct LaneState;
+
 enum class Epi : int {
     StoreBF16 = 0,  // out[t][n] = bf16(acc)
     ResidAdd = 1,   // out[t][n] += acc           (fp32 residual stream)
@@ -38,6 +40,7 @@ struct GemmArgs {
     float2* amax_ws;  // [n_tiles][tp] (value, index bits)
     float* ws;        // stream-K partial slots [2 * grid][tp][128]
     int* counters;    // [n_tiles], zero between launches
+    const struct LaneState* lane;  // Argmax logits rows: [0, L + c - start) only (nullable: tp rows)
 };
 
 struct GemmWorkspace {  // per decode lane (a lane's GEMMs are stream-ordered)
@@ -54,7 +57,7 @@ CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int
 // Launch one GEMM.  tmW: weights (box 128 x 64), tmX: activations (box 16 x 64).
 void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_out, int K, int tp,
                  int n_valid, void* out, int ld_out, float* logits, int ld_logits, GemmWorkspace& ws,
-                 cudaStream_t s);
+                 cudaStream_t s, const struct LaneState* lane = nullptr);
 struct LaneState;
 // final argmax over the per-tile partials: argmax[lane.start + t] for t in [0, L + c - start)
 void argmax_finish(const GemmWorkspace& ws, int n_tiles, int tp, const LaneState* lane, int32_t* argmax,

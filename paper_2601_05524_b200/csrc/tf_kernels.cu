@@ -1,0 +1,364 @@
+// Non-GEMM verify-forward kernels (see tf_kernels.cuh).
+#include <cmath>
+
+#include "tf_kernels.cuh"
+
+namespace dbl {
+
+namespace {
+
+__host__ __device__ __forceinline__ unsigned long long mix(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d49bb133111ebull;
+    return x ^ (x >> 31);
+}
+// N(0,1) from a 64-bit counter hash (Box-Muller on two 24-bit uniforms)
+__device__ __forceinline__ float normal_of(unsigned long long key) {
+    const unsigned long long h = mix(key);
+    const float u1 = (static_cast<float>(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
+    const float u2 = static_cast<float>((h >> 16) & 0xFFFFFFull) * (1.0f / 16777216.0f);
+    return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+
+__global__ void init_normal_kernel(__nv_bfloat16* dst, int rows, int cols, int ld, unsigned long long base,
+                                   long long r0, long long c0, long long C, float std) {
+    const long long n = static_cast<long long>(rows) * cols;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = i / cols, cc = i % cols;
+        const long long logical = (r0 + r) * C + (c0 + cc);
+        dst[r * ld + cc] = __float2bfloat16_rn(std * normal_of(base ^ static_cast<unsigned long long>(logical)));
+    }
+}
+
+__global__ void init_gateup_kernel(__nv_bfloat16* dst, int ffn_local, int hidden, unsigned long long gbase,
+                                   unsigned long long ubase, long long f0, float std) {
+    const long long n = 2LL * ffn_local * hidden;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long p = i / hidden, col = i % hidden;
+        // physical row p: tile j = p/128, quadrant q = (p%128)/32, half = (p%32)/16, lane = p%16
+        const long long j = p / 128, q = (p % 128) / 32, half = (p % 32) / 16, ln = p % 16;
+        const long long f = f0 + j * 64 + q * 16 + ln;  // logical ffn feature
+        const unsigned long long base = half ? ubase : gbase;
+        dst[i] = __float2bfloat16_rn(std * normal_of(base ^ static_cast<unsigned long long>(f * hidden + col)));
+    }
+}
+
+__global__ void fill_kernel(__nv_bfloat16* dst, long long n, float v) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[i] = __float2bfloat16_rn(v);
+}
+
+__global__ void forward_begin_kernel(LaneState* lane) { lane->start = min(lane->kv_len, lane->row0); }
+__global__ void forward_end_kernel(LaneState* lane) { lane->kv_len = lane->L + lane->c; }
+
+__global__ void embed_kernel(const __nv_bfloat16* __restrict__ E, int hidden, const int32_t* __restrict__ buf,
+                             const LaneState* lane, float* __restrict__ resid) {
+    const int t = blockIdx.x;
+    const int start = lane->start, T = lane->L + lane->c - start;
+    const int tok = t < T ? buf[start + t] : 0;
+    const __nv_bfloat16* row = E + static_cast<long long>(tok) * hidden;
+    for (int i = threadIdx.x; i < hidden; i += blockDim.x)
+        resid[static_cast<long long>(t) * hidden + i] = __bfloat162float(row[i]);
+}
+
+// one CTA per row; 256 threads; fixed-order block reduction
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w, int hidden,
+                               float eps, __nv_bfloat16* __restrict__ out) {
+    __shared__ float red[8];
+    const float* row = x + static_cast<long long>(blockIdx.x) * hidden;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < hidden; i += blockDim.x) ss = fmaf(row[i], row[i], ss);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tot += red[i];
+    const float r = rsqrtf(tot / hidden + eps);
+    __nv_bfloat16* o = out + static_cast<long long>(blockIdx.x) * hidden;
+    for (int i = threadIdx.x; i < hidden; i += blockDim.x) o[i] = __float2bfloat16_rn(row[i] * r * __bfloat162float(w[i]));
+}
+
+__device__ __forceinline__ __nv_bfloat16* kv_addr(__nv_bfloat16* base, const int32_t* pt, int n_kv, int hd, int h,
+                                                  int pos) {
+    const int phys = pt[pos / kPage];
+    return base + ((static_cast<long long>(phys) * n_kv + h) * kPage + (pos % kPage)) * hd;
+}
+
+// one warp per (token, head slot): slots [0, nh) q heads, [nh, nh+nkv) k heads, [nh+nkv, nh+2nkv) v heads
+template <int HD>
+__global__ void qkv_post_kernel(const __nv_bfloat16* __restrict__ qkv, int nh, int nkv, const __nv_bfloat16* qn,
+                                const __nv_bfloat16* kn, float eps, float theta, const LaneState* lane, KVView kv,
+                                __nv_bfloat16* __restrict__ qbuf) {
+    constexpr int E = HD / 32;  // elements per lane: dims lane + 32*e
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, ln = threadIdx.x & 31;
+    const int slots = nh + 2 * nkv;
+    const int t = warp / slots, slot = warp % slots;
+    const int start = lane->start, T = lane->L + lane->c - start;
+    if (t >= T) return;
+    const int pos = start + t;
+    const __nv_bfloat16* src = qkv + static_cast<long long>(t) * slots * HD + static_cast<long long>(slot) * HD;
+    float x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = __bfloat162float(src[ln + 32 * e]);
+    const bool is_q = slot < nh, is_k = !is_q && slot < nh + nkv;
+    if (is_q || is_k) {
+        const __nv_bfloat16* nw = is_q ? qn : kn;
+        if (nw) {  // per-head RMSNorm (Qwen3 q_norm / k_norm)
+            float ss = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) ss = fmaf(x[e], x[e], ss);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+            const float r = rsqrtf(ss / HD + eps);
+#pragma unroll
+            for (int e = 0; e < E; ++e) x[e] = __bfloat162float(__float2bfloat16_rn(x[e] * r * __bfloat162float(nw[ln + 32 * e])));
+        }
+        // RoPE (rotate-half): dim d < HD/2 pairs with d + HD/2 — same lane, element e and e + E/2
+        float y[E];
+#pragma unroll
+        for (int e = 0; e < E / 2; ++e) {
+            const int d = ln + 32 * e;
+            const float inv = powf(theta, -2.0f * static_cast<float>(d) / static_cast<float>(HD));
+            float sn, cs;
+            sincosf(static_cast<float>(pos) * inv, &sn, &cs);
+            y[e] = x[e] * cs - x[e + E / 2] * sn;
+            y[e + E / 2] = x[e + E / 2] * cs + x[e] * sn;
+        }
+        if (is_q) {
+            __nv_bfloat16* dq = qbuf + (static_cast<long long>(t) * nh + slot) * HD;
+#pragma unroll
+            for (int e = 0; e < E; ++e) dq[ln + 32 * e] = __float2bfloat16_rn(y[e]);
+        } else {
+            __nv_bfloat16* dk = kv_addr(kv.k, kv.page_table, nkv, HD, slot - nh, pos);
+#pragma unroll
+            for (int e = 0; e < E; ++e) dk[ln + 32 * e] = __float2bfloat16_rn(y[e]);
+        }
+    } else {
+        __nv_bfloat16* dv = kv_addr(kv.v, kv.page_table, nkv, HD, slot - nh - nkv, pos);
+#pragma unroll
+        for (int e = 0; e < E; ++e) dv[ln + 32 * e] = __float2bfloat16_rn(x[e]);
+    }
+}
+
+constexpr int kQTile = 16;
+
+// grid (n_kv, chunks, q tiles); 256 threads.  Partials (m, l, o) per (token, q head, chunk).
+template <int HD>
+__global__ void __launch_bounds__(256) attn_chunk_kernel(const __nv_bfloat16* __restrict__ qbuf, int nh, int nkv,
+                                                         KVView kv, const LaneState* lane, int max_chunks,
+                                                         float* __restrict__ part_o, float* __restrict__ part_ml) {
+    constexpr int KS = HD + 2;  // padded K row (bank-conflict-free bf16x2 reads)
+    extern __shared__ __align__(16) uint8_t sm[];
+    __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(sm);
+    __nv_bfloat16* sV = sK + kAttnChunk * KS;
+    float* sE = reinterpret_cast<float*>(sV + kAttnChunk * HD);  // [8 warps][kAttnChunk]
+    float* sQ = sE + 8 * kAttnChunk;                             // [8 warps][HD]
+    const int h = blockIdx.x, j = blockIdx.y, qt = blockIdx.z;
+    const int start = lane->start, T = lane->L + lane->c - start;
+    const int t0 = qt * kQTile, t1 = min(T, t0 + kQTile);
+    if (t0 >= t1) return;
+    const int pmax = start + t1 - 1;
+    const int k0 = j * kAttnChunk;
+    if (k0 > pmax) return;
+    const int nk = min(kAttnChunk, pmax - k0 + 1);
+    // stage the chunk's K (padded) and V rows through shared memory
+    for (int idx = threadIdx.x; idx < nk * (HD / 2); idx += blockDim.x) {
+        const int i = idx / (HD / 2), d2 = idx % (HD / 2);
+        const int pos = k0 + i;
+        const __nv_bfloat162 kk = reinterpret_cast<const __nv_bfloat162*>(kv_addr(kv.k, kv.page_table, nkv, HD, h, pos))[d2];
+        const __nv_bfloat162 vv = reinterpret_cast<const __nv_bfloat162*>(kv_addr(kv.v, kv.page_table, nkv, HD, h, pos))[d2];
+        reinterpret_cast<__nv_bfloat162*>(sK + i * KS)[d2] = kk;
+        reinterpret_cast<__nv_bfloat162*>(sV + i * HD)[d2] = vv;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const int g = nh / nkv;
+    const float scale = rsqrtf(static_cast<float>(HD));
+    float* e = sE + warp * kAttnChunk;
+    float* q = sQ + warp * HD;
+    for (int pair = warp; pair < (t1 - t0) * g; pair += 8) {
+        const int t = t0 + pair / g, hq = h * g + pair % g;
+        const int pos = start + t;
+        if (pos < k0) continue;
+        const int n = min(nk, pos - k0 + 1);
+        const __nv_bfloat16* qs = qbuf + (static_cast<long long>(t) * nh + hq) * HD;
+        for (int d = ln; d < HD; d += 32) q[d] = __bfloat162float(qs[d]);
+        __syncwarp();
+        float mx = -INFINITY;
+        for (int i = ln; i < n; i += 32) {
+            const __nv_bfloat162* kr = reinterpret_cast<const __nv_bfloat162*>(sK + i * KS);
+            float s = 0.f;
+#pragma unroll 8
+            for (int d2 = 0; d2 < HD / 2; ++d2) {
+                const float2 kf = __bfloat1622float2(kr[d2]);
+                s = fmaf(q[2 * d2], kf.x, s);
+                s = fmaf(q[2 * d2 + 1], kf.y, s);
+            }
+            s *= scale;
+            e[i] = s;
+            mx = fmaxf(mx, s);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        float l = 0.f;
+        for (int i = ln; i < n; i += 32) {
+            const float p = __expf(e[i] - mx);
+            e[i] = p;
+            l += p;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+        __syncwarp();
+        float o[HD / 32];
+#pragma unroll
+        for (int k = 0; k < HD / 32; ++k) o[k] = 0.f;
+        for (int i = 0; i < n; ++i) {
+            const float p = e[i];
+#pragma unroll
+            for (int k = 0; k < HD / 32; ++k) o[k] = fmaf(p, __bfloat162float(sV[i * HD + ln + 32 * k]), o[k]);
+        }
+        const long long slot = (static_cast<long long>(t) * nh + hq) * max_chunks + j;
+#pragma unroll
+        for (int k = 0; k < HD / 32; ++k) part_o[slot * HD + ln + 32 * k] = o[k];
+        if (ln == 0) {
+            part_ml[2 * slot] = mx;
+            part_ml[2 * slot + 1] = l;
+        }
+        __syncwarp();
+    }
+}
+
+// one warp per (token, q head): combine the position's chunks in chunk order
+template <int HD>
+__global__ void attn_combine_kernel(int nh, int max_chunks, const LaneState* lane, const float* __restrict__ part_o,
+                                    const float* __restrict__ part_ml, __nv_bfloat16* __restrict__ out) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, ln = threadIdx.x & 31;
+    const int start = lane->start, T = lane->L + lane->c - start;
+    const int t = warp / nh, hq = warp % nh;
+    if (t >= T) return;
+    const int pos = start + t;
+    const int nch = pos / kAttnChunk + 1;
+    const long long base = (static_cast<long long>(t) * nh + hq) * max_chunks;
+    float M = -INFINITY;
+    for (int j = 0; j < nch; ++j) M = fmaxf(M, part_ml[2 * (base + j)]);
+    float den = 0.f, acc[HD / 32];
+#pragma unroll
+    for (int k = 0; k < HD / 32; ++k) acc[k] = 0.f;
+    for (int j = 0; j < nch; ++j) {
+        const float w = __expf(part_ml[2 * (base + j)] - M);
+        den = fmaf(part_ml[2 * (base + j) + 1], w, den);
+#pragma unroll
+        for (int k = 0; k < HD / 32; ++k) acc[k] = fmaf(part_o[(base + j) * HD + ln + 32 * k], w, acc[k]);
+    }
+    const float inv = 1.0f / den;
+#pragma unroll
+    for (int k = 0; k < HD / 32; ++k)
+        out[static_cast<long long>(t) * nh * HD + hq * HD + ln + 32 * k] = __float2bfloat16_rn(acc[k] * inv);
+}
+
+int blocks_for(long long n, int threads) {
+    return static_cast<int>(std::min<long long>((n + threads - 1) / threads, 148LL * 32));
+}
+
+}  // namespace
+
+void launch_embed(const __nv_bfloat16* E, int hidden, const int32_t* buf, const LaneState* lane, int tp, float* resid,
+                  cudaStream_t s) {
+    embed_kernel<<<tp, 256, 0, s>>>(E, hidden, buf, lane, resid);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_rmsnorm(const float* x, const __nv_bfloat16* w, int hidden, float eps, int tp, __nv_bfloat16* out,
+                    cudaStream_t s) {
+    rmsnorm_kernel<<<tp, 256, 0, s>>>(x, w, hidden, eps, out);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_qkv_post(const __nv_bfloat16* qkv, int nh, int nkv, int hd, const __nv_bfloat16* qn,
+                     const __nv_bfloat16* kn, float eps, float theta, const LaneState* lane, KVView kv,
+                     __nv_bfloat16* qbuf, int tp, cudaStream_t s) {
+    const long long warps = static_cast<long long>(tp) * (nh + 2 * nkv);
+    const int blocks = static_cast<int>((warps * 32 + 255) / 256);
+    if (hd == 128)
+        qkv_post_kernel<128><<<blocks, 256, 0, s>>>(qkv, nh, nkv, qn, kn, eps, theta, lane, kv, qbuf);
+    else if (hd == 64)
+        qkv_post_kernel<64><<<blocks, 256, 0, s>>>(qkv, nh, nkv, qn, kn, eps, theta, lane, kv, qbuf);
+    else
+        throw_invalid("head_dim must be 64 or 128");
+    CUDA_LAUNCH_CHECK();
+}
+
+template <int HD>
+static size_t attn_smem() {
+    return static_cast<size_t>(kAttnChunk) * (HD + 2) * 2 + static_cast<size_t>(kAttnChunk) * HD * 2 +
+           8 * kAttnChunk * 4 + 8 * HD * 4;
+}
+
+void launch_attention(const __nv_bfloat16* qbuf, int nh, int nkv, int hd, KVView kv, const LaneState* lane, int tp,
+                      int max_chunks, float* part_o, float* part_ml, __nv_bfloat16* out, cudaStream_t s) {
+    const dim3 grid(nkv, max_chunks, (tp + kQTile - 1) / kQTile);
+    const int cwarps = tp * nh;
+    if (hd == 128) {
+        static bool once = [] {
+            CUDA_CHECK(cudaFuncSetAttribute(attn_chunk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(attn_smem<128>())));
+            return true;
+        }();
+        (void)once;
+        attn_chunk_kernel<128><<<grid, 256, attn_smem<128>(), s>>>(qbuf, nh, nkv, kv, lane, max_chunks, part_o, part_ml);
+        CUDA_LAUNCH_CHECK();
+        attn_combine_kernel<128><<<(cwarps * 32 + 255) / 256, 256, 0, s>>>(nh, max_chunks, lane, part_o, part_ml, out);
+    } else if (hd == 64) {
+        static bool once = [] {
+            CUDA_CHECK(cudaFuncSetAttribute(attn_chunk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(attn_smem<64>())));
+            return true;
+        }();
+        (void)once;
+        attn_chunk_kernel<64><<<grid, 256, attn_smem<64>(), s>>>(qbuf, nh, nkv, kv, lane, max_chunks, part_o, part_ml);
+        CUDA_LAUNCH_CHECK();
+        attn_combine_kernel<64><<<(cwarps * 32 + 255) / 256, 256, 0, s>>>(nh, max_chunks, lane, part_o, part_ml, out);
+    } else {
+        throw_invalid("head_dim must be 64 or 128");
+    }
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_init_normal(__nv_bfloat16* dst, int rows, int cols, int ld, uint64_t seed, uint64_t tensor, int64_t r0,
+                        int64_t c0, int64_t C, float std, cudaStream_t s) {
+    const unsigned long long base = mix(seed ^ mix(tensor * 0x9E3779B97F4A7C15ull + 17));
+    init_normal_kernel<<<blocks_for(static_cast<long long>(rows) * cols, 256), 256, 0, s>>>(dst, rows, cols, ld, base,
+                                                                                           r0, c0, C, std);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_init_gateup(__nv_bfloat16* dst, int ffn_local, int hidden, uint64_t seed, uint64_t gate_id, uint64_t up_id,
+                        int64_t f0, float std, cudaStream_t s) {
+    const unsigned long long gb = mix(seed ^ mix(gate_id * 0x9E3779B97F4A7C15ull + 17));
+    const unsigned long long ub = mix(seed ^ mix(up_id * 0x9E3779B97F4A7C15ull + 17));
+    init_gateup_kernel<<<blocks_for(2LL * ffn_local * hidden, 256), 256, 0, s>>>(dst, ffn_local, hidden, gb, ub, f0,
+                                                                                 std);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_fill(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t s) {
+    fill_kernel<<<blocks_for(n, 256), 256, 0, s>>>(dst, n, v);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_forward_begin(LaneState* lane, cudaStream_t s) {
+    forward_begin_kernel<<<1, 1, 0, s>>>(lane);
+    CUDA_LAUNCH_CHECK();
+}
+void launch_forward_end(LaneState* lane, cudaStream_t s) {
+    forward_end_kernel<<<1, 1, 0, s>>>(lane);
+    CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace dbl

@@ -19,8 +19,9 @@ class Transformer final : public Model {
     std::string kind() const override { return "transformer"; }
     void get_weight(const std::string& name, int layer, uint16_t* out, int64_t numel);
 
-  private:
     struct Impl;
+
+  private:
     Impl* impl_ = nullptr;
     dbl_transformer_config cfg_;
     int device_;

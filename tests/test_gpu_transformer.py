@@ -1,0 +1,132 @@
+"""GPU: the transformer verify forward against a plain PyTorch fp32 reference (logits within a stated
+tolerance), batch invariance of the forward (bitwise), and the decode-loop contract on transformer
+models — lossless identity with target-only greedy AR and decision replay through the oracle loop."""
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# Logit tolerance vs the fp32 reference: |gpu - ref| <= ATOL_REL * max|ref| (bf16 rounding points are
+# shared; the residual differences are fp32 summation order inside the tensor-core K loop and
+# occasional one-ulp bf16 flips of intermediates).
+ATOL_REL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def dbl():
+    import paper_2601_05524_b200 as dbl
+    assert dbl._capi.lib().dbl_device_ok() == 1
+    return dbl
+
+
+def make(dbl, name, seed, max_seq=2048):
+    cfg = dbl.transformer_config(name, seed=seed, max_seq=max_seq)
+    return dbl.Transformer(cfg), cfg
+
+
+@pytest.mark.parametrize("name", ["tiny-qwen", "tiny-llama"])
+def test_logits_match_fp32_reference(dbl, name):
+    from ref_transformer import RefTransformer
+    m, cfg = make(dbl, name, 3)
+    ref = RefTransformer(m, cfg)
+    rng = random.Random(1)
+    for L, c in ((1, 0), (5, 3), (40, 10), (300, 12)):
+        ctx = [rng.randrange(cfg.vocab) for _ in range(L)]
+        cands = [rng.randrange(cfg.vocab) for _ in range(c)]
+        got = dbl.forward_logits(m, ctx, cands)
+        want = ref.logits(ctx + cands)[L - 1:].numpy()
+        err = np.abs(got - want).max()
+        assert err <= ATOL_REL * np.abs(want).max(), (L, c, err, np.abs(want).max())
+        am = dbl.forward_batch(m, ctx, cands)
+        assert am == got.argmax(axis=1).tolist()
+
+
+def test_forward_batch_invariance(dbl):
+    """Row k of one batched forward == the single-row forward of ctx ⊕ cands[:k] (bitwise)."""
+    m, cfg = make(dbl, "tiny-qwen", 5)
+    rng = random.Random(2)
+    ctx = [rng.randrange(cfg.vocab) for _ in range(70)]
+    cands = [rng.randrange(cfg.vocab) for _ in range(40)]
+    batched = dbl.forward_logits(m, ctx, cands)
+    for k in (0, 1, 7, 16, 17, 33, 40):
+        single = dbl.forward_logits(m, ctx + cands[:k], [])
+        assert np.array_equal(single[0], batched[k]), k
+
+
+def _prior(vocab, seed, n=10):
+    rng = random.Random(seed)
+    base = [rng.randrange(1, vocab - 1) for _ in range(40)]
+    out = []
+    for i in range(n):  # repetitive code-like stream: replays of a few motifs
+        s = []
+        while len(s) < 64:
+            s += base[rng.randrange(0, 30):][: rng.randrange(4, 12)] if rng.random() < 0.7 else \
+                [rng.randrange(1, vocab - 1) for _ in range(3)]
+        out.append(s[:64])
+    return out
+
+
+@pytest.mark.parametrize("gamma,depth", [(1, 4), (3, 10), (6, 10)])
+def test_double_equals_target_only_ar(dbl, gamma, depth):
+    """Lossless identity (the reference's master property, test_pipeline.cpp:57-72) with transformers."""
+    tgt, tcfg = make(dbl, "tiny-qwen", 11)
+    drf, _ = make(dbl, "tiny-qwen-draft", 12)
+    prior = _prior(tcfg.vocab, 4)
+    prompt = prior[0][:24]
+    st = dbl.HierarchicalDatastore(3, depth)
+    dbl.build_prior(st, prior, 10)
+    r = dbl.run(drf, tgt, st, prompt, 160, dbl.PipelineOptions(gamma=gamma, depth=depth))
+    ar = dbl.run_vanilla_ar(tgt, prompt, 160)
+    assert r.output == ar.output
+    assert r.metrics["tokens"] >= len(ar.output)
+
+
+def test_self_draft_accepts_everything(dbl):
+    """draft == target (alpha = 1): every speculative token verifies; output still == AR."""
+    tgt, tcfg = make(dbl, "tiny-qwen", 21)
+    st = dbl.HierarchicalDatastore(3, 10)
+    prompt = list(range(1, 30))
+    r = dbl.run(tgt, tgt, st, prompt, 120, dbl.PipelineOptions(gamma=4, depth=10))
+    ar = dbl.run_vanilla_ar(tgt, prompt, 120)
+    assert r.output == ar.output
+    assert not any(t["pending_reject"] for t in r.traces)
+
+
+def test_decision_replay_through_oracle_loop(dbl, oracle):
+    """The device loop's traces == the oracle restatement of run() (pipeline.cpp) driven by the same
+    GPU forward as a stateless callback: retrieval hits, drafted candidates, commits — bit-exact."""
+    from oracle.pyoracle import make_argmax_callback
+    tgt, tcfg = make(dbl, "tiny-qwen", 31)
+    drf, _ = make(dbl, "tiny-qwen-draft", 32)
+    prior = _prior(tcfg.vocab, 9)
+    prompt = prior[1][:16]
+    for gamma, depth in ((2, 10), (4, 5)):
+        st = dbl.HierarchicalDatastore(3, depth)
+        dbl.build_prior(st, prior, 10)
+        r = dbl.run(drf, tgt, st, prompt, 64, dbl.PipelineOptions(gamma=gamma, depth=depth))
+        ost = oracle.store(3, depth)
+        for i, s in enumerate(prior):
+            ost.insert(0, s, i)
+        tcb = make_argmax_callback(lambda ctx, c: dbl.forward_batch(tgt, ctx, c))
+        dcb = make_argmax_callback(lambda ctx, c: dbl.forward_batch(drf, ctx, c))
+        out, js, met = oracle.run(tcfg.vocab, dcb, tcfg.vocab, tcb, ost, prompt, 64, gamma=gamma, depth=depth)
+        assert r.output == out
+        assert hashlib.sha256(r.jsonl.encode()).hexdigest() == hashlib.sha256(js.encode()).hexdigest()
+        assert r.metrics["lookups"] == met[7]
+
+
+def test_long_prompt_prefill_chunks(dbl):
+    """Prompts longer than one 256-token forward are prefetched in chunks; rows are unchanged."""
+    m, cfg = make(dbl, "tiny-llama", 8)
+    rng = random.Random(4)
+    ctx = [rng.randrange(cfg.vocab) for _ in range(700)]
+    a = dbl.forward_logits(m, ctx, [5, 6])
+    b = dbl.forward_logits(m, ctx + [5], [6])
+    assert np.array_equal(a[1:], b)
+    ar = dbl.run_vanilla_ar(m, ctx, 20)
+    st = dbl.HierarchicalDatastore(3, 10)
+    r = dbl.run(m, m, st, ctx, 20, dbl.PipelineOptions(gamma=2))
+    assert r.output == ar.output
