@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""bench.py — the DOUBLE decode loop on B200 (BASELINE.json: decode tokens/s + speedup vs target-only
+AR + mean accepted length).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N=1 workload = BASELINE.json configs[1]: Qwen3-0.6B draft / Qwen3-14B target shapes, random-init
+bf16, synthetic code-like prompt (HumanEval length, 160 tokens), 256 new tokens, greedy, d=10, N=3,
+prior K=10.  A "step" is one complete DOUBLE decode of that request.  N>1 runs N independent replicas
+(one per GPU, weak scaling; the target-TP path is DESIGN.md's next row) with max-over-ranks timing.
+
+value          decode tokens/s of the DOUBLE loop with the weights/KV resident in HBM (CUDA events
+               around the device decode loop, prompt prefill excluded), summed over ranks
+e2e            the same metric through the public C-ABI (dbl_run) with host prompt/prior in and host
+               tokens out, prefill and all copies inside the timed region (CUDA events)
+speedup_vs_ar  value / target-only greedy AR tokens/s with the same kernels (run_vanilla_ar)
+roofline       the verify-forward GEMMs (tcgen05 gemm_kernel): algorithmic bytes / event-timed
+               duration per launch vs MEASURED_PEAKS.json hbm_gbs
+cpu_baseline   the reference's own host decode loop (oracle/_ref, unmodified run()) replaying this
+               run's decision log — the forward is excluded (a transformer forward does not exist in
+               the reference); 1 host core
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # configs[1]: 1 x B200
+    "qwen3-0.6b/qwen3-14b": dict(draft="qwen3-0.6b", target="qwen3-14b", prompt_len=160, max_new=256),
+    # small smoke workload (CI / quick checks)
+    "tiny": dict(draft="tiny-qwen-draft", target="tiny-qwen", prompt_len=64, max_new=64),
+}
+DEPTH, NGRAM, PRIOR_K = 10, 3, 10
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", default="qwen3-0.6b/qwen3-14b", choices=list(WORKLOADS))
+    p.add_argument("--gamma", type=int, default=0, help="0 = ceil(C), C = t_target_fwd / t_draft_fwd")
+    p.add_argument("--max-new", type=int, default=0)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--log-out", default="", help="write this run's decision log (json) here")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------- synthetic workload
+def code_like_stream(vocab: int, n: int, seed: int, rho: float = 0.9):
+    """A repetitive 'code-like' token stream: fresh 1-4 token spans mixed with replays (prob rho) of
+    4-16 token spans of the stream so far — the recipe of gen_corpus (harness.cpp:151-186) with a
+    numpy RNG.  Tokens avoid BOS (0) and EOS (vocab-1)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    s = []
+    while len(s) < n:
+        if len(s) >= 4 and rng.random() < rho:
+            span = 4 + int(rng.random() * 13)
+            st = int(rng.random() * len(s))
+            s.extend(s[st:min(st + span, len(s))])
+        else:
+            s.extend(int(x) for x in rng.integers(1, vocab - 1, 1 + int(rng.random() * 4)))
+    return s[:n]
+
+
+def workload(vocab, prompt_len, seed):
+    stream = code_like_stream(vocab, 64 * PRIOR_K + 4096, seed)
+    corpus = [stream[i:i + 64] for i in range(0, len(stream), 64)]
+    return stream[:prompt_len], corpus[:PRIOR_K]
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, device: int):
+        self.device, self.lines, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- distributed plumbing
+def dist_init(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def all_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def all_sum(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def reference_replay(log, vocab, prompt, prior, max_new, gamma, target_tokens, reps=1):
+    """Replay the decision log through the reference's unmodified host loop (oracle/_ref) — or the
+    oracle port when the reference library was not built — and time it on one host core."""
+    import ctypes as C
+    import numpy as np
+    from oracle.pyoracle import ARGMAX_FN, Oracle, reference_or_none
+    orc = Oracle()
+    L = orc.lib
+    L.orc_replay_new.restype = C.c_void_p
+    L.orc_replay_new.argtypes = [C.POINTER(C.c_int), C.c_long]
+    L.orc_replay_reset.argtypes = [C.c_void_p]
+    L.orc_replay_free.argtypes = [C.c_void_p]
+    arr = np.ascontiguousarray(np.asarray(log, dtype=np.int32))
+    rp = L.orc_replay_new(arr.ctypes.data_as(C.POINTER(C.c_int)), len(arr))
+    dfn = ARGMAX_FN(C.cast(L.orc_replay_draft, C.c_void_p).value)
+    tfn = ARGMAX_FN(C.cast(L.orc_replay_target, C.c_void_p).value)
+    ref = reference_or_none()
+    kind = "reference" if ref is not None else "port"
+    times, out = [], None
+    for _ in range(reps):
+        L.orc_replay_reset(rp)
+        t0 = time.perf_counter()
+        if ref is not None:
+            n = C.c_int()
+            buf = (C.c_int * (max_new + 8))()
+            js = C.create_string_buffer(1 << 22)
+            met = (C.c_double * 8)()
+            flat = [t for s in prior for t in s]
+            rc = ref.lib.ref_run_callback(
+                vocab, dfn, C.c_void_p(rp), tfn, C.c_void_p(rp), NGRAM, len(prior),
+                (C.c_int * len(prior))(*[len(s) for s in prior]), (C.c_int * len(flat))(*flat),
+                (C.c_int * len(prompt))(*prompt), len(prompt), max_new, gamma, DEPTH, 1, 1, 1,
+                1.0, 1.0, 0.0, 0.0, buf, max_new + 8, C.byref(n), js, len(js), met)
+            if rc:
+                raise RuntimeError(ref.lib.ref_last_error().decode())
+            out = list(buf[:n.value])
+        else:
+            st = orc.store(NGRAM, DEPTH)
+            for i, s in enumerate(prior):
+                st.insert(0, s, i)
+            out, _, _ = orc.run(vocab, dfn, vocab, tfn, st, prompt, max_new, gamma=gamma, depth=DEPTH,
+                                t_draft=1.0, duser=rp, tuser=rp)
+        times.append(time.perf_counter() - t0)
+    L.orc_replay_free(rp)
+    if out != target_tokens:
+        raise RuntimeError("reference replay diverged from the device run (parity failure)")
+    return len(out) / min(times), kind
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    a = parse()
+    rank, world, local = dist_init(a.gpus)
+    wl = dict(WORKLOADS[a.workload])
+    max_new = a.max_new or wl["max_new"]
+    metric = "decode tokens/s (DOUBLE, greedy) + speedup vs target-only AR + mean accepted length"
+    base_cfg = {"workload": f"{a.workload} (configs[1]: Qwen3-0.6B draft / Qwen3-14B target shapes, "
+                f"random-init bf16, synthetic code-like prompt)" if a.workload != "tiny" else a.workload,
+                "prompt_len": wl["prompt_len"], "max_new_tokens": max_new, "depth": DEPTH,
+                "ngram": NGRAM, "prior_rounds": PRIOR_K, "temperature": 0,
+                "parallelism": f"replicas x{world}" if world > 1 else "1 GPU (draft+target co-located)",
+                "l2": "weights (28 GB) >> L2 (126 MB): every forward streams from HBM"}
+
+    if a.impl == "reference":
+        return reference_arm(a, rank, world, wl, max_new, metric, base_cfg)
+
+    import paper_2601_05524_b200 as dbl
+    from paper_2601_05524_b200 import _capi
+    import ctypes as C
+    if not _capi.lib().dbl_device_ok():
+        raise SystemExit("no usable sm_100 device (libdouble_b200 has no CPU fallback)")
+    dev = 0
+    import torch
+    torch.cuda.set_device(local)
+    dev_env = local  # the library follows the current device through cudaSetDevice in torch
+    tgt = dbl.Transformer(dbl.transformer_config(wl["target"], seed=a.seed, max_seq=4096), device=local)
+    drf = dbl.Transformer(dbl.transformer_config(wl["draft"], seed=a.seed + 1, max_seq=4096), device=local)
+    V = tgt.cfg.vocab
+    prompt, prior = workload(V, wl["prompt_len"], a.seed + 100 + rank * 0)
+
+    def profile(model, ctx, rows, iters=5):
+        out = (C.c_double * 8)()
+        _capi.check(_capi.lib().dbl_profile_forward(model._h, ctx, rows, iters, out))
+        return list(out)
+
+    # gamma = ceil(C), C = t_target_fwd / t_draft_fwd at M = d+1 (harness.cpp:32-35)
+    pt = profile(tgt, wl["prompt_len"], DEPTH + 1)
+    pd = profile(drf, wl["prompt_len"], DEPTH + 1)
+    C_ratio = pt[0] / pd[0]
+    gamma = a.gamma or max(1, math.ceil(C_ratio))
+    opts = dbl.PipelineOptions(gamma=gamma, depth=DEPTH)
+
+    def store():
+        st = dbl.HierarchicalDatastore(NGRAM, DEPTH, device=local)
+        dbl.build_prior(st, prior, PRIOR_K)
+        return st
+
+    def run_double():
+        return dbl.run(drf, tgt, store(), prompt, max_new, opts, want_jsonl=False)
+
+    for _ in range(a.warmup):
+        run_double()
+        dbl.run_vanilla_ar(tgt, prompt, max_new, want_jsonl=False)
+
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dev_ms, e2e_ms, tokens, launches = 0.0, 0.0, 0, 0
+    results = []
+    with ClockSampler(local) as clk:
+        for _ in range(a.steps):
+            torch.cuda.synchronize()
+            e0.record()
+            r = run_double()  # host prompt/prior in, host tokens out (e2e)
+            e1.record()
+            torch.cuda.synchronize()
+            e2e_ms += e0.elapsed_time(e1)
+            dev_ms += r.metrics["device_ms"]
+            tokens += len(r.output)
+            launches += r.metrics["kernel_launches"]
+            results.append(r)
+    torch.cuda.synchronize()
+    barrier(world)
+    log = dbl.last_run_log()
+    # target-only AR with the same kernels (the speedup denominator) + lossless check
+    ar_ms, ar_tok = 0.0, 0
+    for _ in range(a.steps):
+        ar = dbl.run_vanilla_ar(tgt, prompt, max_new, want_jsonl=False)
+        ar_ms += ar.metrics["device_ms"]
+        ar_tok += len(ar.output)
+    lossless = all(r.output == ar.output for r in results)
+
+    t_dev = all_max(dev_ms, world)
+    t_e2e = all_max(e2e_ms, world)
+    tok_all = all_sum(tokens, world)
+    value = tok_all / (t_dev / 1e3)
+    e2e_value = tok_all / (t_e2e / 1e3)
+    ar_value = all_sum(ar_tok, world) / (all_max(ar_ms, world) / 1e3)
+    m0 = results[-1].metrics
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    rows_per_fwd = max(1, round(m0["target_rows"] / max(1, m0["target_fwd_count"])))
+    pv = profile(tgt, wl["prompt_len"] + max_new // 2, rows_per_fwd, iters=5)
+    achieved = pv[2] / (pv[1] / 1e3) / 1e9  # GB/s over the verify GEMM launches
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        traffic = prof.get(a.workload)
+    except (OSError, ValueError):
+        pass
+    line = {
+        "metric": metric, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_dev / a.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, code-like prompt)",
+        "config": dict(base_cfg, gamma=gamma, C_measured=round(C_ratio, 3)),
+        "speedup_vs_ar": round(value / ar_value, 4), "ar_tokens_per_s": round(ar_value, 3),
+        "mean_accepted_len": round(m0["m"], 4), "amt": round(m0["amt"], 4),
+        "rounds_per_step": m0["rounds"], "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 3),
+        "lossless_vs_ar": lossless,
+        "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s",
+                "h2d_bytes_per_step": 4 * (len(prompt) + sum(len(s) for s in prior)),
+                "d2h_bytes_per_step": 4 * max_new},
+        "roofline": {"bound": "hbm", "kernel": "gemm_kernel (tcgen05 swap-AB stream-K), verify forward",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback",
+                     "per_forward": {"tokens": int(pv[5]), "fwd_ms": round(pv[0], 4), "gemm_ms": round(pv[1], 4),
+                                     "gemm_bytes": pv[2], "gemm_launches": int(pv[3]),
+                                     "kernel_launches": int(pv[4]),
+                                     "weight_stream_gbs": round(tgt.weight_bytes / (pv[0] / 1e3) / 1e9, 1)}},
+        "gpu_launches": int(all_sum(launches, world)),
+    }
+    cs = clk.summary()
+    line["clocks"] = {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"]}
+    if a.log_out and rank == 0:
+        json.dump({"vocab": V, "prompt": prompt, "prior": prior, "max_new": max_new, "gamma": gamma,
+                   "output": results[-1].output, "log": [int(x) for x in log]}, open(a.log_out, "w"))
+    if rank == 0:
+        try:
+            cpu_v, kind = reference_replay(log, V, prompt, prior, max_new, gamma, results[-1].output, reps=2)
+            line["cpu_baseline"] = {"value": round(cpu_v, 3), "unit": "tokens/s", "cores": 1, "kind": kind,
+                                    "sample": f"one {max_new}-token DOUBLE decode of this workload replayed "
+                                              "through the reference host loop (run(), pipeline.cpp) with the "
+                                              "forward excluded: argmax rows served from this run's decision "
+                                              "log as one-hot fp64 rows of V=151936 (argmax_token included)"}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+
+
+def reference_arm(a, rank, world, wl, max_new, metric, base_cfg):
+    """--impl reference: the reference's own CPU decode loop on this workload (forward excluded), from
+    the recorded decision log bench_data/<workload>.json (produced by this bench, --log-out)."""
+    if rank != 0:
+        return
+    path = os.path.join(ROOT, "bench_data", a.workload.replace("/", "_") + ".json")
+    try:
+        d = json.load(open(path))
+    except OSError:
+        print(json.dumps({"impl": "reference", "unavailable": f"no recorded decision log at {path}"}))
+        return
+    times = []
+    vals = []
+    for _ in range(a.warmup):
+        reference_replay(d["log"], d["vocab"], d["prompt"], d["prior"], d["max_new"], d["gamma"], d["output"])
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        v, kind = reference_replay(d["log"], d["vocab"], d["prompt"], d["prior"], d["max_new"], d["gamma"],
+                                   d["output"])
+        times.append(time.perf_counter() - t0)
+        vals.append(v)
+    value = statistics.median(vals)
+    print(json.dumps({
+        "impl": "reference", "metric": metric, "value": round(value, 3), "unit": "tokens/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(1e3 * statistics.median(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (recorded decision log)",
+        "config": dict(base_cfg, gamma=d["gamma"]),
+        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": 1, "kind": kind,
+                         "sample": f"{d['max_new']}-token DOUBLE decode replayed through the reference host "
+                                   "loop (forward excluded)"},
+        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -137,6 +137,11 @@ typedef struct { /* RunMetrics (pipeline.hpp:73-82) + device timing */
 int dbl_run(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
             int n_prompt, int max_new, const dbl_pipeline_options* opts, int32_t* out, int cap,
             int* n_out, dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len);
+/* The decision log of this thread's last dbl_run: the argmax rows the loop consumed, per round
+ * n_segs, {matched, emitted[matched+1]} x n_segs, n_spec, rej, correction, ext_matched,
+ * ext_emitted[ext_matched+1].  Used to replay the reference's own host loop with the forward
+ * excluded (bench.py cpu_baseline / --impl reference).  len receives the full length. */
+int dbl_last_run_log(int32_t* buf, int64_t cap, int64_t* len);
 /* run_vanilla_ar (harness.cpp:233-258), greedy: target-only, one forward per token */
 int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
@@ -152,6 +157,12 @@ int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, 
  * dbl_debug_gemm: W [n_out x K] bf16 bits, X [T x K] bf16 bits, padded to tp token columns.
  *   epi 0 StoreBF16 / 4 StoreF32 -> io[T x n_out]; 1 ResidAdd -> io[T x n_out] += W X^T;
  *   2 SiluMul (16 gate | 16 up rows per 32) -> io[T x n_out/2]; 3 Argmax -> argmax[T], io = logits. */
+/* Times one model forward of `rows` tokens after a ctx_len context (CUDA events, `iters` repeats):
+ * out[8] = forward ms, GEMM ms, GEMM algorithmic bytes, GEMM launches, kernel launches (per
+ * forward), token columns, LM-head GEMM ms, LM-head bytes.  Feeds bench.py's roofline. */
+int dbl_profile_forward(dbl_model_t m, int ctx_len, int rows, int iters, double* out);
+/* back-to-back launches of one GEMM shape, ms per launch (weights rotate over `chain` copies) */
+int dbl_debug_gemm_bench(int epi, int n_out, int K, int tp, int iters, int chain, double* ms_per_launch);
 int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,
                    int n_valid, float* io, int32_t* argmax);
 

@@ -144,7 +144,7 @@ class Oracle:
 
     def run(self, draft_vocab, draft_cb, target_vocab, target_cb, store: "Store", prompt, max_new,
             gamma=4, depth=10, draft_retrieval=True, target_retrieval=True, t_target=1.0,
-            t_draft=0.25, t_lookup=0.0, t_sync=0.0, cap=1 << 16):
+            t_draft=0.25, t_lookup=0.0, t_sync=0.0, cap=1 << 16, duser=None, tuser=None):
         class Opts(C.Structure):
             _fields_ = [("gamma", C.c_int), ("depth", C.c_int), ("dr", C.c_int), ("tr", C.c_int),
                         ("t_target", C.c_double), ("t_draft", C.c_double),
@@ -155,7 +155,7 @@ class Oracle:
         n = C.c_int()
         js = C.c_void_p()
         m = (C.c_double * 8)()
-        if self.lib.orc_run(draft_vocab, draft_cb, None, target_vocab, target_cb, None, store.h,
+        if self.lib.orc_run(draft_vocab, draft_cb, duser, target_vocab, target_cb, tuser, store.h,
                             _ints(prompt), len(prompt), max_new, C.byref(o), out, cap, C.byref(n),
                             C.byref(js), m):
             self._err()

@@ -1159,3 +1159,73 @@ done:
     free(toks); free(lens);
     return rc;
 }
+
+/* ------------------------------------------------------------------ replay models (bench only) */
+typedef struct { int matched; int off; } rseg;
+typedef struct { int seg0, nseg, n_spec, rej, corr, ext_m, ext_off; } rround;
+struct orc_replay {
+    int* data; long len;
+    rround* rounds; long n_rounds;
+    rseg* segs; long n_segs;
+    long dr, ds, tr; /* cursors: draft round/seg, target round */
+};
+
+orc_replay* orc_replay_new(const int* log, long len) {
+    orc_replay* r = (orc_replay*)calloc(1, sizeof *r);
+    r->data = (int*)malloc((size_t)(len ? len : 1) * sizeof(int));
+    memcpy(r->data, log, (size_t)len * sizeof(int));
+    r->len = len;
+    long cap_r = 64, cap_s = 256, at = 0;
+    r->rounds = (rround*)malloc((size_t)cap_r * sizeof(rround));
+    r->segs = (rseg*)malloc((size_t)cap_s * sizeof(rseg));
+    while (at < len) {
+        if (r->n_rounds == cap_r) { cap_r *= 2; r->rounds = (rround*)realloc(r->rounds, (size_t)cap_r * sizeof(rround)); }
+        rround* rd = &r->rounds[r->n_rounds++];
+        rd->nseg = log[at++];
+        rd->seg0 = (int)r->n_segs;
+        for (int j = 0; j < rd->nseg; ++j) {
+            if (r->n_segs == cap_s) { cap_s *= 2; r->segs = (rseg*)realloc(r->segs, (size_t)cap_s * sizeof(rseg)); }
+            rseg* sg = &r->segs[r->n_segs++];
+            sg->matched = log[at++];
+            sg->off = (int)at;
+            at += sg->matched + 1;
+        }
+        rd->n_spec = log[at++];
+        rd->rej = log[at++];
+        rd->corr = log[at++];
+        rd->ext_m = log[at++];
+        rd->ext_off = (int)at;
+        at += rd->ext_m + 1;
+    }
+    return r;
+}
+void orc_replay_free(orc_replay* r) {
+    if (!r) return;
+    free(r->data); free(r->rounds); free(r->segs); free(r);
+}
+void orc_replay_reset(orc_replay* r) { r->dr = r->ds = r->tr = 0; }
+
+int orc_replay_draft(void* user, const int* ctx, int L, const int* cands, int c, int* out) {
+    (void)ctx; (void)L;
+    orc_replay* r = (orc_replay*)user;
+    while (r->dr < r->n_rounds && r->ds >= r->rounds[r->dr].nseg) { r->dr++; r->ds = 0; }
+    if (r->dr >= r->n_rounds) return fail("replay: draft log exhausted");
+    const rseg* sg = &r->segs[r->rounds[r->dr].seg0 + r->ds++];
+    const int m = sg->matched;
+    const int e = r->data[sg->off + m];
+    for (int s = 0; s <= c; ++s) out[s] = s < m ? cands[s] : e;
+    return 0;
+}
+
+int orc_replay_target(void* user, const int* ctx, int L, const int* cands, int c, int* out) {
+    (void)ctx; (void)L;
+    orc_replay* r = (orc_replay*)user;
+    if (r->tr >= r->n_rounds) return fail("replay: target log exhausted");
+    const rround* rd = &r->rounds[r->tr++];
+    for (int k = 0; k < rd->n_spec && k <= c; ++k)
+        out[k] = (rd->rej < 0 || k < rd->rej) ? cands[k] : rd->corr;
+    const int e = r->data[rd->ext_off + rd->ext_m];
+    for (int s = 0; rd->n_spec + s <= c; ++s)
+        out[rd->n_spec + s] = s < rd->ext_m ? cands[rd->n_spec + s] : e;
+    return 0;
+}

@@ -86,6 +86,15 @@ int orc_run_ar(int target_vocab, orc_argmax_fn tfn, void* tuser, const int* prom
 int orc_run_config(const char* cfg_text, const char* method, int* out_tokens, int cap, int* n_out,
                    char** jsonl, double* metrics);
 
+/* Replay models: serve the argmax rows a device run consumed (its decision log, dbl_last_run_log)
+ * so the reference/oracle host loop can be timed on the same workload with the forward excluded. */
+typedef struct orc_replay orc_replay;
+orc_replay* orc_replay_new(const int* log, long len);
+void orc_replay_free(orc_replay* r);
+void orc_replay_reset(orc_replay* r);
+int orc_replay_draft(void* replay, const int* ctx, int L, const int* cands, int c, int* out);
+int orc_replay_target(void* replay, const int* ctx, int L, const int* cands, int c, int* out);
+
 const char* orc_last_error(void);
 void orc_free(void* p);
 

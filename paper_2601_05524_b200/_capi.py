@@ -84,6 +84,9 @@ PROTOTYPES = {
     "dbl_run_serial_sd": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), C.c_int,
                           I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p,
                           C.c_int64, I64P],
+    "dbl_last_run_log": [I32P, C.c_int64, I64P],
+    "dbl_profile_forward": [VP, C.c_int, C.c_int, C.c_int, F64P],
+    "dbl_debug_gemm_bench": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, F64P],
     "dbl_debug_gemm": [C.c_int, U16P, C.c_int, C.c_int, U16P, C.c_int, C.c_int, C.c_int, F32P,
                        I32P],
 }

@@ -10,6 +10,7 @@
 #include "transformer.cuh"
 #include "gemm.cuh"
 #include "lane.cuh"
+#include "tf_kernels.cuh"
 #include <cuda_bf16.h>
 
 struct dbl_store_s {
@@ -21,6 +22,7 @@ struct dbl_model_s {
 
 namespace {
 thread_local std::string g_last_error;
+thread_local std::vector<int32_t> g_last_log;
 
 template <class F>
 int guarded(F&& f) {
@@ -63,6 +65,17 @@ int copy_run(const dbl::RunOutput& r, int32_t* out, int cap, int* n_out, dbl_run
 }  // namespace
 
 namespace dbl {
+long long& launch_counter() {
+    thread_local long long n = 0;
+    return n;
+}
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DBL_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 void require_device(int device) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
@@ -248,7 +261,17 @@ int dbl_run(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int3
         if (n_prompt > 0) need(prompt, "prompt");
         const dbl::RunOutput r = dbl::run_double(*draft->impl, *target->impl, *store->impl, prompt,
                                                  n_prompt, max_new, *opts);
+        g_last_log = r.log;
         copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+int dbl_last_run_log(int32_t* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        if (len) *len = static_cast<int64_t>(g_last_log.size());
+        if (buf) {
+            if (cap < static_cast<int64_t>(g_last_log.size())) dbl::throw_invalid("log buffer too small");
+            std::memcpy(buf, g_last_log.data(), g_last_log.size() * 4);
+        }
     });
 }
 int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
@@ -274,6 +297,59 @@ int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, 
         const dbl::RunOutput r = dbl::run_serial_sd(*draft->impl, *target->impl, *store->impl, prompt,
                                                     n_prompt, max_new, *opts, use_retrieval != 0);
         copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+
+int dbl_profile_forward(dbl_model_t m, int ctx_len, int rows, int iters, double* out) {
+    return guarded([&] {
+        need(m, "model");
+        need(out, "out");
+        dbl::profile_forward(*m->impl, ctx_len, rows, iters, out);
+    });
+}
+
+// Back-to-back launches of one GEMM shape (weights/activations resident): ms per launch.  With
+// `chain` > 1 the weights rotate over `chain` distinct copies (no L2 reuse between launches).
+int dbl_debug_gemm_bench(int epi, int n_out, int K, int tp, int iters, int chain, double* ms_per_launch) {
+    return guarded([&] {
+        using namespace dbl;
+        require_device(0);
+        chain = std::max(chain, 1);
+        std::vector<DevBuf<__nv_bfloat16>> W(chain);
+        std::vector<CUtensorMap> tW(chain);
+        for (int i = 0; i < chain; ++i) {
+            W[i].alloc(static_cast<size_t>(n_out) * K);
+            launch_init_normal(W[i].p, n_out, K, K, 7 + i, 1, 0, 0, K, 0.02f, 0);
+            tW[i] = make_tmap_bf16_2d(W[i].p, n_out, K, 128);
+        }
+        DevBuf<__nv_bfloat16> X(static_cast<size_t>(tp) * K);
+        launch_init_normal(X.p, tp, K, K, 3, 2, 0, 0, K, 1.0f, 0);
+        const CUtensorMap tX = make_tmap_bf16_2d(X.p, tp, K, 16);
+        GemmWorkspace ws;
+        ws.ensure(num_sms(0), tp, (n_out + 127) / 128);
+        const int cols = epi == 2 ? n_out / 2 : n_out;
+        DevBuf<float> o32(static_cast<size_t>(tp) * cols);
+        DevBuf<__nv_bfloat16> o16(static_cast<size_t>(tp) * cols);
+        o32.zero();
+        void* out = (epi == 0 || epi == 2) ? static_cast<void*>(o16.p) : static_cast<void*>(o32.p);
+        cudaStream_t s;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        for (int i = 0; i < 3; ++i)
+            gemm_launch(static_cast<Epi>(epi), tW[i % chain], tX, n_out, K, tp, n_out, out, cols, nullptr, 0, ws, s);
+        cudaEvent_t a, b;
+        CUDA_CHECK(cudaEventCreate(&a));
+        CUDA_CHECK(cudaEventCreate(&b));
+        CUDA_CHECK(cudaEventRecord(a, s));
+        for (int i = 0; i < iters; ++i)
+            gemm_launch(static_cast<Epi>(epi), tW[i % chain], tX, n_out, K, tp, n_out, out, cols, nullptr, 0, ws, s);
+        CUDA_CHECK(cudaEventRecord(b, s));
+        CUDA_CHECK(cudaStreamSynchronize(s));
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+        *ms_per_launch = ms / iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(s);
     });
 }
 

@@ -28,7 +28,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     }
 }
 #define CUDA_CHECK(x) ::dbl::cuda_check((x), #x, __FILE__, __LINE__)
-#define CUDA_LAUNCH_CHECK() ::dbl::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// every kernel launch in the library is followed by CUDA_LAUNCH_CHECK(), which also counts it
+// (dbl_run_metrics::kernel_launches, bench.py's gpu_launches)
+long long& launch_counter();
+#define CUDA_LAUNCH_CHECK()                                                                  \
+    do {                                                                                     \
+        ::dbl::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);          \
+        ++::dbl::launch_counter();                                                           \
+    } while (0)
 
 // RAII device buffer
 template <class T>

@@ -316,6 +316,7 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
     RunOutput res;
     Timer loop;
     CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    const long long launches0 = launch_counter();
     double tfwd_ms = 0.0;
     int64_t tfwd_n = 0, trows = 0;
     const int32_t eos = tm.vocab() - 1;
@@ -427,6 +428,21 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
         const double target_time = o.t_target + (o.target_retrieval ? o.t_lookup : 0.0);
         tr.clock_delta = std::max(draft_time, target_time) + o.t_sync;
         res.traces.push_back(std::move(tr));
+        {  // decision log (see RunOutput::log)
+            auto& lg = res.log;
+            lg.push_back(rr->n_segs);
+            int at = 0;
+            for (int j = 0; j < rr->n_segs; ++j) {
+                lg.push_back(rr->segs[j].matched);
+                lg.insert(lg.end(), chain + at, chain + at + rr->segs[j].n_emit);
+                at += rr->segs[j].n_emit;
+            }
+            lg.push_back(ns);
+            lg.push_back(rr->tgt_rej);
+            lg.push_back(rr->tgt_correction);
+            lg.push_back(rr->ext_matched);
+            lg.insert(lg.end(), ext, ext + ne);
+        }
 
         // ---- lane cursors for the next round (KV commit by length)
         std::vector<int32_t> X = committed;
@@ -473,6 +489,7 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
                                ? 0.0
                                : static_cast<double>(hits - base_hits) / static_cast<double>(res.metrics.lookups);
     res.metrics.device_ms = loop.ms();
+    res.metrics.kernel_launches = launch_counter() - launches0;
     res.metrics.prefill_ms = pre.ms();
     res.metrics.target_fwd_ms = tfwd_ms;
     res.metrics.target_fwd_count = tfwd_n;
@@ -520,6 +537,7 @@ RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, do
     CUDA_CHECK(cudaEventRecord(pre.b, S.main));
     tl.set_state(n_prompt, 0, tl.kv_len, n_prompt - 1, S.main);
     CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    const long long launches0 = launch_counter();
     RunOutput res;
     const int32_t eos = tm.vocab() - 1;
     int produced = 0;
@@ -554,6 +572,7 @@ RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, do
     res.metrics.clock = static_cast<double>(res.metrics.tokens) * t_target;  // harness.cpp:254-256
     res.metrics.speedup = 1.0;
     res.metrics.device_ms = loop.ms();
+    res.metrics.kernel_launches = launch_counter() - launches0;
     res.metrics.prefill_ms = pre.ms();
     res.metrics.target_fwd_count = produced;
     res.metrics.target_rows = produced;
@@ -587,6 +606,7 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
     RunOutput res;
     Timer loop;
     CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    const long long launches0 = launch_counter();
     const int32_t eos = tm.vocab() - 1;
     long round = 0;
     size_t scanned = n_prompt;
@@ -677,6 +697,7 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
                                ? 0.0
                                : static_cast<double>(hits - base_hits) / static_cast<double>(res.metrics.lookups);
     res.metrics.device_ms = loop.ms();
+    res.metrics.kernel_launches = launch_counter() - launches0;
     return res;
 }
 
@@ -716,6 +737,53 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     CUDA_CHECK(cudaStreamSynchronize(S.main));
     for (int i = 0; i <= c; ++i)
         if (out_argmax[i] < 0) throw_runtime("degenerate distribution");
+}
+
+// ------------------------------------------------------------------------ forward profiling
+void profile_forward(Model& m, int ctx_len, int rows, int iters, double* out) {
+    if (ctx_len < 1 || rows < 1 || iters < 1) throw_invalid("profile_forward: bad arguments");
+    DeviceGuard g(m.device());
+    Streams S;
+    Lane lane(m, ctx_len + rows + 16);
+    LaneIO io(&lane);
+    std::vector<int32_t> X(ctx_len + rows);
+    for (size_t i = 0; i < X.size(); ++i) X[i] = static_cast<int32_t>((i * 7919 + 13) % m.vocab());
+    io.sync_tokens(X, S.main);
+    catch_up(lane, ctx_len - 1, S.main);
+    lane.set_state(ctx_len, rows - 1, lane.kv_len, ctx_len - 1, S.main);
+    for (int i = 0; i < 2; ++i) m.forward(lane, rows, S.main);  // warm-up
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    // pass 1: whole-forward time (no per-GEMM events)
+    Timer t;
+    const long long l0 = launch_counter();
+    CUDA_CHECK(cudaEventRecord(t.a, S.main));
+    for (int i = 0; i < iters; ++i) m.forward(lane, rows, S.main);
+    CUDA_CHECK(cudaEventRecord(t.b, S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    const long long launches = launch_counter() - l0;
+    // pass 2: per-GEMM CUDA events on the launching stream
+    GemmProfiler prof;
+    m.set_profiler(&prof);
+    for (int i = 0; i < iters; ++i) m.forward(lane, rows, S.main);
+    m.set_profiler(nullptr);
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    double gemm_ms = 0.0, bytes = 0.0, lm_ms = 0.0, lm_bytes = 0.0;
+    const size_t per_fwd = prof.bytes.size() / iters;
+    for (size_t k = 0; k < prof.bytes.size(); ++k) {
+        float ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, prof.ev[2 * k], prof.ev[2 * k + 1]));
+        gemm_ms += ms;
+        bytes += prof.bytes[k];
+        if (per_fwd && k % per_fwd == per_fwd - 1) { lm_ms += ms; lm_bytes += prof.bytes[k]; }
+    }
+    out[0] = t.ms() / iters;                          // forward ms
+    out[1] = gemm_ms / iters;                          // GEMM ms per forward (event-timed launches)
+    out[2] = bytes / iters;                            // GEMM algorithmic bytes per forward
+    out[3] = static_cast<double>(per_fwd);             // GEMM launches per forward
+    out[4] = static_cast<double>(launches) / iters;    // kernel launches per forward
+    out[5] = static_cast<double>((rows + 15) / 16 * 16);  // token columns (tp)
+    out[6] = lm_ms / iters;                            // LM-head GEMM ms
+    out[7] = lm_bytes / iters;                         // LM-head GEMM bytes
 }
 
 }  // namespace dbl

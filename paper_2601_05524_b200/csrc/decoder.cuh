@@ -27,6 +27,11 @@ struct RunOutput {
     std::vector<int32_t> output;
     std::vector<Trace> traces;
     dbl_run_metrics metrics{};
+    // Decision log (argmax rows the loop consumed), per round:
+    //   n_segs, {matched, emitted[matched+1]} x n_segs, n_spec, rej, correction, ext_matched,
+    //   ext_emitted[ext_matched+1]
+    // It lets the reference loop be replayed on the host with the forward excluded (bench.py).
+    std::vector<int32_t> log;
 };
 
 std::string traces_to_jsonl(const std::vector<Trace>& traces);
@@ -37,6 +42,9 @@ RunOutput run_double(Model& draft, Model& target, DeviceStore& store, const int3
 RunOutput run_ar(Model& target, const int32_t* prompt, int n_prompt, int max_new, double t_target);
 RunOutput run_serial_sd(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
                         int n_prompt, int max_new, const dbl_pipeline_options& o, bool use_retrieval);
+
+// forward of `rows` tokens after a ctx_len context, timed (out[8], see decoder.cu)
+void profile_forward(Model& m, int ctx_len, int rows, int iters, double* out);
 
 // forward_batch as a stateless call (fresh lane / KV): argmax rows (c+1) and optionally logits
 void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,

@@ -7,6 +7,7 @@
 
 #include "gemm.cuh"
 #include "lane.cuh"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace dbl {
@@ -16,6 +17,7 @@ namespace {
 constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps 2..5 epilogue
 constexpr int kBlockM = 128, kBlockK = 64;
 constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KiB
+constexpr int kMaxBatchContrib = 8;             // split-K fan-in reduced with batched loads
 
 __device__ __forceinline__ long long range_begin(long long c, long long U, long long G) { return c * U / G; }
 // CTA whose range contains unit u: largest c with floor(cU/G) <= u
@@ -24,7 +26,7 @@ __device__ __forceinline__ long long cta_of(long long u, long long U, long long 
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmArgs a) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -65,24 +67,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
+    griddep_launch_dependents();  // PDL: the next kernel may start its prologue / weight prefetch
 
     if (warp == 0) {
         if (lane == 0) {  // ------------------------------------------------ TMA producer
-            int stage = 0;
-            uint32_t phase = 0;
-            for (long long u = b0; u < b1;) {
-                const int m = static_cast<int>(u / KB), kb0 = static_cast<int>(u % KB);
-                const int kb1 = static_cast<int>(std::min<long long>(KB, kb0 + (b1 - u)));
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
-                    tma_load_2d(sA + stage * kABytes, &tmW, &full[stage], kb * kBlockK, m * kBlockM, kEvictFirst);
-                    for (int j = 0; j < tp / 16; ++j)
-                        tma_load_2d(sB + stage * b_bytes + j * 2048, &tmX, &full[stage], kb * kBlockK, j * 16,
-                                    kEvictLast);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
-                }
-                u += kb1 - kb0;
+            // The weights never depend on the previous kernel: prefetch the first S stages' weight
+            // tiles BEFORE the grid-dependency wait (overlapping the previous kernel's tail), then
+            // wait and fetch the activation tiles.
+            const long long n_units = b1 - b0;
+            const int pre = static_cast<int>(std::min<long long>(S, n_units));
+            for (int i = 0; i < pre; ++i) {
+                const long long u = b0 + i;
+                mbar_arrive_expect_tx(&full[i], kABytes + b_bytes);
+                tma_load_2d(sA + i * kABytes, &tmW, &full[i], static_cast<int>(u % KB) * kBlockK,
+                            static_cast<int>(u / KB) * kBlockM, kEvictFirst);
+            }
+            griddep_wait();
+            for (int i = 0; i < pre; ++i) {
+                const int kb = static_cast<int>((b0 + i) % KB);
+                for (int j = 0; j < tp / 16; ++j)
+                    tma_load_2d(sB + i * b_bytes + j * 2048, &tmX, &full[i], kb * kBlockK, j * 16, kEvictLast);
+            }
+            int stage = pre % S;
+            uint32_t phase = pre == S ? 1u : 0u;
+            for (long long u = b0 + pre; u < b1; ++u) {
+                const int m = static_cast<int>(u / KB), kb = static_cast<int>(u % KB);
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
+                tma_load_2d(sA + stage * kABytes, &tmW, &full[stage], kb * kBlockK, m * kBlockM, kEvictFirst);
+                for (int j = 0; j < tp / 16; ++j)
+                    tma_load_2d(sB + stage * b_bytes + j * 2048, &tmX, &full[stage], kb * kBlockK, j * 16,
+                                kEvictLast);
+                if (++stage == S) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp == 1) {
@@ -134,49 +150,99 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[32];
                     tmem_ld32(taddr + ch, v);
                     const int nc = min(32, tp - ch);
-                    for (int i = 0; i < nc; ++i) __stcg(P + (ch + i) * kBlockM + r, v[i]);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < nc) __stcg(P + (ch + i) * kBlockM + r, v[i]);
                 }
-                __threadfence();
+                // publish: CTA barrier, then ONE gpu-scope fence + arrival (semaphore pattern)
                 named_bar_sync(1, 128);
-                if (et == 0) sflag[0] = atomicAdd(&a.counters[m], 1) == n_contrib - 1;
+                if (et == 0) {
+                    __threadfence();
+                    const bool last_in = atomicAdd(&a.counters[m], 1) == n_contrib - 1;
+                    if (last_in) {
+                        __threadfence();     // acquire the other contributors' partials
+                        a.counters[m] = 0;   // reusable by the next launch
+                    }
+                    sflag[0] = last_in;
+                }
                 named_bar_sync(1, 128);
                 finisher = sflag[0] != 0;
-                if (finisher) {
-                    __threadfence();
-                    if (et == 0) a.counters[m] = 0;  // reusable by the next launch
-                }
             }
             if (finisher) {
                 for (int ch = 0; ch < tp; ch += 32) {
                     float v[32];
                     tmem_ld32(taddr + ch, v);
                     const int nc = min(32, tp - ch);
-                    if (n_contrib > 1) {  // ordered sum p_0 + p_1 + ... (fixed for every token count)
+                    if (n_contrib > 1 && n_contrib <= kMaxBatchContrib) {
+                        // ordered sum p_0 + p_1 + ... with every contributor's loads of an 8-column
+                        // group in flight at once (one L2 round trip per group)
+                        const float* Pj[kMaxBatchContrib];
+#pragma unroll
+                        for (int j = 0; j < kMaxBatchContrib; ++j) {
+                            const long long cj = first + j;
+                            const long long bj = range_begin(cj, U, G);
+                            const int slot = static_cast<int>(2 * cj + (std::max(bj, tile_u0) == bj ? 0 : 1));
+                            Pj[j] = a.ws + static_cast<long long>(slot) * tp * kBlockM + ch * kBlockM + r;
+                        }
+#pragma unroll
+                        for (int g8 = 0; g8 < 32; g8 += 8) {
+                            if (g8 >= nc) break;
+                            float x[kMaxBatchContrib][8];
+#pragma unroll
+                            for (int j = 0; j < kMaxBatchContrib; ++j)
+#pragma unroll
+                                for (int i = 0; i < 8; ++i)
+                                    x[j][i] = (j < n_contrib && j != my && g8 + i < nc)
+                                                  ? __ldcg(Pj[j] + (g8 + i) * kBlockM) : v[g8 + i];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                float s = x[0][i];
+#pragma unroll
+                                for (int j = 1; j < kMaxBatchContrib; ++j)
+                                    if (j < n_contrib) s += x[j][i];
+                                v[g8 + i] = s;
+                            }
+                        }
+                    } else if (n_contrib > 1) {  // ordered sum p_0 + p_1 + ... (fixed for every token count)
                         float acc[32];
                         for (int j = 0; j < n_contrib; ++j) {
                             const long long cj = first + j;
                             const long long bj = range_begin(cj, U, G);
                             const int slot = static_cast<int>(2 * cj + (std::max(bj, tile_u0) == bj ? 0 : 1));
-                            const float* P = a.ws + static_cast<long long>(slot) * tp * kBlockM;
+                            const float* P = a.ws + static_cast<long long>(slot) * tp * kBlockM + ch * kBlockM + r;
+                            float x[32];
+                            if (j == my) {
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) {
-                                const float x = (j == my || i >= nc) ? v[i] : __ldcg(P + (ch + i) * kBlockM + r);
-                                acc[i] = j == 0 ? x : acc[i] + x;
+                                for (int i = 0; i < 32; ++i) x[i] = v[i];
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) x[i] = i < nc ? __ldcg(P + i * kBlockM) : 0.f;
                             }
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) acc[i] = j == 0 ? x[i] : acc[i] + x[i];
                         }
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = acc[i];
                     }
                     const int n = m * kBlockM + r;
                     if constexpr (EPI == static_cast<int>(Epi::StoreBF16)) {
-                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out);
-                        for (int i = 0; i < nc; ++i) o[static_cast<long long>(ch + i) * a.ld_out + n] = __float2bfloat16_rn(v[i]);
+                        __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(ch) * a.ld_out + n;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < nc) o[static_cast<long long>(i) * a.ld_out] = __float2bfloat16_rn(v[i]);
                     } else if constexpr (EPI == static_cast<int>(Epi::StoreF32)) {
-                        float* o = static_cast<float*>(a.out);
-                        for (int i = 0; i < nc; ++i) o[static_cast<long long>(ch + i) * a.ld_out + n] = v[i];
+                        float* o = static_cast<float*>(a.out) + static_cast<long long>(ch) * a.ld_out + n;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < nc) o[static_cast<long long>(i) * a.ld_out] = v[i];
                     } else if constexpr (EPI == static_cast<int>(Epi::ResidAdd)) {
-                        float* o = static_cast<float*>(a.out);
-                        for (int i = 0; i < nc; ++i) o[static_cast<long long>(ch + i) * a.ld_out + n] += v[i];
+                        float* o = static_cast<float*>(a.out) + static_cast<long long>(ch) * a.ld_out + n;
+                        float old[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) old[i] = i < nc ? o[static_cast<long long>(i) * a.ld_out] : 0.f;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < nc) o[static_cast<long long>(i) * a.ld_out] = old[i] + v[i];
                     } else if constexpr (EPI == static_cast<int>(Epi::SiluMul)) {
                         __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out);
                         const int f = m * 64 + q * 16 + lane;
@@ -193,8 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const bool ok = n < a.n_valid;
                         if (a.logits && ok) {  // only the forward's valid rows (the buffer holds no padding)
                             const int nrow = a.lane ? a.lane->L + a.lane->c - a.lane->start : tp;
-                            for (int i = 0; i < nc && ch + i < nrow; ++i)
-                                a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (i < nc && ch + i < nrow) a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
                         }
 #pragma unroll
                         for (int i = 0; i < 32; ++i) {
@@ -239,6 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // one warp per token row: reduce the per-tile (max, lowest idx) partials in tile order
 __global__ void argmax_finish_kernel(const float2* __restrict__ ws, int n_tiles, int tp, const LaneState* lane,
                                      int32_t* __restrict__ argmax) {
+    sm100::griddep_launch_dependents();
+    sm100::griddep_wait();
     const int start = lane->start;
     const int T = lane->L + lane->c - start;
     const int t = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -287,9 +356,20 @@ void set_smem_attr() {
 }  // namespace
 
 int num_sms(int device) {
+    static int cache[64] = {0};
+    if (device >= 0 && device < 64 && cache[device]) return cache[device];
     int n = 0;
     CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    if (device >= 0 && device < 64) cache[device] = n;
     return n;
+}
+
+void gemm_prepare() {
+    set_smem_attr<static_cast<int>(Epi::StoreBF16)>();
+    set_smem_attr<static_cast<int>(Epi::ResidAdd)>();
+    set_smem_attr<static_cast<int>(Epi::SiluMul)>();
+    set_smem_attr<static_cast<int>(Epi::Argmax)>();
+    set_smem_attr<static_cast<int>(Epi::StoreF32)>();
 }
 
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int box_rows) {
@@ -306,7 +386,8 @@ CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int
     return m;
 }
 
-void GemmWorkspace::ensure(int g, int mtp, int mtiles) {
+void GemmWorkspace::ensure(int sms, int mtp, int mtiles) {
+    const int g = 2 * sms + kMaxBatchContrib;  // split-K grids reach tiles * S < sms + tiles * 1
     if (g <= grid && mtp <= max_tp && mtiles <= max_tiles) return;
     grid = std::max(grid, g);
     max_tp = std::max(max_tp, mtp);
@@ -332,12 +413,31 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
     a.kb_total = K / kBlockK;
     a.units = static_cast<long long>(a.n_tiles) * a.kb_total;
     const int stage_bytes = kABytes + tp * kBlockK * 2;
-    const int budget = 227 * 1024 - 1024 - 2048;  // alignment slack + barriers/scratch (<= 1.3 KB)
+    // decode-sized forwards (tp <= 64): ~110 KB so two GEMM CTAs (consecutive kernels under PDL)
+    // co-reside on an SM and the next GEMM streams weights while this one drains; prefill-sized
+    // forwards take the whole SM for a deeper pipeline.
+    const int budget = (tp <= 64 ? 110 * 1024 : 227 * 1024) - 1024 - 2048;
     a.stages = std::max(2, std::min(12, budget / stage_bytes));
     const size_t smem = 1024 + static_cast<size_t>(a.stages) * stage_bytes + 2048;
     int dev = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
-    const int grid = static_cast<int>(std::min<long long>(num_sms(dev), a.units));
+    static const int grid_cap = [] {  // DBL_GEMM_GRID: debug override of the stream-K grid
+        const char* e = std::getenv("DBL_GEMM_GRID");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int sms = grid_cap > 0 ? std::min(grid_cap, num_sms(dev)) : num_sms(dev);
+    // Grid = a pure function of (n_out, K, #SMs) — never of tp — so split points (and numerics) are
+    // the same for every token count.  Few tiles: regular split-K, S aligned slices per tile (S =
+    // ceil(SMs / tiles) <= 8, the fan-in the finisher reduces with batched loads; up to 2 CTAs/SM).
+    // Many tiles: stream-K over one CTA per SM (<= 2-3 contributors per tile).
+    int grid;
+    if (a.n_tiles >= sms) {
+        grid = sms;
+    } else {
+        const int S = std::min({kMaxBatchContrib, (sms + a.n_tiles - 1) / a.n_tiles, a.kb_total});
+        grid = a.n_tiles * S;
+    }
+    grid = static_cast<int>(std::min<long long>(grid, a.units));
     if (ws.grid < grid || ws.max_tp < tp || ws.max_tiles < a.n_tiles)
         throw_runtime("GEMM workspace too small (call GemmWorkspace::ensure)");
     a.out = out;
@@ -349,10 +449,10 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
     a.ws = ws.partials.p;
     a.counters = ws.counters.p;
     switch (epi) {
-#define DBL_GEMM_CASE(E)                                                                   \
-    case E:                                                                                \
-        set_smem_attr<static_cast<int>(E)>();                                              \
-        gemm_kernel<static_cast<int>(E)><<<grid, kThreads, smem, s>>>(tmW, tmX, a);        \
+#define DBL_GEMM_CASE(E)                                                                     \
+    case E:                                                                                  \
+        set_smem_attr<static_cast<int>(E)>();                                                \
+        launch_pdl(gemm_kernel<static_cast<int>(E)>, dim3(grid), dim3(kThreads), smem, s, tmW, tmX, a); \
         break;
         DBL_GEMM_CASE(Epi::StoreBF16)
         DBL_GEMM_CASE(Epi::ResidAdd)
@@ -361,13 +461,12 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
         DBL_GEMM_CASE(Epi::StoreF32)
 #undef DBL_GEMM_CASE
     }
-    CUDA_LAUNCH_CHECK();
 }
 
 void argmax_finish(const GemmWorkspace& ws, int n_tiles, int tp, const LaneState* lane, int32_t* argmax,
                    cudaStream_t s) {
-    argmax_finish_kernel<<<(tp + 7) / 8, 256, 0, s>>>(ws.amax.p, n_tiles, tp, lane, argmax);
-    CUDA_LAUNCH_CHECK();
+    launch_pdl(argmax_finish_kernel, dim3((tp + 7) / 8), dim3(256), 0, s, static_cast<const float2*>(ws.amax.p),
+               n_tiles, tp, lane, argmax);
 }
 
 }  // namespace dbl

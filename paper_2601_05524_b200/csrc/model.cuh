@@ -18,6 +18,26 @@ struct LaneCache {
 
 class Lane;
 
+// Optional per-GEMM CUDA-event timing of a model's forwards (bench roofline; off in the decode loop)
+struct GemmProfiler {
+    std::vector<cudaEvent_t> ev;  // pairs (before, after) per GEMM launch
+    std::vector<double> bytes;    // algorithmic bytes of each timed GEMM (weights + activations)
+    size_t used = 0;
+    cudaEvent_t next(cudaStream_t s) {
+        if (used == ev.size()) {
+            cudaEvent_t e;
+            CUDA_CHECK(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+        cudaEvent_t e = ev[used++];
+        CUDA_CHECK(cudaEventRecord(e, s));
+        return e;
+    }
+    ~GemmProfiler() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 class Model {
   public:
     virtual ~Model() = default;
@@ -34,6 +54,7 @@ class Model {
     // order, to out_dev ((L+c-row0) x vocab).
     virtual void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) = 0;
     virtual int max_forward_tokens() const { return 1 << 30; }
+    virtual void set_profiler(GemmProfiler*) {}
     virtual std::string kind() const = 0;
 };
 

@@ -10,7 +10,7 @@
 namespace dbl {
 
 constexpr int kPage = 64;       // KV page (tokens)
-constexpr int kAttnChunk = 256; // keys per split-KV chunk (fixed => batch invariant)
+constexpr int kAttnChunk = 64;  // keys per split-KV chunk = one page (fixed => batch invariant)
 
 struct KVView {  // one layer of a lane's paged KV cache
     __nv_bfloat16* k;  // [n_pages][n_kv][kPage][hd]

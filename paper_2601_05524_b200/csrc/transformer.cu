@@ -12,7 +12,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include "gemm.cuh"
@@ -43,7 +45,10 @@ struct Transformer::Impl {
     const __nv_bfloat16* lm_head = nullptr;
     CUtensorMap t_lm;
     std::unique_ptr<TpComm> comm;
+    GemmProfiler* prof = nullptr;
 };
+
+void Transformer::set_profiler(GemmProfiler* p) { impl_->prof = p; }
 
 struct TfCache final : LaneCache {
     int capacity, pages, max_chunks;
@@ -54,7 +59,24 @@ struct TfCache final : LaneCache {
     CUtensorMap t_xn, t_attn, t_act;
     GemmWorkspace ws;
     size_t layer_stride = 0;
+    // one CUDA graph per token-column bucket: the whole forward (~370 kernels with programmatic
+    // dependent-launch edges) replays with a single launch; every argument is fixed per cache
+    std::map<int, cudaGraphExec_t> graphs;
+    std::map<int, long long> graph_nodes;
+    ~TfCache() override {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    }
 };
+
+namespace {
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DBL_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace
 
 Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nccl_comm)
     : cfg_(cfg), device_(device) {
@@ -201,7 +223,35 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
 }
 
 void Transformer::forward(Lane& lane, int max_tokens, cudaStream_t s) {
-    run_forward(*impl_, lane, max_tokens, nullptr, 0, s);
+    if (!graphs_enabled() || impl_->prof || impl_->world > 1) {
+        run_forward(*impl_, lane, max_tokens, nullptr, 0, s);
+        return;
+    }
+    TfCache& c = *static_cast<TfCache*>(lane.cache.get());
+    const int tp = (std::max(max_tokens, 1) + 15) / 16 * 16;
+    auto it = c.graphs.find(tp);
+    if (it == c.graphs.end()) {
+        gemm_prepare();  // kernel attributes must be set outside capture
+        cudaGraph_t g = nullptr;
+        const long long l0 = launch_counter();
+        CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        try {
+            run_forward(*impl_, lane, tp, nullptr, 0, s);
+        } catch (...) {
+            cudaStreamEndCapture(s, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        CUDA_CHECK(cudaStreamEndCapture(s, &g));
+        c.graph_nodes[tp] = launch_counter() - l0;
+        launch_counter() = l0;  // counted when replayed
+        cudaGraphExec_t exec = nullptr;
+        CUDA_CHECK(cudaGraphInstantiate(&exec, g, 0));
+        CUDA_CHECK(cudaGraphDestroy(g));
+        it = c.graphs.emplace(tp, exec).first;
+    }
+    CUDA_CHECK(cudaGraphLaunch(it->second, s));
+    launch_counter() += c.graph_nodes[tp];
 }
 
 void Transformer::logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) {
@@ -217,38 +267,46 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     TfCache& c = *static_cast<TfCache*>(lane.cache.get());
     const auto& cfg = m.c;
     const int h = m.h;
+    // every GEMM goes through G (optional per-launch event timing for the bench roofline)
+    auto G = [&](Epi e, const CUtensorMap& W, const CUtensorMap& X, int n_out, int K, int n_valid, void* out, int ld,
+                 float* lgp, int ldl, const LaneState* ln) {
+        if (m.prof) m.prof->next(s);
+        gemm_launch(e, W, X, n_out, K, tp, n_valid, out, ld, lgp, ldl, c.ws, s, ln);
+        if (m.prof) {
+            m.prof->next(s);
+            m.prof->bytes.push_back(2.0 * n_out * K + 2.0 * tp * K);
+        }
+    };
     launch_forward_begin(lane.state, s);
     launch_embed(m.embed.p, h, lane.buf.p, lane.state, tp, c.resid.p, s);
     for (int l = 0; l < cfg.n_layers; ++l) {
         LayerW& w = m.layers[l];
         KVView kv{c.kbuf.p + c.layer_stride * l, c.vbuf.p + c.layer_stride * l, c.page_table.p, m.nkv, m.hd};
         launch_rmsnorm(c.resid.p, w.attn_norm.p, h, cfg.rms_eps, tp, c.xn.p, s);
-        gemm_launch(Epi::StoreBF16, w.t_qkv, c.t_xn, m.qkv_rows, h, tp, m.qkv_rows, c.qkv.p, m.qkv_rows, nullptr, 0,
-                    c.ws, s);
+        G(Epi::StoreBF16, w.t_qkv, c.t_xn, m.qkv_rows, h, m.qkv_rows, c.qkv.p, m.qkv_rows, nullptr, 0, nullptr);
         launch_qkv_post(c.qkv.p, m.nh, m.nkv, m.hd, cfg.qk_norm ? w.q_norm.p : nullptr,
                         cfg.qk_norm ? w.k_norm.p : nullptr, cfg.rms_eps, cfg.rope_theta, lane.state, kv, c.qbuf.p, tp, s);
         launch_attention(c.qbuf.p, m.nh, m.nkv, m.hd, kv, lane.state, tp, c.max_chunks, c.part_o.p, c.part_ml.p,
                          c.attn.p, s);
         if (m.world == 1) {
-            gemm_launch(Epi::ResidAdd, w.t_o, c.t_attn, h, m.q_dim, tp, h, c.resid.p, h, nullptr, 0, c.ws, s);
+            G(Epi::ResidAdd, w.t_o, c.t_attn, h, m.q_dim, h, c.resid.p, h, nullptr, 0, nullptr);
         } else {
-            gemm_launch(Epi::StoreF32, w.t_o, c.t_attn, h, m.q_dim, tp, h, c.tp_partial.p, h, nullptr, 0, c.ws, s);
+            G(Epi::StoreF32, w.t_o, c.t_attn, h, m.q_dim, h, c.tp_partial.p, h, nullptr, 0, nullptr);
             m.comm->allreduce_add(c.tp_partial.p, tp, h, c.resid.p, s);
         }
         launch_rmsnorm(c.resid.p, w.mlp_norm.p, h, cfg.rms_eps, tp, c.xn.p, s);
-        gemm_launch(Epi::SiluMul, w.t_gu, c.t_xn, 2 * m.ffn_l, h, tp, 2 * m.ffn_l, c.act.p, m.ffn_l, nullptr, 0, c.ws, s);
+        G(Epi::SiluMul, w.t_gu, c.t_xn, 2 * m.ffn_l, h, 2 * m.ffn_l, c.act.p, m.ffn_l, nullptr, 0, nullptr);
         if (m.world == 1) {
-            gemm_launch(Epi::ResidAdd, w.t_down, c.t_act, h, m.ffn_l, tp, h, c.resid.p, h, nullptr, 0, c.ws, s);
+            G(Epi::ResidAdd, w.t_down, c.t_act, h, m.ffn_l, h, c.resid.p, h, nullptr, 0, nullptr);
         } else {
-            gemm_launch(Epi::StoreF32, w.t_down, c.t_act, h, m.ffn_l, tp, h, c.tp_partial.p, h, nullptr, 0, c.ws, s);
+            G(Epi::StoreF32, w.t_down, c.t_act, h, m.ffn_l, h, c.tp_partial.p, h, nullptr, 0, nullptr);
             m.comm->allreduce_add(c.tp_partial.p, tp, h, c.resid.p, s);
         }
     }
     launch_rmsnorm(c.resid.p, m.final_norm.p, h, cfg.rms_eps, tp, c.xn.p, s);
     const int lm_tiles = (m.vocab_l + 127) / 128;
     float* lg = logits ? logits + static_cast<size_t>(m.rank) * m.vocab_l : nullptr;
-    gemm_launch(Epi::Argmax, m.t_lm, c.t_xn, m.vocab_l, h, tp, m.vocab_l, nullptr, 0, lg, ld_logits, c.ws, s,
-                lane.state);
+    G(Epi::Argmax, m.t_lm, c.t_xn, m.vocab_l, h, m.vocab_l, nullptr, 0, lg, ld_logits, lane.state);
     if (m.world == 1) {
         argmax_finish(c.ws, lm_tiles, tp, lane.state, lane.argmax.p, s);
     } else {

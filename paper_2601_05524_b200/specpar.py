@@ -33,7 +33,7 @@ PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
 __all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "run", "run_vanilla_ar",
-           "run_serial_sd", "build_prior", "DoubleError", "InvalidArgument", "LogicError",
+           "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
            "parse_model_v1", "parse_dstore_v1"]
 
 
@@ -387,6 +387,15 @@ def run(draft: _Model, target: _Model, store: HierarchicalDatastore, prompt, max
                        C.byref(o), _p32(out), cap, C.byref(n), C.byref(m), js,
                        len(js) if js is not None else 0, C.byref(jl))
     return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+def last_run_log() -> np.ndarray:
+    """Decision log of this thread's last run() (include/double_b200.h: dbl_last_run_log)."""
+    n = C.c_int64()
+    check(lib().dbl_last_run_log(None, 0, C.byref(n)))
+    buf = np.zeros(max(n.value, 1), np.int32)
+    check(lib().dbl_last_run_log(_p32(buf), len(buf), C.byref(n)))
+    return buf[:n.value]
 
 
 def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float = 1.0,
