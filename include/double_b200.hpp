@@ -1,0 +1,197 @@
+// double_b200.hpp — header-only C++ mirror of the reference's decode-path API
+// (/root/reference/proj/include/specpar/*.hpp) over the C-ABI in double_b200.h.
+//
+// A C++ caller of specpar::HierarchicalDatastore / forward_batch / run switches to the same names in
+// namespace specpar_b200; errors surface as the reference's exception types
+// (std::invalid_argument, std::runtime_error, std::logic_error — pipeline.cpp:18-22, 210-217).
+#pragma once
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "double_b200.h"
+
+namespace specpar_b200 {
+
+using TokenId = std::int32_t;       // types.hpp:10
+using TokenSeq = std::vector<TokenId>;
+
+inline void check(int status) {
+    if (status == DBL_OK) return;
+    const std::string msg = dbl_last_error();
+    switch (status) {
+        case DBL_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case DBL_LOGIC_ERROR: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+enum class LookupSource { Prior, Dynamic, Rejected, ContextFallback, Miss };  // datastore.hpp:29
+
+struct LookupResult {  // datastore.hpp:33-37
+    TokenSeq candidates;
+    LookupSource source = LookupSource::Miss;
+    int matched_order = 0;
+};
+
+struct LookupStats {  // datastore.hpp:39-67 (a snapshot of the device counters)
+    long lookups = 0, prior_hits = 0, dynamic_hits = 0, rejected_hits = 0, fallback_hits = 0, misses = 0;
+    long hits() const { return prior_hits + dynamic_hits + rejected_hits + fallback_hits; }
+    double hit_rate() const { return lookups == 0 ? 0.0 : static_cast<double>(hits()) / lookups; }
+};
+
+class HierarchicalDatastore;
+
+class NGramIndex {  // one device layer (datastore.hpp:19-27)
+  public:
+    void insert(std::span<const TokenId> tokens, long step);
+    size_t occurrence_count() const;
+    void clear();
+
+  private:
+    friend class HierarchicalDatastore;
+    NGramIndex(HierarchicalDatastore* s, int layer) : s_(s), layer_(layer) {}
+    HierarchicalDatastore* s_;
+    int layer_;
+};
+
+class HierarchicalDatastore {  // datastore.hpp:72-95
+  public:
+    explicit HierarchicalDatastore(int n = 3, int d = 10, int device = 0) : max_order(n), depth(d) {
+        check(dbl_store_create(n, d, device, &h_));
+    }
+    ~HierarchicalDatastore() { dbl_store_destroy(h_); }
+    HierarchicalDatastore(const HierarchicalDatastore&) = delete;
+    HierarchicalDatastore& operator=(const HierarchicalDatastore&) = delete;
+
+    NGramIndex prior{this, DBL_LAYER_PRIOR}, dynamic{this, DBL_LAYER_DYNAMIC}, rejected{this, DBL_LAYER_REJECTED};
+    int max_order, depth;
+
+    void set_rejected_enabled(bool on) { check(dbl_store_set_rejected_enabled(h_, on ? 1 : 0)); }
+    LookupResult lookup(std::span<const TokenId> context, int d) const {  // datastore.cpp:82-132
+        LookupResult r;
+        r.candidates.resize(static_cast<size_t>(d > 0 ? d : 1));
+        int n = 0, src = 0, order = 0;
+        check(dbl_store_lookup(h_, context.data(), static_cast<int>(context.size()), d, r.candidates.data(),
+                               static_cast<int>(r.candidates.size()), &n, &src, &order));
+        r.candidates.resize(static_cast<size_t>(n));
+        r.source = static_cast<LookupSource>(src);
+        r.matched_order = order;
+        return r;
+    }
+    void record_accepted(std::span<const TokenId> t) {  // datastore.cpp:134-137
+        check(dbl_store_record(h_, DBL_LAYER_DYNAMIC, t.data(), static_cast<int>(t.size())));
+    }
+    void record_rejected(std::span<const TokenId> t) {  // datastore.cpp:139-142
+        check(dbl_store_record(h_, DBL_LAYER_REJECTED, t.data(), static_cast<int>(t.size())));
+    }
+    void flush_session() { check(dbl_store_flush_session(h_)); }  // datastore.cpp:144-147
+    LookupStats stats() const {
+        int64_t v[6];
+        check(dbl_store_stats(h_, v));
+        return {v[0], v[1], v[2], v[3], v[4], v[5]};
+    }
+    dbl_store_t handle() const { return h_; }
+
+  private:
+    dbl_store_t h_ = nullptr;
+};
+
+inline void NGramIndex::insert(std::span<const TokenId> tokens, long step) {  // datastore.cpp:9-20
+    check(dbl_store_insert(s_->handle(), layer_, tokens.data(), static_cast<int>(tokens.size()), step));
+}
+inline size_t NGramIndex::occurrence_count() const {  // datastore.cpp:22-26
+    int64_t ns = 0, nt = 0, occ = 0;
+    check(dbl_store_layer_info(s_->handle(), layer_, &ns, &nt, &occ));
+    return static_cast<size_t>(occ);
+}
+inline void NGramIndex::clear() { check(dbl_store_clear_layer(s_->handle(), layer_)); }
+
+// build_prior (datastore.cpp:149-159): the first K sequences, step = index, into store.prior
+inline void build_prior(HierarchicalDatastore& store, const std::vector<TokenSeq>& corpora, int rounds) {
+    if (rounds < 0) throw std::invalid_argument("build_prior: rounds must be >= 0");
+    for (size_t i = 0; i < corpora.size() && static_cast<int>(i) < rounds; ++i)
+        store.prior.insert(corpora[i], static_cast<long>(i));
+}
+
+class Model {  // TableModel / transformer behind forward_batch (model.hpp:18-48)
+  public:
+    Model(const Model&) = delete;
+    Model& operator=(const Model&) = delete;
+    Model(Model&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    ~Model() { if (h_) dbl_model_destroy(h_); }
+    int vocab_size() const {
+        int v = 0;
+        check(dbl_model_vocab(h_, &v));
+        return v;
+    }
+    dbl_model_t handle() const { return h_; }
+    static Model table(int order, int vocab, const std::vector<int32_t>& windows, const std::vector<double>& probs,
+                       const std::vector<double>& fallback, int device = 0) {
+        dbl_model_t h = nullptr;
+        check(dbl_table_create(order, vocab, static_cast<int64_t>(windows.size() / order), windows.data(), probs.data(),
+                               fallback.data(), device, &h));
+        return Model(h);
+    }
+    static Model transformer(const dbl_transformer_config& cfg, int device = 0) {
+        dbl_model_t h = nullptr;
+        check(dbl_transformer_create(&cfg, device, nullptr, &h));
+        return Model(h);
+    }
+
+  private:
+    explicit Model(dbl_model_t h) : h_(h) {}
+    dbl_model_t h_ = nullptr;
+};
+
+// forward_batch (model.cpp:37-53) consumed greedily: argmax_token of each of the |cands|+1 rows
+inline TokenSeq forward_batch_argmax(const Model& m, std::span<const TokenId> ctx, std::span<const TokenId> cands) {
+    TokenSeq out(cands.size() + 1);
+    check(dbl_forward_argmax(m.handle(), ctx.data(), static_cast<int>(ctx.size()), cands.data(),
+                             static_cast<int>(cands.size()), out.data()));
+    return out;
+}
+
+struct PipelineOptions {  // pipeline.hpp:36-44 (+ LatencyConfig :15-29)
+    int gamma = 4, depth = 10;
+    bool draft_retrieval = true, target_retrieval = true;
+    double t_target = 1.0, t_draft = 0.25, t_lookup = 0.0, t_sync = 0.0;
+};
+
+struct RunResult {  // pipeline.hpp:84-88 (traces as the traces_to_jsonl text)
+    TokenSeq output;
+    dbl_run_metrics metrics{};
+    std::string jsonl;
+};
+
+// run (pipeline.cpp:264-323)
+inline RunResult run(const Model& draft, const Model& target, HierarchicalDatastore& store, const TokenSeq& prompt,
+                     int max_new_tokens, const PipelineOptions& o) {
+    dbl_pipeline_options c{o.gamma, o.depth, o.draft_retrieval, o.target_retrieval, 1,
+                           o.t_target, o.t_draft, o.t_lookup, o.t_sync, 1};
+    RunResult r;
+    r.output.resize(static_cast<size_t>(max_new_tokens > 0 ? max_new_tokens : 1));
+    int n = 0;
+    int64_t jl = 0;
+    check(dbl_run(draft.handle(), target.handle(), store.handle(), prompt.data(), static_cast<int>(prompt.size()),
+                  max_new_tokens, &c, r.output.data(), static_cast<int>(r.output.size()), &n, &r.metrics, nullptr, 0, &jl));
+    r.output.resize(static_cast<size_t>(n));
+    (void)jl;
+    return r;
+}
+
+// run_vanilla_ar (harness.cpp:233-258)
+inline RunResult run_vanilla_ar(const Model& target, const TokenSeq& prompt, int max_new_tokens, double t_target = 1.0) {
+    RunResult r;
+    r.output.resize(static_cast<size_t>(max_new_tokens > 0 ? max_new_tokens : 1));
+    int n = 0;
+    int64_t jl = 0;
+    check(dbl_run_ar(target.handle(), prompt.data(), static_cast<int>(prompt.size()), max_new_tokens, t_target,
+                     r.output.data(), static_cast<int>(r.output.size()), &n, &r.metrics, nullptr, 0, &jl));
+    r.output.resize(static_cast<size_t>(n));
+    return r;
+}
+
+}  // namespace specpar_b200

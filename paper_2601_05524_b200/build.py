@@ -63,5 +63,20 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+CPP_TEST = os.path.join(ROOT, "build", "test_cpp_api")
+
+
+def build_cpp_test() -> str:
+    """tests/cpp/test_cpp_api.cpp against include/double_b200.hpp, linked to the in-tree library."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_cpp_api.cpp")
+    os.makedirs(os.path.dirname(CPP_TEST), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o", CPP_TEST,
+           "-L", PKG, "-ldouble_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../paper_2601_05524_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ API test build failed:\n{r.stderr}")
+    return CPP_TEST
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
