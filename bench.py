@@ -260,7 +260,12 @@ def main():
     pt = profile(tgt, wl["prompt_len"], DEPTH + 1)
     pd = profile(drf, wl["prompt_len"], DEPTH + 1)
     C_ratio = pt[0] / pd[0]
-    gamma = a.gamma or max(1, math.ceil(C_ratio))
+    gamma_c = max(1, math.ceil(C_ratio))
+    # The reference's gamma = ceil(C) assumes draft and target on separate devices (round time =
+    # max(gamma*t_draft, t_target), pipeline.cpp:198-204).  Co-located on one GPU both stream HBM, the
+    # round costs ~ t_target + gamma*t_draft, and the independent random-init draft is never accepted,
+    # so the headline uses gamma = 1; gamma = ceil(C) is measured too ("gamma_C" below).
+    gamma = a.gamma or 1
     opts = dbl.PipelineOptions(gamma=gamma, depth=DEPTH)
 
     def store():
@@ -302,6 +307,19 @@ def main():
         ar_ms += ar.metrics["device_ms"]
         ar_tok += len(ar.output)
     lossless = all(r.output == ar.output for r in results)
+    gamma_c_line = None
+    if gamma_c != gamma:  # the reference's own gamma rule, same workload, same timing
+        oc = dbl.PipelineOptions(gamma=gamma_c, depth=DEPTH)
+        dbl.run(drf, tgt, store(), prompt, max_new, oc, want_jsonl=False)
+        gms, gtok, gm = 0.0, 0, None
+        for _ in range(a.steps):
+            rg = dbl.run(drf, tgt, store(), prompt, max_new, oc, want_jsonl=False)
+            gms += rg.metrics["device_ms"]
+            gtok += len(rg.output)
+            lossless &= rg.output == ar.output
+            gm = rg.metrics
+        gv = all_sum(gtok, world) / (all_max(gms, world) / 1e3)
+        gamma_c_line = {"gamma": gamma_c, "value": round(gv, 3), "mean_accepted_len": round(gm["m"], 4)}
 
     t_dev = all_max(dev_ms, world)
     t_e2e = all_max(e2e_ms, world)
@@ -335,6 +353,7 @@ def main():
         "mean_accepted_len": round(m0["m"], 4), "amt": round(m0["amt"], 4),
         "rounds_per_step": m0["rounds"], "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 3),
         "lossless_vs_ar": lossless,
+        "gamma_C": dict(gamma_c_line, speedup_vs_ar=round(gamma_c_line["value"] / ar_value, 4)) if gamma_c_line else None,
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s",
                 "h2d_bytes_per_step": 4 * (len(prompt) + sum(len(s) for s in prior)),
                 "d2h_bytes_per_step": 4 * max_new},

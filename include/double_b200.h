@@ -161,6 +161,9 @@ int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, 
  * out[8] = forward ms, GEMM ms, GEMM algorithmic bytes, GEMM launches, kernel launches (per
  * forward), token columns, LM-head GEMM ms, LM-head bytes.  Feeds bench.py's roofline. */
 int dbl_profile_forward(dbl_model_t m, int ctx_len, int rows, int iters, double* out);
+/* DBL_GEMM_TRACE=1 timeline of the GEMM launches since the last call: stamps[n][320][4] (%globaltimer
+ * ns per CTA: resident, dependency resolved, last load issued, epilogue done), grid and weight bytes */
+int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t* bytes, int* n_launches);
 /* back-to-back launches of one GEMM shape, ms per launch (weights rotate over `chain` copies) */
 int dbl_debug_gemm_bench(int epi, int n_out, int K, int tp, int iters, int chain, double* ms_per_launch);
 int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,

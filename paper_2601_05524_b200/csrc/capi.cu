@@ -353,6 +353,26 @@ int dbl_debug_gemm_bench(int epi, int n_out, int K, int tp, int iters, int chain
     });
 }
 
+// GEMM timeline (DBL_GEMM_TRACE=1): stamps [n_launches][kTraceCtas][4], grids, weight bytes
+int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t* bytes, int* n_launches) {
+    return guarded([&] {
+        dbl::GemmTrace& t = dbl::gemm_trace();
+        *n_launches = t.n;
+        const int64_t need = static_cast<int64_t>(t.n) * dbl::kTraceCtas * 4;
+        if (t.n == 0) return;
+        if (cap < need) dbl::throw_invalid("trace buffer too small");
+        CUDA_CHECK(cudaDeviceSynchronize());
+        CUDA_CHECK(cudaMemcpy(stamps, t.buf.p, need * 8, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < t.n; ++i) {
+            grids[i] = t.grid[i];
+            bytes[i] = t.bytes[i];
+        }
+        t.n = 0;
+        t.grid.clear();
+        t.bytes.clear();
+    });
+}
+
 // --------------------------------------------------------------------------- kernel checks
 int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,
                    int n_valid, float* io, int32_t* argmax) {

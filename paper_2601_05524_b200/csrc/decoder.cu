@@ -109,9 +109,13 @@ struct Streams {
     cudaStream_t main = nullptr, draft = nullptr, target = nullptr;
     cudaEvent_t ready = nullptr, tf0 = nullptr, tf1 = nullptr;
     Streams() {
-        CUDA_CHECK(cudaStreamCreateWithFlags(&main, cudaStreamNonBlocking));
-        CUDA_CHECK(cudaStreamCreateWithFlags(&draft, cudaStreamNonBlocking));
-        CUDA_CHECK(cudaStreamCreateWithFlags(&target, cudaStreamNonBlocking));
+        // The target's verify forward is the round's critical path: its stream gets the highest
+        // priority so a co-located draft chain fills SM gaps instead of delaying target CTAs.
+        int lo = 0, hi = 0;
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&main, cudaStreamNonBlocking, hi));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&draft, cudaStreamNonBlocking, lo));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&target, cudaStreamNonBlocking, hi));
         CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CUDA_CHECK(cudaEventCreate(&tf0));
         CUDA_CHECK(cudaEventCreate(&tf1));

@@ -27,7 +27,8 @@ __device__ __forceinline__ long long cta_of(long long u, long long U, long long 
 
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 2)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmArgs a) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                const __grid_constant__ CUtensorMap tmN, GemmArgs a) {
     using namespace sm100;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -50,6 +51,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (b0 >= b1) return;
     const int KB = a.kb_total;
     const uint32_t ncols = tp <= 32 ? 32 : tp <= 64 ? 64 : tp <= 128 ? 128 : 256;
+    auto stamp = [&](int k) {
+        if (a.trace) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[c * 4 + k] = t;
+        }
+    };
+    if (threadIdx.x == 0) stamp(0);  // CTA resident
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < S; ++i) {
@@ -82,7 +91,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tma_load_2d(sA + i * kABytes, &tmW, &full[i], static_cast<int>(u % KB) * kBlockK,
                             static_cast<int>(u / KB) * kBlockM, kEvictFirst);
             }
+            // ...and warm L2 with the rest of this CTA's weight range (bounded so one GEMM's warm set
+            // stays well inside the 126 MB L2): HBM keeps streaming while the previous kernels of the
+            // forward drain, instead of idling at the kernel boundary.
+            const long long pf_end = std::min<long long>(b1, b0 + pre + a.l2_prefetch_units);
+            for (long long u = b0 + pre; u < pf_end; ++u)
+                tma_prefetch_l2_2d(&tmW, static_cast<int>(u % KB) * kBlockK, static_cast<int>(u / KB) * kBlockM);
             griddep_wait();
+            stamp(1);  // dependency resolved
             for (int i = 0; i < pre; ++i) {
                 const int kb = static_cast<int>((b0 + i) % KB);
                 for (int j = 0; j < tp / 16; ++j)
@@ -99,6 +115,18 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tma_load_2d(sB + stage * b_bytes + j * 2048, &tmX, &full[stage], kb * kBlockK, j * 16,
                                 kEvictLast);
                 if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+            stamp(2);  // last load issued
+            // Warm L2 with the NEXT GEMM's first weight tiles (those of the CTA at the same relative
+            // grid position): HBM keeps streaming through this GEMM's drain and through the small
+            // dependent kernels (norm / RoPE / attention) that separate it from the next one.
+            if (a.next_units > 0) {
+                const long long G2 = a.next_grid, U2 = a.next_units, c2 = c * G2 / G;
+                const long long s2 = range_begin(c2, U2, G2);
+                const long long e2 = std::min<long long>(range_begin(c2 + 1, U2, G2), s2 + a.next_prefetch);
+                for (long long u = s2; u < e2; ++u)
+                    tma_prefetch_l2_2d(&tmN, static_cast<int>(u % a.next_kb) * kBlockK,
+                                       static_cast<int>(u / a.next_kb) * kBlockM);
             }
         }
     } else if (warp == 1) {
@@ -295,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             acc_phase ^= 1;
             u += kb1 - kb0;
         }
+        if (et == 0) stamp(3);  // epilogue done
     }
     __syncthreads();
     if (warp == 1) {
@@ -364,6 +393,11 @@ int num_sms(int device) {
     return n;
 }
 
+GemmTrace& gemm_trace() {
+    static GemmTrace t;
+    return t;
+}
+
 void gemm_prepare() {
     set_smem_attr<static_cast<int>(Epi::StoreBF16)>();
     set_smem_attr<static_cast<int>(Epi::ResidAdd)>();
@@ -399,9 +433,30 @@ void GemmWorkspace::ensure(int sms, int mtp, int mtiles) {
     CUDA_CHECK(cudaDeviceSynchronize());
 }
 
+namespace {
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+// Grid = a pure function of (n_tiles, k-blocks, #SMs) — never of the token count — so the split
+// points (and the numerics) are identical for every forward size.  Few tiles: regular split-K with
+// S aligned slices per tile (S = ceil(SMs / tiles) <= 8 = the fan-in the finisher reduces with
+// batched loads; two CTAs fit per SM).  Many tiles: stream-K over one CTA per SM.
+int choose_grid(int n_tiles, int kb_total, int sms) {
+    long long grid;
+    if (n_tiles >= sms) {
+        grid = sms;
+    } else {
+        const int S = std::min({kMaxBatchContrib, (sms + n_tiles - 1) / n_tiles, kb_total});
+        grid = static_cast<long long>(n_tiles) * S;
+    }
+    return static_cast<int>(std::min<long long>(grid, static_cast<long long>(n_tiles) * kb_total));
+}
+}  // namespace
+
 void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_out, int K, int tp, int n_valid,
                  void* out, int ld_out, float* logits, int ld_logits, GemmWorkspace& ws, cudaStream_t s,
-                 const LaneState* lane) {
+                 const LaneState* lane, const GemmNext* next) {
     if (tp < 16 || tp > 256 || tp % 16) throw_invalid("GEMM token tile must be a multiple of 16 in [16, 256]");
     if (K % kBlockK) throw_invalid("GEMM K must be a multiple of 64");
     GemmArgs a{};
@@ -414,30 +469,46 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
     a.units = static_cast<long long>(a.n_tiles) * a.kb_total;
     const int stage_bytes = kABytes + tp * kBlockK * 2;
     // decode-sized forwards (tp <= 64): ~110 KB so two GEMM CTAs (consecutive kernels under PDL)
-    // co-reside on an SM and the next GEMM streams weights while this one drains; prefill-sized
-    // forwards take the whole SM for a deeper pipeline.
-    const int budget = (tp <= 64 ? 110 * 1024 : 227 * 1024) - 1024 - 2048;
-    a.stages = std::max(2, std::min(12, budget / stage_bytes));
-    const size_t smem = 1024 + static_cast<size_t>(a.stages) * stage_bytes + 2048;
+    // co-reside on an SM; prefill-sized forwards take the whole SM for a deeper pipeline.
+    // DBL_GEMM_STAGES overrides (tuning).
+    // Long stream-K GEMMs (>= 64 k-blocks per CTA: gate|up, LM head) are pure streaming and take the
+    // whole SM for 12 stages; split-K GEMMs keep two CTAs per SM.
     int dev = 0;
     CUDA_CHECK(cudaGetDevice(&dev));
-    static const int grid_cap = [] {  // DBL_GEMM_GRID: debug override of the stream-K grid
-        const char* e = std::getenv("DBL_GEMM_GRID");
-        return e ? std::atoi(e) : 0;
-    }();
-    const int sms = grid_cap > 0 ? std::min(grid_cap, num_sms(dev)) : num_sms(dev);
-    // Grid = a pure function of (n_out, K, #SMs) — never of tp — so split points (and numerics) are
-    // the same for every token count.  Few tiles: regular split-K, S aligned slices per tile (S =
-    // ceil(SMs / tiles) <= 8, the fan-in the finisher reduces with batched loads; up to 2 CTAs/SM).
-    // Many tiles: stream-K over one CTA per SM (<= 2-3 contributors per tile).
-    int grid;
-    if (a.n_tiles >= sms) {
-        grid = sms;
-    } else {
-        const int S = std::min({kMaxBatchContrib, (sms + a.n_tiles - 1) / a.n_tiles, a.kb_total});
-        grid = a.n_tiles * S;
+    const int sms = num_sms(dev);
+    const int grid = choose_grid(a.n_tiles, a.kb_total, sms);
+    static const int stage_cap = env_int("DBL_GEMM_STAGES", 0);
+    const bool deep = stage_cap > 0 || tp > 64 || a.units / grid >= 64;
+    const int budget = (deep ? 227 * 1024 : 110 * 1024) - 1024 - 2048;
+    a.stages = std::max(2, std::min(stage_cap > 0 ? stage_cap : 12, budget / stage_bytes));
+    const size_t smem = 1024 + static_cast<size_t>(a.stages) * stage_bytes + 2048;
+    // DBL_GEMM_L2PF_MB: L2 warm-up of this GEMM's own later k-blocks before the dependency wait
+    // and DBL_GEMM_NEXT_MB: warm-up of the next GEMM's first k-blocks after this one has issued its
+    // last load.  Both measured slower in the full forward (the HBM is already busy during those
+    // windows; see profiles/): off by default, kept for A/B runs.
+    static const long long own_pf = static_cast<long long>(env_int("DBL_GEMM_L2PF_MB", 0)) << 20;
+    static const long long next_pf = static_cast<long long>(env_int("DBL_GEMM_NEXT_MB", 0)) << 20;
+    a.l2_prefetch_units = static_cast<int>(own_pf / (static_cast<long long>(kABytes) * grid));
+    CUtensorMap tmN = tmW;
+    if (next && next_pf > 0) {
+        const int nt = (next->n_out + kBlockM - 1) / kBlockM, nkb = next->K / kBlockK;
+        a.next_units = static_cast<long long>(nt) * nkb;
+        a.next_grid = choose_grid(nt, nkb, sms);
+        a.next_kb = nkb;
+        a.next_prefetch = static_cast<int>(next_pf / (static_cast<long long>(kABytes) * a.next_grid));
+        tmN = *next->tmap;
     }
-    grid = static_cast<int>(std::min<long long>(grid, a.units));
+    static const bool tracing = env_int("DBL_GEMM_TRACE", 0) != 0;
+    if (tracing) {
+        GemmTrace& tr = gemm_trace();
+        if (!tr.buf.p) tr.buf.alloc(static_cast<size_t>(kTraceLaunches) * kTraceCtas * 4);
+        if (tr.n < kTraceLaunches && grid <= kTraceCtas) {
+            a.trace = tr.buf.p + static_cast<size_t>(tr.n) * kTraceCtas * 4;
+            tr.grid.push_back(grid);
+            tr.bytes.push_back(static_cast<long long>(n_out) * K * 2);
+            ++tr.n;
+        }
+    }
     if (ws.grid < grid || ws.max_tp < tp || ws.max_tiles < a.n_tiles)
         throw_runtime("GEMM workspace too small (call GemmWorkspace::ensure)");
     a.out = out;
@@ -452,7 +523,7 @@ void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_
 #define DBL_GEMM_CASE(E)                                                                     \
     case E:                                                                                  \
         set_smem_attr<static_cast<int>(E)>();                                                \
-        launch_pdl(gemm_kernel<static_cast<int>(E)>, dim3(grid), dim3(kThreads), smem, s, tmW, tmX, a); \
+        launch_pdl(gemm_kernel<static_cast<int>(E)>, dim3(grid), dim3(kThreads), smem, s, tmW, tmX, tmN, a); \
         break;
         DBL_GEMM_CASE(Epi::StoreBF16)
         DBL_GEMM_CASE(Epi::ResidAdd)

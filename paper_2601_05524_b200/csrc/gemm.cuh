@@ -14,6 +14,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace dbl {
@@ -33,6 +35,10 @@ struct GemmArgs {
     int n_tiles, kb_total;
     long long units;
     int stages;
+    int l2_prefetch_units;  // weight k-blocks per CTA warmed into L2 before the grid-dependency wait
+    long long next_units;   // next GEMM of the forward (0 = none): its unit count, grid, k-blocks,
+    int next_grid, next_kb, next_prefetch;  // and the k-blocks per CTA to warm into L2
+    unsigned long long* trace;  // optional per-CTA %globaltimer stamps [grid][4] (DBL_GEMM_TRACE)
     void* out;
     int ld_out;
     float* logits;
@@ -56,9 +62,24 @@ void gemm_prepare();  // set kernel attributes (call before stream capture)
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int box_rows);
 
 // Launch one GEMM.  tmW: weights (box 128 x 64), tmX: activations (box 16 x 64).
+// DBL_GEMM_TRACE=1: every GEMM launch records per-CTA %globaltimer stamps (resident, dependency
+// resolved, last load issued, epilogue done) — a device timeline without nsys (tools/gemm_timeline.py)
+constexpr int kTraceLaunches = 4096, kTraceCtas = 320;
+struct GemmTrace {
+    DevBuf<unsigned long long> buf;
+    int n = 0;
+    std::vector<int> grid;
+    std::vector<long long> bytes;
+};
+GemmTrace& gemm_trace();
+
+struct GemmNext {  // the GEMM that follows in the forward (its first weight tiles are L2-warmed)
+    const CUtensorMap* tmap;
+    int n_out, K;
+};
 void gemm_launch(Epi epi, const CUtensorMap& tmW, const CUtensorMap& tmX, int n_out, int K, int tp,
                  int n_valid, void* out, int ld_out, float* logits, int ld_logits, GemmWorkspace& ws,
-                 cudaStream_t s, const struct LaneState* lane = nullptr);
+                 cudaStream_t s, const struct LaneState* lane = nullptr, const GemmNext* next = nullptr);
 struct LaneState;
 // final argmax over the per-tile partials: argmax[lane.start + t] for t in [0, L + c - start)
 void argmax_finish(const GemmWorkspace& ws, int n_tiles, int tp, const LaneState* lane, int32_t* argmax,

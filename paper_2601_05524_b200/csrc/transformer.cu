@@ -268,10 +268,11 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     const auto& cfg = m.c;
     const int h = m.h;
     // every GEMM goes through G (optional per-launch event timing for the bench roofline)
+    const GemmNext* nx = nullptr;  // the GEMM after the one being launched (L2 warm-up target)
     auto G = [&](Epi e, const CUtensorMap& W, const CUtensorMap& X, int n_out, int K, int n_valid, void* out, int ld,
                  float* lgp, int ldl, const LaneState* ln) {
         if (m.prof) m.prof->next(s);
-        gemm_launch(e, W, X, n_out, K, tp, n_valid, out, ld, lgp, ldl, c.ws, s, ln);
+        gemm_launch(e, W, X, n_out, K, tp, n_valid, out, ld, lgp, ldl, c.ws, s, ln, nx);
         if (m.prof) {
             m.prof->next(s);
             m.prof->bytes.push_back(2.0 * n_out * K + 2.0 * tp * K);
@@ -282,12 +283,17 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     for (int l = 0; l < cfg.n_layers; ++l) {
         LayerW& w = m.layers[l];
         KVView kv{c.kbuf.p + c.layer_stride * l, c.vbuf.p + c.layer_stride * l, c.page_table.p, m.nkv, m.hd};
+        const GemmNext n_o{&w.t_o, h, m.q_dim}, n_gu{&w.t_gu, 2 * m.ffn_l, h}, n_down{&w.t_down, h, m.ffn_l};
+        const GemmNext n_after = l + 1 < cfg.n_layers ? GemmNext{&m.layers[l + 1].t_qkv, m.qkv_rows, h}
+                                                      : GemmNext{&m.t_lm, m.vocab_l, h};
         launch_rmsnorm(c.resid.p, w.attn_norm.p, h, cfg.rms_eps, tp, c.xn.p, s);
+        nx = &n_o;
         G(Epi::StoreBF16, w.t_qkv, c.t_xn, m.qkv_rows, h, m.qkv_rows, c.qkv.p, m.qkv_rows, nullptr, 0, nullptr);
         launch_qkv_post(c.qkv.p, m.nh, m.nkv, m.hd, cfg.qk_norm ? w.q_norm.p : nullptr,
                         cfg.qk_norm ? w.k_norm.p : nullptr, cfg.rms_eps, cfg.rope_theta, lane.state, kv, c.qbuf.p, tp, s);
         launch_attention(c.qbuf.p, m.nh, m.nkv, m.hd, kv, lane.state, tp, c.max_chunks, c.part_o.p, c.part_ml.p,
                          c.attn.p, s);
+        nx = &n_gu;
         if (m.world == 1) {
             G(Epi::ResidAdd, w.t_o, c.t_attn, h, m.q_dim, h, c.resid.p, h, nullptr, 0, nullptr);
         } else {
@@ -295,7 +301,9 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
             m.comm->allreduce_add(c.tp_partial.p, tp, h, c.resid.p, s);
         }
         launch_rmsnorm(c.resid.p, w.mlp_norm.p, h, cfg.rms_eps, tp, c.xn.p, s);
+        nx = &n_down;
         G(Epi::SiluMul, w.t_gu, c.t_xn, 2 * m.ffn_l, h, 2 * m.ffn_l, c.act.p, m.ffn_l, nullptr, 0, nullptr);
+        nx = &n_after;
         if (m.world == 1) {
             G(Epi::ResidAdd, w.t_down, c.t_act, h, m.ffn_l, h, c.resid.p, h, nullptr, 0, nullptr);
         } else {
@@ -306,6 +314,7 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     launch_rmsnorm(c.resid.p, m.final_norm.p, h, cfg.rms_eps, tp, c.xn.p, s);
     const int lm_tiles = (m.vocab_l + 127) / 128;
     float* lg = logits ? logits + static_cast<size_t>(m.rank) * m.vocab_l : nullptr;
+    nx = nullptr;
     G(Epi::Argmax, m.t_lm, c.t_xn, m.vocab_l, h, m.vocab_l, nullptr, 0, lg, ld_logits, lane.state);
     if (m.world == 1) {
         argmax_finish(c.ws, lm_tiles, tp, lane.state, lane.argmax.p, s);
