@@ -164,6 +164,8 @@ int dbl_profile_forward(dbl_model_t m, int ctx_len, int rows, int iters, double*
 /* DBL_GEMM_TRACE=1 timeline of the GEMM launches since the last call: stamps[n][320][4] (%globaltimer
  * ns per CTA: resident, dependency resolved, last load issued, epilogue done), grid and weight bytes */
 int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t* bytes, int* n_launches);
+/* DBL_FWD_TRACE=1: per-(phase, CTA) stamps of the most recent stream forward, [n_ph][grid][4] */
+int dbl_debug_fwd_trace(uint64_t* stamps, int64_t cap, int* n_ph, int* grid);
 /* back-to-back launches of one GEMM shape, ms per launch (weights rotate over `chain` copies) */
 int dbl_debug_gemm_bench(int epi, int n_out, int K, int tp, int iters, int chain, double* ms_per_launch);
 int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,

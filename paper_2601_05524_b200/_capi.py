@@ -87,6 +87,7 @@ PROTOTYPES = {
     "dbl_last_run_log": [I32P, C.c_int64, I64P],
     "dbl_profile_forward": [VP, C.c_int, C.c_int, C.c_int, F64P],
     "dbl_debug_gemm_trace": [C.POINTER(C.c_uint64), C.c_int64, I32P, I64P, C.POINTER(C.c_int)],
+    "dbl_debug_fwd_trace": [C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "dbl_debug_gemm_bench": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, F64P],
     "dbl_debug_gemm": [C.c_int, U16P, C.c_int, C.c_int, U16P, C.c_int, C.c_int, C.c_int, F32P,
                        I32P],

@@ -8,6 +8,7 @@
 #include "store.cuh"
 #include "table_model.cuh"
 #include "transformer.cuh"
+#include "fwd.cuh"
 #include "gemm.cuh"
 #include "lane.cuh"
 #include "tf_kernels.cuh"
@@ -374,6 +375,14 @@ int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t*
 }
 
 // --------------------------------------------------------------------------- kernel checks
+int dbl_debug_fwd_trace(uint64_t* stamps, int64_t cap, int* n_ph, int* grid) {
+    return guarded([&] {
+        need(n_ph, "n_ph");
+        need(grid, "grid");
+        dbl::fwd_trace_read(reinterpret_cast<unsigned long long*>(stamps), cap, n_ph, grid);
+    });
+}
+
 int dbl_debug_gemm(int epi, const uint16_t* W, int n_out, int K, const uint16_t* X, int T, int tp,
                    int n_valid, float* io, int32_t* argmax) {
     return guarded([&] {

@@ -53,6 +53,26 @@ __global__ void init_gateup_kernel(__nv_bfloat16* dst, int ffn_local, int hidden
     }
 }
 
+// fused [q; k; v] projection with the rows of every head permuted so that RoPE partners share a warp:
+// physical head row 32*w + l holds logical dim 16*w + l (l < 16) or hd/2 + 16*w + (l - 16) (l >= 16)
+__global__ void init_qkv_kernel(__nv_bfloat16* dst, int q_dim, int kv_dim, int hd, int hidden,
+                                unsigned long long qb, unsigned long long kb, unsigned long long vb, long long rq0,
+                                long long rkv0, float std) {
+    const long long rows = q_dim + 2LL * kv_dim;
+    const long long n = rows * hidden;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long p = i / hidden, col = i % hidden;
+        const int region = p < q_dim ? 0 : p < q_dim + kv_dim ? 1 : 2;
+        const long long pl = p - (region == 0 ? 0 : region == 1 ? q_dim : q_dim + kv_dim);
+        const long long head = pl / hd, pr = pl % hd, w = pr / 32, l = pr % 32;
+        const long long dd = l < 16 ? 16 * w + l : hd / 2 + 16 * w + l - 16;
+        const long long logical_row = (region == 0 ? rq0 : rkv0) + head * hd + dd;
+        const unsigned long long base = region == 0 ? qb : region == 1 ? kb : vb;
+        dst[i] = __float2bfloat16_rn(std * normal_of(base ^ static_cast<unsigned long long>(logical_row * hidden + col)));
+    }
+}
+
 __global__ void fill_kernel(__nv_bfloat16* dst, long long n, float v) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -394,6 +414,15 @@ void launch_init_gateup(__nv_bfloat16* dst, int ffn_local, int hidden, uint64_t 
     const unsigned long long ub = mix(seed ^ mix(up_id * 0x9E3779B97F4A7C15ull + 17));
     init_gateup_kernel<<<blocks_for(2LL * ffn_local * hidden, 256), 256, 0, s>>>(dst, ffn_local, hidden, gb, ub, f0,
                                                                                  std);
+    CUDA_LAUNCH_CHECK();
+}
+
+void launch_init_qkv(__nv_bfloat16* dst, int q_dim, int kv_dim, int hd, int hidden, uint64_t seed, uint64_t q_id,
+                     uint64_t k_id, uint64_t v_id, int64_t rq0, int64_t rkv0, float std, cudaStream_t s) {
+    auto base = [&](uint64_t id) { return mix(seed ^ mix(id * 0x9E3779B97F4A7C15ull + 17)); };
+    const long long n = (q_dim + 2LL * kv_dim) * hidden;
+    init_qkv_kernel<<<blocks_for(n, 256), 256, 0, s>>>(dst, q_dim, kv_dim, hd, hidden, base(q_id), base(k_id),
+                                                       base(v_id), rq0, rkv0, std);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -39,6 +39,15 @@ void launch_init_normal(__nv_bfloat16* dst, int rows, int cols, int ld, uint64_t
 // gate/up fused layout: physical row p of the [2*ffn_local, h] block, interleaved 16 gate | 16 up per 32
 void launch_init_gateup(__nv_bfloat16* dst, int ffn_local, int hidden, uint64_t seed, uint64_t gate_id,
                         uint64_t up_id, int64_t f0, float std, cudaStream_t s);
+// fused [q; k; v] rows (q rows from rq0, k/v rows from rkv0 of the logical tensors), head rows permuted
+// so that RoPE partners d, d + hd/2 sit in lanes l, l ^ 16 of one warp (fwd.cuh)
+void launch_init_qkv(__nv_bfloat16* dst, int q_dim, int kv_dim, int hd, int hidden, uint64_t seed, uint64_t q_id,
+                     uint64_t k_id, uint64_t v_id, int64_t rq0, int64_t rkv0, float std, cudaStream_t s);
+// logical dim held by physical row pr of a head (the permutation above)
+inline int qkv_perm_dim(int pr, int hd) {
+    const int w = pr / 32, l = pr % 32;
+    return l < 16 ? 16 * w + l : hd / 2 + 16 * w + l - 16;
+}
 void launch_fill(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t s);
 void launch_forward_begin(LaneState* lane, cudaStream_t s);  // lane.start = min(kv_len, row0)
 void launch_forward_end(LaneState* lane, cudaStream_t s);    // lane.kv_len = L + c
