@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "fwd.cuh"
 #include "sm100.cuh"
@@ -19,7 +20,8 @@ using namespace sm100;
 constexpr int kBM = 128, kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // one 128 x 64 bf16 weight tile
 constexpr unsigned long long kWatchdogNs = 4000000000ull;
-constexpr int kBatch = 4;               // split-K partials: 4 contributors x 16 columns of loads in flight
+constexpr int kVRows = 8;              // attention: V rows loaded per round trip
+constexpr int kBatch = 2;               // split-K partials: 2 contributors x 16 columns of loads in flight
 
 // ------------------------------------------------------------------ small helpers
 __device__ __noinline__ void watchdog_fire(int* err, int code, int phase) {
@@ -50,9 +52,7 @@ struct Range {
     int b0, b1;
     int ci;  // phase-local CTA index
 };
-__device__ __forceinline__ int range_begin(int ci, int U, int A) {
-    return static_cast<int>(static_cast<long long>(ci) * U / A);
-}
+__device__ __forceinline__ int range_begin(int ci, int U, int A) { return ci * U / A; }  // ci*U < 2^31
 __device__ __forceinline__ Range cta_range(const FwdPhase& P, int c, int G) {
     int ci = c - P.offset;
     if (ci < 0) ci += G;
@@ -64,9 +64,7 @@ __device__ __forceinline__ Range cta_range(const FwdPhase& P, int c, int G) {
     return r;
 }
 // phase-local CTA whose range contains unit u: largest ci with floor(ci U / A) <= u
-__device__ __forceinline__ int owner_of(int u, int U, int A) {
-    return static_cast<int>(((static_cast<long long>(u) + 1) * A - 1) / U);
-}
+__device__ __forceinline__ int owner_of(int u, int U, int A) { return ((u + 1) * A - 1) / U; }
 
 __device__ __forceinline__ bool dep_ok(const FwdArgs& a, int p, unsigned long long ep) {
     if (p < 0) return true;
@@ -185,24 +183,27 @@ __device__ __forceinline__ void attn_item(const FwdArgs& a, const FwdPhase& P, i
     __syncwarp();
     const float scale = rsqrtf(static_cast<float>(HD));
     float sc[2];
-#pragma unroll
+#pragma unroll 1
     for (int h2 = 0; h2 < 2; ++h2) {
         const int kk = lane + 32 * h2;
         sc[h2] = -INFINITY;
         if (kk < nk) {
             const uint4* kr = reinterpret_cast<const uint4*>(kp + static_cast<long long>(kk) * HD);
-            uint4 w[HD / 8];
-#pragma unroll
-            for (int d8 = 0; d8 < HD / 8; ++d8) w[d8] = kr[d8];
             float acc = 0.f;
 #pragma unroll
-            for (int d8 = 0; d8 < HD / 8; ++d8) {
-                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w[d8]);
+            for (int hh = 0; hh < HD / 64; ++hh) {  // 128-byte halves of the row: 8 loads in flight
+                uint4 w[8];
 #pragma unroll
-                for (int e2 = 0; e2 < 4; ++e2) {
-                    const float2 kf = __bfloat1622float2(b2[e2]);
-                    acc = fmaf(q_s[d8 * 8 + 2 * e2], kf.x, acc);
-                    acc = fmaf(q_s[d8 * 8 + 2 * e2 + 1], kf.y, acc);
+                for (int d8 = 0; d8 < 8; ++d8) w[d8] = kr[hh * 8 + d8];
+#pragma unroll
+                for (int d8 = 0; d8 < 8; ++d8) {
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w[d8]);
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const float2 kf = __bfloat1622float2(b2[e2]);
+                        acc = fmaf(q_s[(hh * 8 + d8) * 8 + 2 * e2], kf.x, acc);
+                        acc = fmaf(q_s[(hh * 8 + d8) * 8 + 2 * e2 + 1], kf.y, acc);
+                    }
                 }
             }
             sc[h2] = acc * scale;
@@ -222,21 +223,24 @@ __device__ __forceinline__ void attn_item(const FwdArgs& a, const FwdPhase& P, i
 #pragma unroll
     for (int e = 0; e < DPL; ++e) o[e] = 0.f;
     const __nv_bfloat16* vl = vp + lane * DPL;
-#pragma unroll 8
-    for (int i = 0; i < nk; ++i) {
-        const float pi = p_s[i];
-        if constexpr (DPL == 4) {
-            const uint2 raw = *reinterpret_cast<const uint2*>(vl + static_cast<long long>(i) * HD);
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-            const float2 v0 = __bfloat1622float2(b2[0]), v1 = __bfloat1622float2(b2[1]);
-            o[0] = fmaf(pi, v0.x, o[0]);
-            o[1] = fmaf(pi, v0.y, o[1]);
-            o[2] = fmaf(pi, v1.x, o[2]);
-            o[3] = fmaf(pi, v1.y, o[3]);
-        } else {
-            const float2 v0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vl + static_cast<long long>(i) * HD));
-            o[0] = fmaf(pi, v0.x, o[0]);
-            o[1] = fmaf(pi, v0.y, o[1]);
+    using VT = typename std::conditional<DPL == 4, uint2, uint32_t>::type;  // this lane's DPL bf16 of a row
+#pragma unroll 1
+    for (int i0 = 0; i0 < nk; i0 += kVRows) {  // kVRows V rows in flight per round trip
+        VT raw[kVRows];
+#pragma unroll
+        for (int i = 0; i < kVRows; ++i)
+            if (i0 + i < nk) raw[i] = *reinterpret_cast<const VT*>(vl + static_cast<long long>(i0 + i) * HD);
+#pragma unroll
+        for (int i = 0; i < kVRows; ++i) {
+            if (i0 + i >= nk) break;
+            const float pi = p_s[i0 + i];
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+#pragma unroll
+            for (int e2 = 0; e2 < DPL / 2; ++e2) {
+                const float2 vf = __bfloat1622float2(b2[e2]);
+                o[2 * e2] = fmaf(pi, vf.x, o[2 * e2]);
+                o[2 * e2 + 1] = fmaf(pi, vf.y, o[2 * e2 + 1]);
+            }
         }
     }
     __nv_bfloat16* out = a.attn + static_cast<long long>(t) * a.q_dim + hq * HD + lane * DPL;
@@ -282,7 +286,7 @@ __device__ __forceinline__ void attn_item(const FwdArgs& a, const FwdPhase& P, i
 }
 
 struct FwdSmem {
-    uint64_t fullW[kFwdMaxStages], fullX[kFwdMaxStages], empty[kFwdMaxStages], tfull[2], tempty[2];
+    uint64_t full[kFwdMaxStages], empty[kFwdMaxStages], tfull[2], tempty[2];
     unsigned long long ep;
     uint32_t tslot;
     int sint[12];
@@ -295,6 +299,270 @@ struct FwdSmem {
 };
 static_assert(sizeof(FwdSmem) <= kFwdMiscBytes, "misc shared state exceeds its budget");
 
+// ------------------------------------------------------------------ GEMM tile finisher
+// The last contributor of an output tile sums the split-K partials (fixed contributor order) and
+// applies the fused epilogue.  This runs on the phase's critical path once per tile, with one warp
+// per scheduler, so it is written for instruction-level parallelism: CH-column chunks (16 for decode
+// forwards), loads issued before their uses, butterfly column reductions (31 shuffles per 32 lanes x
+// CH columns) and compile-time loop bounds.
+struct TileCtx {
+    const FwdArgs* a;
+    const FwdPhase* P;
+    int p, m, n_contrib, my, first, tile_u0, U, A;
+    uint32_t taddr;
+    int tp, T, start, q, lane, et, r;
+    float *rs, *red, *sval;
+    int* sidx;
+    unsigned long long tag;  // slot-flag value of this (forward, phase)
+    const float* pre;        // presummed partials of the other contributors (decode), or nullptr
+};
+
+template <int CH>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[CH]) {
+    if constexpr (CH == 16) tmem_ld16(taddr, v);
+    else tmem_ld32(taddr, v);
+}
+
+// lane l ends with the sum over the warp's 32 lanes of column (l % CH)
+template <int CH>
+__device__ __forceinline__ float warp_colsum(float (&v)[CH], int lane) {
+    if constexpr (CH == 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
+    }
+#pragma unroll
+    for (int s = CH / 2; s >= 1; s >>= 1) {
+        const bool hi = (lane & s) != 0;
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            const float send = hi ? v[i] : v[i + s];
+            const float keep = hi ? v[i + s] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+    return v[0];
+}
+// (max value, lowest index) — associative and commutative, so the same butterfly applies
+__device__ __forceinline__ void amax_merge(float& bv, int& bi, float ov, int oi) {
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+}
+template <int CH>
+__device__ __forceinline__ void warp_colmax(float (&v)[CH], int (&id)[CH], int lane) {
+    if constexpr (CH == 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            amax_merge(v[i], id[i], __shfl_xor_sync(0xffffffffu, v[i], 16), __shfl_xor_sync(0xffffffffu, id[i], 16));
+    }
+#pragma unroll
+    for (int s = CH / 2; s >= 1; s >>= 1) {
+        const bool hi = (lane & s) != 0;
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            const float sv = hi ? v[i] : v[i + s];
+            const int si = hi ? id[i] : id[i + s];
+            float kv = hi ? v[i + s] : v[i];
+            int ki = hi ? id[i + s] : id[i];
+            amax_merge(kv, ki, __shfl_xor_sync(0xffffffffu, sv, s), __shfl_xor_sync(0xffffffffu, si, s));
+            v[i] = kv;
+            id[i] = ki;
+        }
+    }
+}
+
+// Split tiles: the tile's first contributor (it processes the tile at the END of its range, the others
+// at the START of theirs) is the designated finisher.  The others store their partial and release a
+// per-slot flag; the finisher waits for the flags (usually long set) and sums the partials in
+// contributor order — for decode forwards before its own accumulator is even ready.
+__device__ __forceinline__ int slot_of(const TileCtx& x, int j) {  // partial slot of contributor first + j
+    const int cj = x.first + j;
+    return 2 * cj + (range_begin(cj, x.U, x.A) >= x.tile_u0 ? 0 : 1);
+}
+__device__ __forceinline__ void wait_partials(const TileCtx& x) {  // et == 0 polls, then the epilogue barrier
+    if (x.et == 0) {
+        for (int j = 1; j < x.n_contrib; ++j) {
+            const unsigned long long* f = x.a->slot_flag + slot_of(x, j);
+            Spin sp;
+            while (ld_relaxed_u64(f) != x.tag) sp.tick(x.a->err, 8, x.p);
+        }
+        fence_acq_rel_gpu();
+    }
+    named_bar_sync(1, 128);
+}
+// pre[i] = p_1 + p_2 + ... + p_{n-1} for columns [ch, ch + 16) of this thread's row
+__device__ __forceinline__ void presum(const TileCtx& x, int ch, float (&pre)[16]) {
+    const FwdArgs& a = *x.a;
+    const int tp = x.tp, nc = min(16, tp - ch);
+    for (int jb = 1; jb < x.n_contrib; jb += kBatch) {
+        float xs[kBatch][16];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const bool load = jb + j < x.n_contrib;
+            const float* Pj = a.ws + static_cast<long long>(load ? slot_of(x, jb + j) : 0) * tp * kBM + ch * kBM + x.r;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) xs[j][i] = (load && i < nc) ? __ldcg(Pj + i * kBM) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            float s2 = jb == 1 ? xs[0][i] : pre[i] + xs[0][i];
+#pragma unroll
+            for (int j = 1; j < kBatch; ++j)
+                if (jb + j < x.n_contrib) s2 += xs[j][i];
+            pre[i] = s2;
+        }
+    }
+}
+
+template <int CH>
+__device__ __forceinline__ void finish_tile(const TileCtx& x) {
+    const FwdArgs& a = *x.a;
+    const FwdPhase& P = *x.P;
+    const int tp = x.tp, T = x.T, lane = x.lane, q = x.q, et = x.et, r = x.r, m = x.m;
+    const int n = m * kBM + r;
+    const int h = a.h;
+    for (int ch = 0; ch < tp; ch += CH) {
+        float v[CH];
+        tmem_ld<CH>(x.taddr + ch, v);
+        const int nc = min(CH, tp - ch);
+        if (x.n_contrib > 1) {  // own + (p_1 + p_2 + ...): fixed contributor order (per shape)
+            float pre[16];
+            if (x.pre) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pre[i] = x.pre[i];
+            } else {
+                presum(x, ch, pre);
+            }
+#pragma unroll
+            for (int i = 0; i < CH; ++i) v[i] += pre[i];
+        }
+        if (et == 0) stamp(a, x.p, 9);
+        if (P.epi == kFeResid) {  // resid += acc; xb = bf16(resid); per-tile sum of squares
+            float* o = a.resid + static_cast<long long>(ch) * h + n;
+            float sq[CH];
+#pragma unroll
+            for (int i = 0; i < CH; ++i) sq[i] = i < nc ? __ldcg(o + static_cast<long long>(i) * h) : 0.f;
+#pragma unroll
+            for (int i = 0; i < CH; ++i) {
+                const float nv = sq[i] + v[i];
+                if (i < nc) {
+                    o[static_cast<long long>(i) * h] = nv;
+                    a.xb[static_cast<long long>(ch + i) * h + n] = __float2bfloat16_rn(nv);
+                }
+                sq[i] = i < nc ? nv * nv : 0.f;
+            }
+            x.red[q * 32 + lane] = warp_colsum<CH>(sq, lane);
+            named_bar_sync(1, 128);
+            if (et < CH && ch + et < tp)
+                a.ssq[m * 256 + ch + et] = ((x.red[et] + x.red[32 + et]) + x.red[64 + et]) + x.red[96 + et];
+            named_bar_sync(1, 128);
+        } else if (P.epi == kFeSilu) {  // rows interleaved 16 gate | 16 up per warp
+            const int f = m * 64 + q * 16 + lane;
+            __nv_bfloat16* o = a.act + static_cast<long long>(ch) * a.ffn_l + f;
+#pragma unroll
+            for (int i = 0; i < CH; ++i) {
+                const float g = v[i] * x.rs[ch + i];
+                const float up = __shfl_down_sync(0xffffffffu, g, 16);
+                if (lane < 16 && i < nc) o[static_cast<long long>(i) * a.ffn_l] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * up);
+            }
+        } else if (P.epi == kFeQkv) {  // rstd scale, q/k RMSNorm, RoPE, q -> qbuf, k/v -> paged KV cache
+            const int hd = a.hd, half = hd >> 1;
+            const bool in_rows = n < P.n_out;  // warp-uniform (n_out % 64 == 0)
+            const bool is_q = n < a.q_dim, is_k = !is_q && n < a.q_dim + a.kv_dim;
+            const int base = is_q ? 0 : is_k ? a.q_dim : a.q_dim + a.kv_dim;
+            const int head = (n - base) / hd, pr = (n - base) % hd, qh = pr >> 5;
+            const int dd = lane < 16 ? 16 * qh + lane : half + 16 * qh + lane - 16;
+            const __nv_bfloat16* nw = is_q ? P.qn : is_k ? P.kn : nullptr;
+            const bool norm = in_rows && nw != nullptr;
+            const float wd = norm ? __bfloat162float(nw[dd]) : 1.f;
+            float xv[CH];
+#pragma unroll
+            for (int i = 0; i < CH; ++i) xv[i] = bf16r(v[i] * x.rs[ch + i]);
+            {
+                float sq[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) sq[i] = xv[i] * xv[i];
+                x.red[q * 32 + lane] = warp_colsum<CH>(sq, lane);
+            }
+            named_bar_sync(1, 128);
+            if (norm) {
+                const int fq = q - qh, nwq = hd >> 5;
+                const float inv_hd = 1.0f / static_cast<float>(hd);
+                float ss[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                    ss[i] = x.red[fq * 32 + i];
+#pragma unroll
+                    for (int w2 = 1; w2 < 4; ++w2)
+                        if (w2 < nwq) ss[i] += x.red[(fq + w2) * 32 + i];
+                }
+#pragma unroll
+                for (int i = 0; i < CH; ++i) xv[i] = bf16r(xv[i] * rsqrtf(ss[i] * inv_hd + a.eps) * wd);
+            }
+            named_bar_sync(1, 128);
+            if (in_rows) {
+                if (is_q || is_k) {  // RoPE: partner dim d +- hd/2 sits in lane ^ 16
+                    const int dm = dd % half;
+                    float2 cs[CH];
+#pragma unroll
+                    for (int i = 0; i < CH; ++i)
+                        cs[i] = ch + i < T ? __ldg(a.rope + static_cast<long long>(x.start + ch + i) * half + dm)
+                                           : make_float2(1.f, 0.f);
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        const float partner = __shfl_xor_sync(0xffffffffu, xv[i], 16);
+                        xv[i] = lane < 16 ? xv[i] * cs[i].x - partner * cs[i].y : xv[i] * cs[i].x + partner * cs[i].y;
+                    }
+                }
+                if (is_q) {
+                    __nv_bfloat16* dq = a.qbuf + (static_cast<long long>(ch) * a.nh + head) * hd + dd;
+#pragma unroll
+                    for (int i = 0; i < CH; ++i)
+                        if (ch + i < T) dq[static_cast<long long>(i) * a.nh * hd] = __float2bfloat16_rn(xv[i]);
+                } else {
+                    __nv_bfloat16* kvc = is_k ? P.kc : P.vc;
+                    int pg[CH];
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) pg[i] = ch + i < T ? __ldg(a.page_table + (x.start + ch + i) / kPage) : 0;
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        const int pos = x.start + ch + i;
+                        if (ch + i < T)
+                            kvc[((static_cast<long long>(pg[i]) * a.nkv + head) * kPage + pos % kPage) * hd + dd] =
+                                __float2bfloat16_rn(xv[i]);
+                    }
+                }
+            }
+        } else {  // kFeLogits: scaled logits; per-tile (max, lowest index) per column
+            const bool ok = n < P.n_out;
+#pragma unroll
+            for (int i = 0; i < CH; ++i) v[i] *= x.rs[ch + i];
+            if (a.logits && ok) {
+#pragma unroll
+                for (int i = 0; i < CH; ++i)
+                    if (i < nc && ch + i < T) a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
+            }
+            int id[CH];
+#pragma unroll
+            for (int i = 0; i < CH; ++i) {
+                id[i] = ok ? n : 0x7fffffff;
+                if (!ok) v[i] = -INFINITY;
+            }
+            warp_colmax<CH>(v, id, lane);
+            if (lane < CH) {
+                x.sval[q * 32 + lane] = v[0];
+                x.sidx[q * 32 + lane] = id[0];
+            }
+            named_bar_sync(1, 128);
+            if (et < CH && et < nc) {
+                float bv = x.sval[et];
+                int bi = x.sidx[et];
+                for (int qq = 1; qq < 4; ++qq) amax_merge(bv, bi, x.sval[qq * 32 + et], x.sidx[qq * 32 + et]);
+                a.amax[static_cast<long long>(m) * tp + ch + et] = make_float2(bv, __int_as_float(bi));
+            }
+            named_bar_sync(1, 128);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ the kernel
 __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_constant__ FwdArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -302,10 +570,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = a.stages, tp = a.tp;
     const int bbytes = tp * kBK * 2;
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + S * kABytes;
-    uint64_t* fullW = sm.fullW;
-    uint64_t* fullX = sm.fullX;
+    uint8_t* sA = smem;                   // stage s: weight tile at sA + s * 16 KiB
+    uint8_t* sB = smem + S * kABytes;     //          activation rows at sB + s * tp * 128 B
+    uint64_t* full = sm.full;  // one barrier per stage: weight tile + activation tile bytes
     uint64_t* empty = sm.empty;
     uint64_t* tfull = sm.tfull;
     uint64_t* tempty = sm.tempty;
@@ -331,8 +598,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         sint[2] = Lc;
         *sep = *reinterpret_cast<volatile unsigned long long*>(a.epoch);
         for (int i = 0; i < S; ++i) {
-            mbar_init(&fullW[i], 1);
-            mbar_init(&fullX[i], 1);
+            mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -360,37 +626,38 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
 
     if (warp == 0) {
         if (lane == 0) {  // ======================================================== TMA producer
+            // One ring of stages (weight tile + the unit's activation rows, one barrier).  Weight tiles are
+            // issued as soon as a slot frees — across phase boundaries, never waiting on data; a stage's
+            // barrier expects both byte counts, so the activation load can follow later (once the phase's
+            // input is complete) and simply completes the transaction.  Only the T valid token rows are
+            // loaded (boxes of 1..16 rows): rows >= T keep stale data that reaches only padded columns.
             for (int i = 0; i < 5; ++i) tma_prefetch_desc(&a.wmaps[i]);
-            for (int i = 0; i < 3; ++i) tma_prefetch_desc(&a.xmaps[i]);
+            const int xb_i = T <= 1 ? 0 : T <= 2 ? 1 : T <= 4 ? 2 : T <= 8 ? 3 : 4;
+            const int x_rows = 1 << xb_i, n_xbox = T <= 16 ? 1 : (T + 15) / 16;
+            const uint32_t stage_tx = static_cast<uint32_t>(kABytes + n_xbox * x_rows * kBK * 2);
+            for (int i = 0; i < 3; ++i) tma_prefetch_desc(&a.xmaps[i][xb_i]);
             Cur w{}, x{};
             seek(w, a, c, G);
             seek(x, a, c, G);
             Ring wr, xr;
-            if (a.simple_producer) {  // A/B reference: in-order, blocking (weights wait on dependencies)
-                int dep_phase = -1;
-                while (w.p < a.n_ph) {
-                    mbar_wait_wd(&empty[wr.st], wr.ph ^ 1u, a.err, 1, w.p);
-                    mbar_arrive_expect_tx(&fullW[wr.st], kABytes);
-                    tma_load_2d(sA + wr.st * kABytes, &a.wmaps[w.wmap], &fullW[wr.st], w.kb * kBK, w.wrow + w.m * kBM,
-                                kEvictFirst);
-                    if (w.p != dep_phase) {
-                        wait_dep(a, w.dep, ep, 1);
-                        fence_proxy_async_global();
-                        dep_phase = w.p;
-                    }
-                    mbar_arrive_expect_tx(&fullX[wr.st], bbytes);
-                    for (int j = 0; j < tp / 16; ++j)
-                        tma_load_2d(sB + wr.st * bbytes + j * 2048, &a.xmaps[w.xmap], &fullX[wr.st], w.kb * kBK, j * 16,
-                                    kEvictLast);
-                    wr.next(S);
-                    step(w, a, c, G);
-                }
-            }
             int pending = 0;  // units whose weights are issued but whose activations are not
             int dep_phase = -1, stamped = -1;
             Spin spin;
             while (w.p < a.n_ph || pending > 0) {
                 bool prog = false;
+                if (w.p < a.n_ph && mbar_test(&empty[wr.st], wr.ph ^ 1u)) {
+                    if (stamped != w.p) {
+                        stamp(a, w.p, 0);
+                        stamped = w.p;
+                    }
+                    mbar_arrive_expect_tx(&full[wr.st], stage_tx);
+                    tma_load_2d(sA + wr.st * kABytes, &a.wmaps[w.wmap], &full[wr.st], w.kb * kBK, w.wrow + w.m * kBM,
+                                kEvictFirst);
+                    wr.next(S);
+                    ++pending;
+                    step(w, a, c, G);
+                    prog = true;
+                }
                 if (pending > 0) {  // activations: only once the phase's input is complete
                     bool ok = x.p == dep_phase;
                     if (!ok && dep_ok(a, x.dep, ep)) {
@@ -400,32 +667,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         stamp(a, x.p, 1);
                     }
                     if (ok) {
-                        if (a.dbg & 1) {
-                            mbar_arrive(&fullX[xr.st]);
-                        } else {
-                            mbar_arrive_expect_tx(&fullX[xr.st], bbytes);
-                            for (int j = 0; j < tp / 16; ++j)
-                                tma_load_2d(sB + xr.st * bbytes + j * 2048, &a.xmaps[x.xmap], &fullX[xr.st],
-                                            x.kb * kBK, j * 16, kEvictLast);
-                        }
+                        for (int j = 0; j < n_xbox; ++j)
+                            tma_load_2d(sB + xr.st * bbytes + j * 2048, &a.xmaps[x.xmap][xb_i], &full[xr.st],
+                                        x.kb * kBK, j * 16, kEvictLast);
                         xr.next(S);
                         --pending;
                         step(x, a, c, G);
                         prog = true;
                     }
-                }
-                if (w.p < a.n_ph && mbar_test(&empty[wr.st], wr.ph ^ 1u)) {  // weights: as soon as a slot frees
-                    if (stamped != w.p) {
-                        stamp(a, w.p, 0);
-                        stamped = w.p;
-                    }
-                    mbar_arrive_expect_tx(&fullW[wr.st], kABytes);
-                    tma_load_2d(sA + wr.st * kABytes, &a.wmaps[w.wmap], &fullW[wr.st], w.kb * kBK, w.wrow + w.m * kBM,
-                                kEvictFirst);
-                    wr.next(S);
-                    ++pending;
-                    step(w, a, c, G);
-                    prog = true;
                 }
                 if (prog) {
                     spin = Spin{};
@@ -446,7 +695,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             const uint32_t idesc = idesc_bf16_m128(tp);
             Cur k{};
             seek(k, a, c, G);
-            Ring rr, tr;  // smem ring; TMEM accumulator ring (nacc buffers)
+            Ring rr, tr;  // stage ring; TMEM accumulator ring (nacc buffers)
             int mma_stamped = -1;
             while (k.p < a.n_ph) {
                 const int p = k.p;
@@ -455,28 +704,22 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                 tc_fence_after();
                 const uint32_t d = tmem + static_cast<uint32_t>(tr.st * a.acc_cols);
                 for (int i = 0; i < n; ++i) {
-                    mbar_wait_wd(&fullW[rr.st], rr.ph, a.err, 3, p);
-                    mbar_wait_wd(&fullX[rr.st], rr.ph, a.err, 4, p);
+                    mbar_wait_wd(&full[rr.st], rr.ph, a.err, 3, p);
                     tc_fence_after();
                     if (p != mma_stamped) {
                         stamp(a, p, 4);  // first MMA of the phase
                         mma_stamped = p;
                     }
-                    if (a.dbg & 2) {
-                        mbar_arrive(&empty[rr.st]);
-                    } else {
-                        const uint64_t ad = umma_desc_sw128(smem_u32(sA + rr.st * kABytes));
-                        const uint64_t bd = umma_desc_sw128(smem_u32(sB + rr.st * bbytes));
+                    const uint64_t ad = umma_desc_sw128(smem_u32(sA + rr.st * kABytes));
+                    const uint64_t bd = umma_desc_sw128(smem_u32(sB + rr.st * bbytes));
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 16; ++kk)
-                            mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-                        mma_commit(&empty[rr.st]);
-                    }
+                    for (int kk = 0; kk < kBK / 16; ++kk)
+                        mma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    mma_commit(&empty[rr.st]);
                     rr.next(S);
                     step(k, a, c, G);
                 }
-                if (a.dbg & 2) mbar_arrive(&tfull[tr.st]);
-                else mma_commit(&tfull[tr.st]);
+                mma_commit(&tfull[tr.st]);
                 tr.next(a.nacc);
                 stamp(a, p, 5);  // last MMA issued (so far) for the phase
             }
@@ -554,6 +797,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     named_bar_sync(1, 128);
                 }
                 const int U = P.units, A = P.active;
+                const unsigned long long tag = (ep << 12) | static_cast<unsigned long long>(p + 1);
                 for (int u = rg.b0; u < rg.b1;) {
                     const int m = u / P.kb;
                     const int tile_u0 = m * P.kb, tile_u1 = tile_u0 + P.kb;
@@ -562,204 +806,36 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     const int n_contrib = static_cast<int>(last - first + 1);
                     const int my = static_cast<int>(rg.ci - first);
                     const int buf = it % a.nacc;
+                    const uint32_t taddr = tmem + static_cast<uint32_t>(buf * a.acc_cols) + (static_cast<uint32_t>(q * 32) << 16);
+                    const bool finisher = my == 0;
+                    const TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
+                                     q, lane, et, r, rs, red, sval, sidx, tag, nullptr};
+                    float pre[16];
+                    const bool early = finisher && n_contrib > 1 && tp == 16;
+                    if (early) {  // the other contributors are (nearly always) done: sum them now
+                        wait_partials(tc);
+                        presum(tc, 0, pre);
+                    }
                     mbar_wait_wd(&tfull[buf], static_cast<uint32_t>((it / a.nacc) & 1), a.err, 6, p);
                     tc_fence_after();
                     if (et == 0) stamp(a, p, 7);  // accumulator of this CTA's latest tile ready
-                    const uint32_t taddr = tmem + static_cast<uint32_t>(buf * a.acc_cols) + (static_cast<uint32_t>(q * 32) << 16);
-                    bool finisher = true;
-                    if (n_contrib > 1) {
+                    if (!finisher) {  // partial -> slot, then release the slot flag
                         const int slot = 2 * rg.ci + (u == rg.b0 ? 0 : 1);
                         float* Pp = a.ws + static_cast<long long>(slot) * tp * kBM;
-                        for (int ch = 0; ch < tp; ch += 32) {
-                            float v[32];
-                            tmem_ld32(taddr + ch, v);
-                            const int nc = min(32, tp - ch);
+                        for (int ch = 0; ch < tp; ch += 16) {
+                            float v[16];
+                            tmem_ld16(taddr + ch, v);
 #pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                if (i < nc) __stcg(Pp + (ch + i) * kBM + r, v[i]);
+                            for (int i = 0; i < 16; ++i) __stcg(Pp + (ch + i) * kBM + r, v[i]);
                         }
                         named_bar_sync(1, 128);
-                        if (et == 0) {  // one acq_rel RMW: releases our partial, acquires the others'
-                            const bool last_in = atom_add_acq_rel_gpu(&a.tile_cnt[m], 1) == n_contrib - 1;
-                            if (last_in) a.tile_cnt[m] = 0;  // reusable by the next split tile here
-                            sint[3] = last_in;
-                        }
-                        named_bar_sync(1, 128);
-                        finisher = sint[3] != 0;
-                    }
-                    if (et == 0 && finisher) stamp(a, p, 8);
-                    if (finisher) {
-                        const int n = m * kBM + r;
-                        for (int ch = 0; ch < tp; ch += 32) {
-                            float v[32];
-                            tmem_ld32(taddr + ch, v);
-                            const int nc = min(32, tp - ch);
-                            if (n_contrib > 1) {  // ordered sum p_first + p_first+1 + ... (fixed per shape)
-#pragma unroll
-                                for (int g = 0; g < 32; g += 16) {
-                                    if (g >= nc) break;
-                                    float acc[16];
-                                    for (int jb = 0; jb < n_contrib; jb += kBatch) {
-                                        float x[kBatch][16];
-#pragma unroll
-                                        for (int j = 0; j < kBatch; ++j) {
-                                            const int cj = first + jb + j;
-                                            const int bj = range_begin(cj, U, A);
-                                            const int slot = 2 * cj + (bj >= tile_u0 ? 0 : 1);
-                                            const float* Pj = a.ws + static_cast<long long>(slot) * tp * kBM + (ch + g) * kBM + r;
-                                            const bool load = jb + j < n_contrib && jb + j != my;
-#pragma unroll
-                                            for (int i = 0; i < 16; ++i)
-                                                x[j][i] = (load && g + i < nc) ? __ldcg(Pj + i * kBM) : v[g + i];
-                                        }
-#pragma unroll
-                                        for (int i = 0; i < 16; ++i) {
-                                            float s2 = jb == 0 ? x[0][i] : acc[i] + x[0][i];
-#pragma unroll
-                                            for (int j = 1; j < kBatch; ++j)
-                                                if (jb + j < n_contrib) s2 += x[j][i];
-                                            acc[i] = s2;
-                                        }
-                                    }
-#pragma unroll
-                                    for (int i = 0; i < 16; ++i) v[g + i] = acc[i];
-                                }
-                            }
-                            if (et == 0) stamp(a, p, 9);
-                            // ---------------------------------------------- fused epilogues
-                            if (P.epi == kFeResid) {
-                                float sq[32];
-                                float* o = a.resid + static_cast<long long>(ch) * h + n;
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) sq[i] = i < nc ? __ldcg(o + static_cast<long long>(i) * h) : 0.f;
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) {
-                                    if (i < nc) {
-                                        const float nv = sq[i] + v[i];
-                                        o[static_cast<long long>(i) * h] = nv;
-                                        a.xb[static_cast<long long>(ch + i) * h + n] = __float2bfloat16_rn(nv);
-                                        sq[i] = nv * nv;
-                                    }
-                                }
-                                red[q * 32 + lane] = warp_colsum32(sq, lane);
-                                named_bar_sync(1, 128);
-                                if (et < 32 && ch + et < tp)
-                                    a.ssq[m * 256 + ch + et] = ((red[et] + red[32 + et]) + red[64 + et]) + red[96 + et];
-                                named_bar_sync(1, 128);
-                            } else if (P.epi == kFeSilu) {
-                                const int f = m * 64 + q * 16 + lane;
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) {
-                                    const float x = i < nc ? v[i] * rs[ch + i] : 0.f;
-                                    const float up = __shfl_down_sync(0xffffffffu, x, 16);
-                                    if (lane < 16 && i < nc)
-                                        a.act[static_cast<long long>(ch + i) * a.ffn_l + f] =
-                                            __float2bfloat16_rn(x / (1.0f + __expf(-x)) * up);
-                                }
-                            } else if (P.epi == kFeQkv) {
-                                const int hd = a.hd, half = hd >> 1;
-                                const bool in_rows = n < P.n_out;  // warp-uniform (n_out % 64 == 0)
-                                const bool is_q = n < a.q_dim, is_k = !is_q && n < a.q_dim + a.kv_dim;
-                                const int base = is_q ? 0 : is_k ? a.q_dim : a.q_dim + a.kv_dim;
-                                const int head = (n - base) / hd, pr = (n - base) % hd, qh = pr >> 5;
-                                const int dd = lane < 16 ? 16 * qh + lane : half + 16 * qh + lane - 16;
-                                const __nv_bfloat16* nw = is_q ? P.qn : is_k ? P.kn : nullptr;
-                                const bool norm = in_rows && nw != nullptr && !(a.dbg & 4);
-                                float x[32];
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) x[i] = bf16r(v[i] * rs[ch + i]);
-                                {
-                                    float sq[32];
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) sq[i] = x[i] * x[i];
-                                    red[q * 32 + lane] = warp_colsum32(sq, lane);
-                                }
-                                if (et == 0) stamp(a, p, 12);
-                                named_bar_sync(1, 128);
-                                if (et == 0) stamp(a, p, 13);
-                                if (norm) {
-                                    const int fq = q - qh, nwq = hd >> 5;
-                                    const float wd = (a.dbg & 32) ? 1.0f : __bfloat162float(nw[dd]);
-                                    const float inv_hd = 1.0f / static_cast<float>(hd);
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) {
-                                        if (a.dbg & 64) break;
-                                        float ss = red[fq * 32 + i];
-                                        for (int w2 = 1; w2 < nwq; ++w2) ss += red[(fq + w2) * 32 + i];
-                                        x[i] = bf16r(x[i] * rsqrtf(ss * inv_hd + a.eps) * wd);
-                                    }
-                                }
-                                if (et == 0) stamp(a, p, 14);
-                                named_bar_sync(1, 128);
-                                if (et == 0) stamp(a, p, 15);
-                                if (in_rows) {
-                                    const int dm = dd % half;
-                                    // RoPE partners, then every table load in flight before any store
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i) {
-                                        const float partner = __shfl_xor_sync(0xffffffffu, x[i], 16);
-                                        if ((is_q || is_k) && !(a.dbg & 8)) {
-                                            const float2 cs = ch + i < T ? __ldg(a.rope + static_cast<long long>(start + ch + i) * half + dm)
-                                                                         : make_float2(1.f, 0.f);
-                                            x[i] = lane < 16 ? x[i] * cs.x - partner * cs.y : x[i] * cs.x + partner * cs.y;
-                                        }
-                                    }
-                                    if (a.dbg & 16) {
-                                    } else if (is_q) {
-                                        __nv_bfloat16* dq = a.qbuf + (static_cast<long long>(ch) * a.nh + head) * hd + dd;
-#pragma unroll
-                                        for (int i = 0; i < 32; ++i)
-                                            if (ch + i < T) dq[static_cast<long long>(i) * a.nh * hd] = __float2bfloat16_rn(x[i]);
-                                    } else {
-                                        __nv_bfloat16* kvc = is_k ? P.kc : P.vc;
-                                        int pg[32];
-#pragma unroll
-                                        for (int i = 0; i < 32; ++i)
-                                            pg[i] = ch + i < T ? __ldg(a.page_table + (start + ch + i) / kPage) : 0;
-#pragma unroll
-                                        for (int i = 0; i < 32; ++i) {
-                                            const int pos = start + ch + i;
-                                            if (ch + i < T)
-                                                kvc[((static_cast<long long>(pg[i]) * a.nkv + head) * kPage + pos % kPage) * hd + dd] =
-                                                    __float2bfloat16_rn(x[i]);
-                                        }
-                                    }
-                                }
-                            } else {  // kFeLogits: scaled logits, per-tile (max, lowest index) per column
-                                const bool ok = n < P.n_out;
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) v[i] *= rs[ch + i];
-                                if (a.logits && ok) {
-#pragma unroll
-                                    for (int i = 0; i < 32; ++i)
-                                        if (i < nc && ch + i < T) a.logits[static_cast<long long>(ch + i) * a.ld_logits + n] = v[i];
-                                }
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) {
-                                    float bv = ok ? v[i] : -INFINITY;
-                                    int bi = ok ? n : 0x7fffffff;
-#pragma unroll
-                                    for (int off = 16; off > 0; off >>= 1) {
-                                        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                                        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                                        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-                                    }
-                                    if (lane == i) { sval[q * 32 + i] = bv; sidx[q * 32 + i] = bi; }
-                                }
-                                named_bar_sync(1, 128);
-                                if (et < 32 && et < nc) {
-                                    float bv = sval[et];
-                                    int bi = sidx[et];
-                                    for (int qq = 1; qq < 4; ++qq) {
-                                        const float ov = sval[qq * 32 + et];
-                                        const int oi = sidx[qq * 32 + et];
-                                        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-                                    }
-                                    a.amax[static_cast<long long>(m) * tp + ch + et] = make_float2(bv, __int_as_float(bi));
-                                }
-                                named_bar_sync(1, 128);
-                            }
-                        }
+                        if (et == 0) st_release_u64(a.slot_flag + slot, tag);
+                    } else {
+                        if (et == 0) stamp(a, p, 8);
+                        if (n_contrib > 1 && !early) wait_partials(tc);
+                        TileCtx tf = tc;
+                        tf.pre = early ? pre : nullptr;
+                        finish_tile<16>(tf);  // 16-column chunks: no spills
                     }
                     if (et == 0 && finisher) stamp(a, p, 10);
                     tc_fence_before();
@@ -785,6 +861,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     if (a.hd == 128) attn_item<128>(a, P, t, hq, j, start, q_s, p_s, lane);
                     else attn_item<64>(a, P, t, hq, j, start, q_s, p_s, lane);
                 }
+                if (lane == 0) stamp(a, p, 8 + ew);  // each aux warp's last item done
                 signal(p);
             } else {  // kPhArgmax ----------------------------------------- final argmax + cursor
                 acquire(P.dep);
@@ -825,14 +902,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
 }
 
 }  // namespace
-
-bool fwd_simple_producer() {
-    static const bool on = [] {
-        const char* e = std::getenv("DBL_FWD_SIMPLE");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
 
 void fwd_prepare() {
     static std::once_flag once;

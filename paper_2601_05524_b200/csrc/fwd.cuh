@@ -53,10 +53,9 @@ struct FwdPhase {
 
 struct FwdArgs {
     CUtensorMap wmaps[5];  // qkv, o, gate|up, down (all layers stacked), lm head
-    CUtensorMap xmaps[3];  // xb, attn, act
+    CUtensorMap xmaps[3][5];  // xb, attn, act; boxes of 1, 2, 4, 8, 16 token rows
     const FwdPhase* ph;
     int n_ph;
-    int simple_producer;   // A/B: 1 = blocking in-order producer (no lookahead across dependencies)
     int dbg;               // DBL_FWD_DBG (timing experiments only; results invalid): 1 no X loads, 2 no MMA
     int tp, stages, nacc, acc_cols;
     LaneState* lane;
@@ -78,7 +77,7 @@ struct FwdArgs {
     int max_seq;
     const int32_t* page_table;
     float* ws;           // stream-K partial slots [2*G][tp][128]
-    int* tile_cnt;       // [max tiles] (self-resetting)
+    unsigned long long* slot_flag;  // [2*G] partial-slot flags: (epoch << 12 | phase + 1) when written
     float2* amax;        // LM-head per-tile (max, idx) [n_tiles][tp]
     float* logits;       // optional fp32 logits rows [T][ld_logits]
     int ld_logits;
@@ -94,10 +93,10 @@ constexpr int kFwdMaxStages = 24;
 constexpr int kFwdSmemBudget = 113 * 1024;  // two CTAs per SM: a draft and a target forward co-reside
 constexpr int kFwdMinUnits = 4;             // smallest stream-K range worth a CTA (4 x 16 KiB)
 
-bool fwd_simple_producer();  // DBL_FWD_SIMPLE=1
 void fwd_prepare();  // kernel attributes (call once, outside graph capture)
 // stages for a token-column bucket; smem bytes returned through *smem
 int fwd_stages(int tp, size_t* smem);
+
 void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s);
 
 // DBL_FWD_TRACE=1: every forward records per-(phase, CTA) %globaltimer stamps — [0] first weight tile

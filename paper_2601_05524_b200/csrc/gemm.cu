@@ -420,6 +420,23 @@ CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int
     return m;
 }
 
+CUtensorMap make_tmap_bf16_kblocks(const void* ptr, uint64_t rows, uint64_t cols, int box_rows, int box_kb) {
+    // [rows][cols] K-major viewed as (64 elements, row, k-block): one box = box_kb consecutive 64-wide
+    // k-blocks of box_rows rows, laid out in shared memory as box_kb stacked [box_rows][64] SW128 tiles
+    CUtensorMap m;
+    if (cols % kBlockK) throw_invalid("GEMM K must be a multiple of 64");
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBlockK), rows, cols / kBlockK};
+    const cuuint64_t strides[2] = {cols * 2, static_cast<cuuint64_t>(kBlockK) * 2};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(kBlockK), static_cast<cuuint32_t>(box_rows),
+                               static_cast<cuuint32_t>(box_kb)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(DBL_CUDA_ERROR, "cuTensorMapEncodeTiled (k-block view) failed: " + std::to_string(r));
+    return m;
+}
+
 void GemmWorkspace::ensure(int sms, int mtp, int mtiles) {
     const int g = 2 * sms + kMaxBatchContrib;  // split-K grids reach tiles * S < sms + tiles * 1
     if (g <= grid && mtp <= max_tp && mtiles <= max_tiles) return;

@@ -60,6 +60,7 @@ struct GemmWorkspace {  // per decode lane (a lane's GEMMs are stream-ordered)
 int num_sms(int device);
 void gemm_prepare();  // set kernel attributes (call before stream capture)
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int box_rows);
+CUtensorMap make_tmap_bf16_kblocks(const void* ptr, uint64_t rows, uint64_t cols, int box_rows, int box_kb);
 
 // Launch one GEMM.  tmW: weights (box 128 x 64), tmX: activations (box 16 x 64).
 // DBL_GEMM_TRACE=1: every GEMM launch records per-CTA %globaltimer stamps (resident, dependency

@@ -63,8 +63,8 @@ struct TfCache final : LaneCache {
     DevBuf<int> attn_cnt, err;
     DevBuf<float2> rope;                    // [capacity][hd/2] (cos, sin)
     DevBuf<FwdPhase> phases;
-    CUtensorMap xmaps[3];
-    DevBuf<unsigned long long> done, epoch;
+    CUtensorMap xmaps[3][5];  // xb, attn, act x boxes of 1, 2, 4, 8, 16 token rows
+    DevBuf<unsigned long long> done, epoch, slot_flag;
     int n_ph = 0;
     GemmWorkspace ws;
     size_t layer_stride = 0;
@@ -228,9 +228,11 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     c.ws.ensure(sms, kMaxTp, max_tiles);
     // ---- the forward's phase list (fwd.cuh); tensor maps: W 0..4 = qkv, o, gate|up, down, lm head;
     // X 0..2 = xb, attn, act
-    c.xmaps[0] = make_tmap_bf16_2d(c.xb.p, kMaxTp, m.h, 16);
-    c.xmaps[1] = make_tmap_bf16_2d(c.attn.p, kMaxTp, m.q_dim, 16);
-    c.xmaps[2] = make_tmap_bf16_2d(c.act.p, kMaxTp, m.ffn_l, 16);
+    for (int b = 0; b < 5; ++b) {
+        c.xmaps[0][b] = make_tmap_bf16_2d(c.xb.p, kMaxTp, m.h, 1 << b);
+        c.xmaps[1][b] = make_tmap_bf16_2d(c.attn.p, kMaxTp, m.q_dim, 1 << b);
+        c.xmaps[2][b] = make_tmap_bf16_2d(c.act.p, kMaxTp, m.ffn_l, 1 << b);
+    }
     const int x_xb = 0, x_attn = 1, x_act = 2;
     std::vector<FwdPhase> ph;
     int offset = 0;
@@ -240,7 +242,7 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
             p.n_tiles = (p.n_out + 127) / 128;
             p.kb = p.K / 64;
             const long long units = static_cast<long long>(p.n_tiles) * p.kb;
-            if (units * (sms + 1) >= (1LL << 31)) throw_invalid("stream forward: projection too large for 32-bit units");
+            if ((units + 1) * (sms + 1) >= (1LL << 31)) throw_invalid("stream forward: projection too large for 32-bit units");
             p.units = static_cast<int>(units);
             p.active = std::max(1, std::min(sms, p.units / kFwdMinUnits));
             p.offset = offset;
@@ -302,6 +304,9 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     c.done.zero();
     c.epoch.alloc(1);
     c.epoch.zero();
+    if (ph.size() >= 4095) throw_invalid("stream forward: too many phases for the slot-flag tag");
+    c.slot_flag.alloc(2 * static_cast<size_t>(sms) + 2);
+    c.slot_flag.zero();
     CUDA_CHECK(cudaDeviceSynchronize());
     return cp;
 }
@@ -320,8 +325,8 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     a.wmaps[2] = m.t_gu;
     a.wmaps[3] = m.t_down;
     a.wmaps[4] = m.t_lm;
-    for (int i = 0; i < 3; ++i) a.xmaps[i] = c.xmaps[i];
-    a.simple_producer = fwd_simple_producer();
+    for (int i = 0; i < 3; ++i)
+        for (int b = 0; b < 5; ++b) a.xmaps[i][b] = c.xmaps[i][b];
     a.dbg = [] {
         const char* e = std::getenv("DBL_FWD_DBG");
         return e ? std::atoi(e) : 0;
@@ -358,7 +363,7 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     a.max_seq = c.capacity;
     a.page_table = c.page_table.p;
     a.ws = c.ws.partials.p;
-    a.tile_cnt = c.ws.counters.p;
+    a.slot_flag = c.slot_flag.p;
     a.amax = c.ws.amax.p;
     a.logits = logits;
     a.ld_logits = ld_logits;

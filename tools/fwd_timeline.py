@@ -111,3 +111,11 @@ for p in range(L0, L0 + 5):
         desc.append(f"c{c}(ci{ci} tiles {b0 // KB}-{(b1 - 1) // KB}) {lag[c]:.1f} [acc/fin/fix/q0/q1/q2/q3/epi/sig/end " +
                     "/".join(f"{x:.1f}" for x in sub) + "]")
     print(f"  {kinds[p]:>8} median {np.median(lag):.1f}:\n      " + "\n      ".join(desc))
+
+ap = L0 + 1  # the middle layer's attention phase
+w_end = st[ap, :, 8:12].max(axis=1)
+prev_done = col(L0, 2, np.max)
+print(f"\nattention (layer {nl // 2}): per-CTA last item done after QKV end: median "
+      f"{(np.median(w_end) - prev_done) / 1e3:.1f} max {(w_end.max() - prev_done) / 1e3:.1f} us; "
+      f"CTA signal max {(col(ap, 2, np.max) - prev_done) / 1e3:.1f} us; epilogue start median "
+      f"{(np.median(st[ap, :, 3]) - prev_done) / 1e3:.1f}")
