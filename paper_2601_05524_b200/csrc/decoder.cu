@@ -780,9 +780,13 @@ void profile_forward(Model& m, int ctx_len, int rows, int iters, double* out) {
         bytes += prof.bytes[k];
         if (per_fwd && k % per_fwd == per_fwd - 1) { lm_ms += ms; lm_bytes += prof.bytes[k]; }
     }
+    // SURVEY §8(d) algorithmic bytes per forward: streamed weights + KV read over the context and
+    // appended for the new rows + the embedding rows gathered
+    const double kv_emb = static_cast<double>(m.kv_bytes_per_token()) * (ctx_len + rows) +
+                          static_cast<double>(m.embed_bytes_per_token()) * rows;
     out[0] = t.ms() / iters;                          // forward ms
-    out[1] = gemm_ms / iters;                          // GEMM ms per forward (event-timed launches)
-    out[2] = bytes / iters;                            // GEMM algorithmic bytes per forward
+    out[1] = gemm_ms / iters;                          // forward-kernel ms (event-timed launches)
+    out[2] = bytes / iters + kv_emb;                   // algorithmic bytes per forward
     out[3] = static_cast<double>(per_fwd);             // GEMM launches per forward
     out[4] = static_cast<double>(launches) / iters;    // kernel launches per forward
     out[5] = static_cast<double>((rows + 15) / 16 * 16);  // token columns (tp)

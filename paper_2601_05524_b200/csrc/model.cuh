@@ -45,6 +45,9 @@ class Model {
     virtual int vocab() const = 0;
     virtual bool has_kv() const = 0;
     virtual int64_t weight_bytes() const { return 0; }
+    // HBM bytes per context position a forward reads from the KV cache (and appends per new row)
+    virtual int64_t kv_bytes_per_token() const { return 0; }
+    virtual int64_t embed_bytes_per_token() const { return 0; }
     virtual std::unique_ptr<LaneCache> make_cache(int capacity) = 0;
     // Enqueue one forward on stream s: process positions [min(kv_len,row0), L+c) of the lane, write
     // lane.argmax[p] for those positions and set lane.start / lane.kv_len = L+c.  `max_tokens` is a

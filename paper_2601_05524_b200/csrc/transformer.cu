@@ -176,6 +176,11 @@ int64_t Transformer::weight_bytes() const {
     return per_layer * cfg_.n_layers + static_cast<int64_t>(m.vocab_l) * m.h * 2 + m.h * 2;
 }
 
+int64_t Transformer::kv_bytes_per_token() const {
+    const Impl& m = *impl_;
+    return static_cast<int64_t>(cfg_.n_layers) * 2 * m.nkv * m.hd * 2;
+}
+
 int Transformer::max_forward_tokens() const { return kMaxTp; }
 
 std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {

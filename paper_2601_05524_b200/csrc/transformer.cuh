@@ -12,6 +12,8 @@ class Transformer final : public Model {
     int vocab() const override { return cfg_.vocab; }
     bool has_kv() const override { return true; }
     int64_t weight_bytes() const override;
+    int64_t kv_bytes_per_token() const override;
+    int64_t embed_bytes_per_token() const override { return static_cast<int64_t>(cfg_.hidden) * 2; }
     std::unique_ptr<LaneCache> make_cache(int capacity) override;
     void forward(Lane& lane, int max_tokens, cudaStream_t s) override;
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
