@@ -40,6 +40,7 @@ typedef enum { DBL_LAYER_PRIOR = 0, DBL_LAYER_DYNAMIC = 1, DBL_LAYER_REJECTED = 
 
 typedef struct dbl_store_s* dbl_store_t;     /* device-resident HierarchicalDatastore */
 typedef struct dbl_model_s* dbl_model_t;     /* device model: table (config 1) or transformer */
+typedef struct dbl_rng_s* dbl_rng_t;         /* specpar::Rng: mt19937_64 stream resident on the device */
 
 const char* dbl_last_error(void);
 int dbl_version(void);
@@ -152,19 +153,44 @@ int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, 
                       int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
                       int64_t jsonl_cap, int64_t* jsonl_len);
 
+/* ===================================================================== verifier + RNG
+ * Replaces specpar::Rng / derive_rng (rng.hpp:19-35) and the verifier interface (verification.hpp:
+ * 30-53, verification.cpp:19-132).  Probability rows are ragged like the reference's ProbVector:
+ * row r = probs[off[r] .. off[r+1]) (fp64), n_rows rows, off[0] = 0.  Draws consume the handle's
+ * mt19937_64 stream exactly as the reference consumes its Rng, so outcomes are bit-identical. */
+typedef enum { DBL_VERIFY_ALL_ACCEPTED = 0, DBL_VERIFY_CORRECTION = 1, DBL_VERIFY_EXTENSION = 2,
+               DBL_VERIFY_RESIDUAL_CORRECTION = 3 } dbl_verify_kind;           /* VerifyKind, verification.hpp:20 */
+int dbl_rng_create(uint64_t seed, int device, dbl_rng_t* out);                  /* Rng(seed), rng.hpp:21 */
+int dbl_rng_derive(uint64_t seed, uint64_t round, uint64_t lane, int device, dbl_rng_t* out); /* derive_rng, rng.hpp:33-35 */
+int dbl_rng_uniform(dbl_rng_t r, double* out, int n);                          /* n x Rng::uniform, rng.hpp:23 */
+int dbl_rng_destroy(dbl_rng_t r);
+int dbl_accept_prob(const double* p, int np, const double* q, int nq, int32_t x, double* out); /* accept_prob, verification.cpp:19-23 */
+int dbl_residual_sample(const double* p, int np, const double* q, int nq, dbl_rng_t r, int32_t* out); /* verification.cpp:40-50 */
+int dbl_residual_sample_point_mass(const double* p, int np, int32_t x, dbl_rng_t r, int32_t* out);    /* verification.cpp:52-58 */
+/* verify_against_target (verification.cpp:60-78): *first_reject = index or -1 (std::nullopt) */
+int dbl_verify_against_target(const int32_t* draft, int n_draft, const double* draft_probs, const int64_t* draft_off,
+                              int n_draft_rows, const double* target_probs, const int64_t* target_off,
+                              int n_target_rows, double temperature, dbl_rng_t r, int* first_reject);
+/* guided_output (verification.cpp:80-132): first_reject = -1 for std::nullopt; committed[cap] */
+int dbl_guided_output(const int32_t* draft, int n_draft, const double* draft_probs, const int64_t* draft_off,
+                      int n_draft_rows, const int32_t* guide_tokens, int n_guide, const double* guide_probs,
+                      const int64_t* guide_off, int n_guide_rows, int first_reject, double temperature, dbl_rng_t r,
+                      int32_t* committed, int cap, int* n_committed, int* accepted_len, int* kind);
+
 /* ===================================================================== kernel-level checks
  * Debug entry points used by the parity tests to exercise one kernel against a host reference.
  * dbl_debug_gemm: W [n_out x K] bf16 bits, X [T x K] bf16 bits, padded to tp token columns.
  *   epi 0 StoreBF16 / 4 StoreF32 -> io[T x n_out]; 1 ResidAdd -> io[T x n_out] += W X^T;
  *   2 SiluMul (16 gate | 16 up rows per 32) -> io[T x n_out/2]; 3 Argmax -> argmax[T], io = logits. */
 /* Times one model forward of `rows` tokens after a ctx_len context (CUDA events, `iters` repeats):
- * out[8] = forward ms, GEMM ms, GEMM algorithmic bytes, GEMM launches, kernel launches (per
- * forward), token columns, LM-head GEMM ms, LM-head bytes.  Feeds bench.py's roofline. */
+ * out[8] = forward ms, forward-kernel ms (per-launch events), algorithmic bytes (SURVEY §8(d):
+ * weights + KV + embedding rows), timed launches, kernel launches (per forward), token columns,
+ * last timed launch ms, its bytes.  Feeds bench.py's roofline. */
 int dbl_profile_forward(dbl_model_t m, int ctx_len, int rows, int iters, double* out);
 /* DBL_GEMM_TRACE=1 timeline of the GEMM launches since the last call: stamps[n][320][4] (%globaltimer
  * ns per CTA: resident, dependency resolved, last load issued, epilogue done), grid and weight bytes */
 int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t* bytes, int* n_launches);
-/* DBL_FWD_TRACE=1: per-(phase, CTA) stamps of the most recent stream forward, [n_ph][grid][4] */
+/* DBL_FWD_TRACE=1: per-(phase, CTA) stamps of the most recent stream forward, [n_ph][grid][16] */
 int dbl_debug_fwd_trace(uint64_t* stamps, int64_t cap, int* n_ph, int* grid);
 /* back-to-back launches of one GEMM shape, ms per launch (weights rotate over `chain` copies) */
 int dbl_debug_gemm_bench(int epi, int n_out, int K, int tp, int iters, int chain, double* ms_per_launch);

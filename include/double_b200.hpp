@@ -6,6 +6,7 @@
 // (std::invalid_argument, std::runtime_error, std::logic_error — pipeline.cpp:18-22, 210-217).
 #pragma once
 #include <cstdint>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -192,6 +193,108 @@ inline RunResult run_vanilla_ar(const Model& target, const TokenSeq& prompt, int
                      r.output.data(), static_cast<int>(r.output.size()), &n, &r.metrics, nullptr, 0, &jl));
     r.output.resize(static_cast<size_t>(n));
     return r;
+}
+
+// ------------------------------------------------------------------ verifier + RNG (verification.hpp, rng.hpp)
+using ProbVector = std::vector<double>;  // types.hpp
+
+class Rng {  // rng.hpp:19-30 — the mt19937_64 stream lives on the device
+  public:
+    explicit Rng(std::uint64_t seed, int device = 0) { check(dbl_rng_create(seed, device, &h_)); }
+    Rng(const Rng&) = delete;
+    Rng& operator=(const Rng&) = delete;
+    Rng(Rng&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    ~Rng() { if (h_) dbl_rng_destroy(h_); }
+    double uniform() {
+        double u = 0.0;
+        check(dbl_rng_uniform(h_, &u, 1));
+        return u;
+    }
+    dbl_rng_t handle() const { return h_; }
+    static Rng derived(std::uint64_t seed, std::uint64_t round, std::uint64_t lane, int device = 0) {
+        dbl_rng_t h = nullptr;
+        check(dbl_rng_derive(seed, round, lane, device, &h));
+        return Rng(h);
+    }
+
+  private:
+    explicit Rng(dbl_rng_t h) : h_(h) {}
+    dbl_rng_t h_ = nullptr;
+};
+inline Rng derive_rng(std::uint64_t seed, std::uint64_t round, std::uint64_t lane) {  // rng.hpp:33-35
+    return Rng::derived(seed, round, lane);
+}
+
+struct SamplerConfig {  // model.hpp:11-14
+    double temperature = 0.0;
+    std::uint64_t rng_seed = 0;
+};
+struct GuidanceChain {  // verification.hpp:13-17
+    TokenSeq tokens;
+    std::vector<ProbVector> probs;
+    int matched_len = 0;
+};
+enum class VerifyKind { AllAccepted, Correction, Extension, ResidualCorrection };  // verification.hpp:20
+struct VerifyOutcome {  // verification.hpp:22-26
+    int accepted_len = 0;
+    TokenSeq committed;
+    VerifyKind kind = VerifyKind::AllAccepted;
+};
+
+namespace detail {
+struct Rows {  // ragged rows -> flat + offsets
+    std::vector<double> data;
+    std::vector<std::int64_t> off{0};
+    explicit Rows(std::span<const ProbVector> rows) {
+        for (const auto& r : rows) {
+            data.insert(data.end(), r.begin(), r.end());
+            off.push_back(static_cast<std::int64_t>(data.size()));
+        }
+        if (data.empty()) data.push_back(0.0);
+    }
+    int n() const { return static_cast<int>(off.size()) - 1; }
+};
+}  // namespace detail
+
+inline double accept_prob(const ProbVector& p, const ProbVector& q, TokenId x) {  // verification.cpp:19-23
+    double out = 0.0;
+    check(dbl_accept_prob(p.data(), static_cast<int>(p.size()), q.data(), static_cast<int>(q.size()), x, &out));
+    return out;
+}
+inline TokenId residual_sample(const ProbVector& p, const ProbVector& q, Rng& rng) {  // :40-50
+    TokenId out = -1;
+    check(dbl_residual_sample(p.data(), static_cast<int>(p.size()), q.data(), static_cast<int>(q.size()),
+                              rng.handle(), &out));
+    return out;
+}
+inline TokenId residual_sample_point_mass(const ProbVector& p, TokenId x, Rng& rng) {  // :52-58
+    TokenId out = -1;
+    check(dbl_residual_sample_point_mass(p.data(), static_cast<int>(p.size()), x, rng.handle(), &out));
+    return out;
+}
+inline std::optional<int> verify_against_target(std::span<const TokenId> draft_tokens,
+                                                std::span<const ProbVector> draft_probs,
+                                                std::span<const ProbVector> target_probs, const SamplerConfig& cfg,
+                                                Rng& rng) {  // verification.cpp:60-78
+    const detail::Rows d(draft_probs), t(target_probs);
+    int fr = -1;
+    check(dbl_verify_against_target(draft_tokens.data(), static_cast<int>(draft_tokens.size()), d.data.data(),
+                                    d.off.data(), d.n(), t.data.data(), t.off.data(), t.n(), cfg.temperature,
+                                    rng.handle(), &fr));
+    return fr < 0 ? std::nullopt : std::optional<int>(fr);
+}
+inline VerifyOutcome guided_output(std::span<const TokenId> draft_tokens, std::span<const ProbVector> draft_probs,
+                                   const GuidanceChain& guidance, std::optional<int> first_reject,
+                                   const SamplerConfig& cfg, Rng& rng) {  // verification.cpp:80-132
+    const detail::Rows d(draft_probs), g(guidance.probs);
+    TokenSeq out(draft_tokens.size() + guidance.tokens.size() + 1);
+    int n = 0, acc = 0, kind = 0;
+    check(dbl_guided_output(draft_tokens.data(), static_cast<int>(draft_tokens.size()), d.data.data(), d.off.data(),
+                            d.n(), guidance.tokens.data(), static_cast<int>(guidance.tokens.size()), g.data.data(),
+                            g.off.data(), g.n(), first_reject ? *first_reject : -1, cfg.temperature, rng.handle(),
+                            out.data(), static_cast<int>(out.size()), &n, &acc, &kind));
+    out.resize(static_cast<size_t>(n));
+    return VerifyOutcome{acc, out, static_cast<VerifyKind>(kind)};
 }
 
 }  // namespace specpar_b200

@@ -357,3 +357,160 @@ def reference_or_none():
         return Reference()
     except (FileNotFoundError, OSError):
         return None
+
+
+# --------------------------------------------------------------------------- verifier (T >= 0)
+class OracleInvalidArgument(OracleError):  # std::invalid_argument
+    pass
+
+
+class OracleRuntimeError(OracleError):  # std::runtime_error
+    pass
+
+
+def _rows(rows):
+    rows = [list(map(float, r)) for r in (rows or [])]
+    off = [0]
+    for r in rows:
+        off.append(off[-1] + len(r))
+    flat = [x for r in rows for x in r]
+    return (C.c_double * max(1, len(flat)))(*flat), (C.c_long * len(off))(*off), len(rows)
+
+
+def _dbl(xs):
+    xs = [float(x) for x in xs]
+    return (C.c_double * max(1, len(xs)))(*xs)
+
+
+def _splitmix64(x: int) -> int:  # rng.hpp:8-13
+    M = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D49BB133111EB) & M  # the reference's constant (rng.hpp:11)
+    return x ^ (x >> 31)
+
+
+class _MT64(C.Structure):
+    _fields_ = [("mt", C.c_uint64 * 312), ("idx", C.c_int)]
+
+
+class _VerifierCalls:
+    """The five verifier functions over either checker; `rng` objects come from .rng()/.derive_rng()."""
+
+    def _call(self, rc):
+        if rc == -1:
+            raise OracleInvalidArgument(self._msg())
+        if rc != 0:
+            raise OracleRuntimeError(self._msg())
+
+    def accept_prob(self, p, q, x):
+        out = C.c_double()
+        self._call(self._f["accept"](_dbl(p), len(p), _dbl(q), len(q), x, C.byref(out)))
+        return out.value
+
+    def residual_sample(self, p, q, rng):
+        out = C.c_int()
+        self._call(self._f["residual"](_dbl(p), len(p), _dbl(q), len(q), self._rp(rng), C.byref(out)))
+        return out.value
+
+    def residual_sample_point_mass(self, p, x, rng):
+        out = C.c_int()
+        self._call(self._f["point"](_dbl(p), len(p), x, self._rp(rng), C.byref(out)))
+        return out.value
+
+    def verify_against_target(self, draft, draft_probs, target_probs, temperature, rng):
+        dp, doff, nd = _rows(draft_probs)
+        tp, toff, nt = _rows(target_probs)
+        out = C.c_int()
+        self._call(self._f["verify"](_ints(draft), len(draft), dp, doff, nd, tp, toff, nt, float(temperature),
+                                     self._rp(rng), C.byref(out)))
+        return None if out.value < 0 else out.value
+
+    def guided_output(self, draft, draft_probs, guide_tokens, guide_probs, first_reject, temperature, rng):
+        dp, doff, nd = _rows(draft_probs)
+        gp, goff, ng = _rows(guide_probs)
+        cap = len(draft) + len(guide_tokens) + 1
+        out = (C.c_int * cap)()
+        n, acc, kind = C.c_int(), C.c_int(), C.c_int()
+        self._call(self._f["guided"](_ints(draft), len(draft), dp, doff, nd, _ints(guide_tokens), len(guide_tokens),
+                                     gp, goff, ng, -1 if first_reject is None else int(first_reject),
+                                     float(temperature), self._rp(rng), out, cap, C.byref(n), C.byref(acc),
+                                     C.byref(kind)))
+        return acc.value, list(out[:n.value]), ["all_accepted", "correction", "extension",
+                                                "residual_correction"][kind.value]
+
+
+class OracleVerifier(_VerifierCalls):
+    def __init__(self, oracle: Oracle):
+        L = oracle.lib
+        self._msg = lambda: L.orc_last_error().decode()
+        rows = [C.c_void_p, C.POINTER(C.c_long), C.c_int]
+        dbl = [C.POINTER(C.c_double), C.c_int]
+        L.orc_mt64_seed.argtypes = [C.POINTER(_MT64), C.c_uint64]
+        L.orc_uniform.restype = C.c_double
+        L.orc_uniform.argtypes = [C.POINTER(_MT64)]
+        L.orc_accept_prob.argtypes = dbl + dbl + [C.c_int, C.POINTER(C.c_double)]
+        L.orc_residual_sample.argtypes = dbl + dbl + [C.POINTER(_MT64), IntP]
+        L.orc_residual_point_mass.argtypes = dbl + [C.c_int, C.POINTER(_MT64), IntP]
+        L.orc_verify_against_target.argtypes = [IntP, C.c_int] + rows + rows + [C.c_double, C.POINTER(_MT64), IntP]
+        L.orc_guided_output.argtypes = ([IntP, C.c_int] + rows + [IntP, C.c_int] + rows +
+                                        [C.c_int, C.c_double, C.POINTER(_MT64), IntP, C.c_int, IntP, IntP, IntP])
+        self._f = {"accept": L.orc_accept_prob, "residual": L.orc_residual_sample,
+                   "point": L.orc_residual_point_mass, "verify": L.orc_verify_against_target,
+                   "guided": L.orc_guided_output}
+        self._L = L
+        self._rp = lambda r: C.byref(r)
+
+    def rng(self, seed: int):  # Rng(seed)
+        g = _MT64()
+        self._L.orc_mt64_seed(C.byref(g), C.c_uint64(seed))
+        return g
+
+    def derive_rng(self, seed: int, round_: int, lane: int):  # rng.hpp:33-35
+        M = (1 << 64) - 1
+        return self.rng(_splitmix64((seed ^ _splitmix64((round_ * 4 + lane + 1) & M)) & M))
+
+    def uniform(self, g):
+        return self._L.orc_uniform(C.byref(g))
+
+
+class ReferenceVerifier(_VerifierCalls):
+    def __init__(self, ref: "Reference"):
+        L = ref.lib
+        self._msg = lambda: L.ref_last_error().decode()
+        rows = [C.c_void_p, C.POINTER(C.c_long), C.c_int]
+        dbl = [C.POINTER(C.c_double), C.c_int]
+        L.ref_rng_new.restype = C.c_void_p
+        L.ref_rng_new.argtypes = [C.c_ulonglong]
+        L.ref_rng_derive.restype = C.c_void_p
+        L.ref_rng_derive.argtypes = [C.c_ulonglong, C.c_ulonglong, C.c_ulonglong]
+        L.ref_rng_free.argtypes = [C.c_void_p]
+        L.ref_rng_uniform.restype = C.c_double
+        L.ref_rng_uniform.argtypes = [C.c_void_p]
+        L.ref_accept_prob.argtypes = dbl + dbl + [C.c_int, C.POINTER(C.c_double)]
+        L.ref_residual_sample.argtypes = dbl + dbl + [C.c_void_p, IntP]
+        L.ref_residual_point_mass.argtypes = dbl + [C.c_int, C.c_void_p, IntP]
+        L.ref_verify_against_target.argtypes = [IntP, C.c_int] + rows + rows + [C.c_double, C.c_void_p, IntP]
+        L.ref_guided_output.argtypes = ([IntP, C.c_int] + rows + [IntP, C.c_int] + rows +
+                                        [C.c_int, C.c_double, C.c_void_p, IntP, C.c_int, IntP, IntP, IntP])
+        self._f = {"accept": L.ref_accept_prob, "residual": L.ref_residual_sample,
+                   "point": L.ref_residual_point_mass, "verify": L.ref_verify_against_target,
+                   "guided": L.ref_guided_output}
+        self._L = L
+        self._rp = lambda r: r.h
+
+    class _Rng:
+        def __init__(self, L, h):
+            self.L, self.h = L, C.c_void_p(h)
+
+        def __del__(self):
+            self.L.ref_rng_free(self.h)
+
+    def rng(self, seed: int):
+        return self._Rng(self._L, self._L.ref_rng_new(seed))
+
+    def derive_rng(self, seed: int, round_: int, lane: int):
+        return self._Rng(self._L, self._L.ref_rng_derive(seed, round_, lane))
+
+    def uniform(self, g):
+        return self._L.ref_rng_uniform(g.h)

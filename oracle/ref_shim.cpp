@@ -9,6 +9,9 @@
 // '>' scan, lowest id on ties, model.cpp:70-81 — returns exactly the callback's id).  All other
 // TableModels go to the real implementation.
 #include <cstring>
+#include <functional>
+#include <optional>
+#include <vector>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -18,6 +21,7 @@
 #include "specpar/harness.hpp"
 #include "specpar/model.hpp"
 #include "specpar/pipeline.hpp"
+#include "specpar/verification.hpp"
 
 using namespace specpar;
 
@@ -284,4 +288,72 @@ int ref_run_callback(int vocab, ref_argmax_fn draft_fn, void* draft_user, ref_ar
     return rc;
 }
 
+}  // extern "C"
+
+// ---- verifier (verification.cpp:19-132) over the unmodified reference; a Rng handle per stream
+namespace {
+std::vector<ProbVector> rows_of(const double* data, const long* off, int n) {
+    std::vector<ProbVector> r;
+    for (int i = 0; i < n; ++i) r.emplace_back(data + off[i], data + off[i + 1]);
+    return r;
+}
+int ref_guard(const std::function<void()>& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -2;
+    }
+}
+}  // namespace
+
+extern "C" {
+void* ref_rng_new(unsigned long long seed) { return new Rng(seed); }
+void* ref_rng_derive(unsigned long long seed, unsigned long long round, unsigned long long lane) {
+    return new Rng(derive_rng(seed, round, lane));
+}
+void ref_rng_free(void* r) { delete static_cast<Rng*>(r); }
+double ref_rng_uniform(void* r) { return static_cast<Rng*>(r)->uniform(); }
+int ref_accept_prob(const double* p, int np, const double* q, int nq, int x, double* out) {
+    return ref_guard([&] { *out = accept_prob(ProbVector(p, p + np), ProbVector(q, q + nq), x); });
+}
+int ref_residual_sample(const double* p, int np, const double* q, int nq, void* rng, int* out) {
+    return ref_guard([&] { *out = residual_sample(ProbVector(p, p + np), ProbVector(q, q + nq), *static_cast<Rng*>(rng)); });
+}
+int ref_residual_point_mass(const double* p, int np, int x, void* rng, int* out) {
+    return ref_guard([&] { *out = residual_sample_point_mass(ProbVector(p, p + np), x, *static_cast<Rng*>(rng)); });
+}
+int ref_verify_against_target(const int* draft, int n_draft, const double* dp, const long* doff, int n_dp,
+                              const double* tp, const long* toff, int n_tp, double temperature, void* rng,
+                              int* first_reject) {
+    return ref_guard([&] {
+        const std::vector<ProbVector> d = rows_of(dp, doff, n_dp), t = rows_of(tp, toff, n_tp);
+        const std::vector<TokenId> dt(draft, draft + n_draft);
+        SamplerConfig cfg{temperature, 0};
+        const std::optional<int> r = verify_against_target(dt, d, t, cfg, *static_cast<Rng*>(rng));
+        *first_reject = r ? *r : -1;
+    });
+}
+int ref_guided_output(const int* draft, int n_draft, const double* dp, const long* doff, int n_dp, const int* gtok,
+                      int n_gtok, const double* gp, const long* goff, int n_gp, int first_reject, double temperature,
+                      void* rng, int* committed, int cap, int* n_committed, int* accepted_len, int* kind) {
+    return ref_guard([&] {
+        const std::vector<ProbVector> d = rows_of(dp, doff, n_dp);
+        GuidanceChain g;
+        g.tokens.assign(gtok, gtok + n_gtok);
+        g.probs = rows_of(gp, goff, n_gp);
+        const std::vector<TokenId> dt(draft, draft + n_draft);
+        SamplerConfig cfg{temperature, 0};
+        const std::optional<int> fr = first_reject < 0 ? std::nullopt : std::optional<int>(first_reject);
+        const VerifyOutcome o = guided_output(dt, d, g, fr, cfg, *static_cast<Rng*>(rng));
+        *n_committed = static_cast<int>(o.committed.size());
+        *accepted_len = o.accepted_len;
+        *kind = static_cast<int>(o.kind);
+        for (int i = 0; i < *n_committed && i < cap; ++i) committed[i] = o.committed[static_cast<size_t>(i)];
+    });
+}
 }  // extern "C"

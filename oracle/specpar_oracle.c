@@ -1229,3 +1229,126 @@ int orc_replay_target(void* user, const int* ctx, int L, const int* cands, int c
         out[rd->n_spec + s] = s < rd->ext_m ? cands[rd->n_spec + s] : e;
     return 0;
 }
+
+
+/* ===================================================================== verifier (T >= 0)
+ * verification.cpp:19-132.  Rows are ragged like ProbVector: row r = probs[off[r] .. off[r+1]).
+ * Errors: -1 std::invalid_argument, -2 std::runtime_error (message in orc_last_error()). */
+int orc_accept_prob(const double* p, int np, const double* q, int nq, int x, double* out) { /* :19-23 */
+    if (x < 0 || x >= nq || x >= np) { (void)fail("token out of range"); return -1; }
+    if (q[x] <= 0.0) { (void)fail("draft mass zero on emitted token"); return -1; }
+    *out = p[x] / q[x] < 1.0 ? p[x] / q[x] : 1.0;
+    return 0;
+}
+
+static int orc_sample_from(const double* w, int n, double total, orc_mt64* g) { /* :25-38 */
+    const double u = orc_uniform(g) * total;
+    double acc = 0.0;
+    int last = -1;
+    for (int i = 0; i < n; ++i) {
+        if (w[i] <= 0.0) continue;
+        last = i;
+        acc += w[i];
+        if (u < acc) return last;
+    }
+    return last;
+}
+
+int orc_residual_sample(const double* p, int np, const double* q, int nq, orc_mt64* g, int* out) { /* :40-50 */
+    if (nq < np) { (void)fail("residual: q shorter than p"); return -1; }
+    double* res = (double*)malloc(sizeof(double) * (size_t)(np > 0 ? np : 1));
+    double total = 0.0;
+    for (int i = 0; i < np; ++i) {
+        res[i] = p[i] - q[i] > 0.0 ? p[i] - q[i] : 0.0;
+        total += res[i];
+    }
+    if (total <= 0.0) { free(res); (void)fail("residual distribution is zero"); return -2; }
+    *out = orc_sample_from(res, np, total, g);
+    free(res);
+    return 0;
+}
+
+int orc_residual_point_mass(const double* p, int np, int x, orc_mt64* g, int* out) { /* :52-58 */
+    if (x < 0 || x >= np) { (void)fail("token out of range"); return -1; }
+    double* res = (double*)malloc(sizeof(double) * (size_t)np);
+    double total = 0.0;
+    for (int i = 0; i < np; ++i) res[i] = i == x ? 0.0 : p[i];
+    for (int i = 0; i < np; ++i) total += res[i];
+    if (total <= 0.0) { free(res); (void)fail("residual distribution is zero"); return -2; }
+    *out = orc_sample_from(res, np, total, g);
+    free(res);
+    return 0;
+}
+
+int orc_verify_against_target(const int* draft, int n_draft, const double* dp, const int64_t* doff, int n_dp,
+                              const double* tp, const int64_t* toff, int n_tp, double temperature, orc_mt64* g,
+                              int* first_reject) { /* :60-78 */
+    *first_reject = -1;
+    if (n_tp < n_draft) { (void)fail("target_probs does not cover the draft slice"); return -1; }
+    for (int k = 0; k < n_draft; ++k) {
+        if (temperature == 0.0) {
+            const int a = orc_argmax(tp + toff[k], (int)(toff[k + 1] - toff[k]));
+            if (a < 0) { (void)fail("degenerate distribution"); return -2; }
+            if (draft[k] != a) { *first_reject = k; return 0; }
+        } else {
+            double a;
+            if (k >= n_dp) { (void)fail("draft_probs does not cover the draft slice"); return -1; }
+            const int rc = orc_accept_prob(tp + toff[k], (int)(toff[k + 1] - toff[k]), dp + doff[k],
+                                           (int)(doff[k + 1] - doff[k]), draft[k], &a);
+            if (rc) return rc;
+            if (orc_uniform(g) >= a) { *first_reject = k; return 0; }
+        }
+    }
+    return 0;
+}
+
+int orc_guided_output(const int* draft, int n_draft, const double* dp, const int64_t* doff, int n_dp,
+                      const int* gtok, int n_gtok, const double* gp, const int64_t* goff, int n_gp,
+                      int first_reject, double temperature, orc_mt64* g, int* committed, int cap,
+                      int* n_committed, int* accepted_len, int* kind) { /* :80-132 */
+    int n = 0;
+#define ORC_PUSH(t) do { if (n < cap) committed[n] = (t); ++n; } while (0)
+    if (first_reject < 0) {
+        *accepted_len = n_draft;
+        for (int i = 0; i < n_draft; ++i) ORC_PUSH(draft[i]);
+        *kind = 0; /* AllAccepted */
+        int covers = temperature == 0.0 && n_gtok > n_draft;
+        for (int i = 0; covers && i < n_draft; ++i) covers = draft[i] == gtok[i];
+        if (covers) {
+            for (int i = n_draft; i < n_gtok; ++i) ORC_PUSH(gtok[i]);
+            *kind = 2; /* Extension */
+        }
+        *n_committed = n;
+        return 0;
+    }
+    const int i = first_reject;
+    if (i > n_draft) { (void)fail("reject index past the draft slice"); return -1; }
+    *accepted_len = i;
+    for (int k = 0; k < i; ++k) ORC_PUSH(draft[k]);
+    if (temperature == 0.0) {
+        if (i < n_gtok) {
+            for (int k = i; k < n_gtok; ++k) ORC_PUSH(gtok[k]);
+        } else if (i < n_gp) {
+            const int a = orc_argmax(gp + goff[i], (int)(goff[i + 1] - goff[i]));
+            if (a < 0) { (void)fail("degenerate distribution"); return -2; }
+            ORC_PUSH(a);
+        } else {
+            (void)fail("guided_output: reject position uncovered");
+            return -1;
+        }
+        *kind = 1; /* Correction */
+        *n_committed = n;
+        return 0;
+    }
+    if (i >= n_gp) { (void)fail("guided_output: reject position uncovered"); return -1; }
+    if (i >= n_dp) { (void)fail("draft_probs does not cover the reject position"); return -1; }
+    int t;
+    const int rc = orc_residual_sample(gp + goff[i], (int)(goff[i + 1] - goff[i]), dp + doff[i],
+                                       (int)(doff[i + 1] - doff[i]), g, &t);
+    if (rc) return rc;
+    ORC_PUSH(t);
+    *kind = 3; /* ResidualCorrection */
+    *n_committed = n;
+#undef ORC_PUSH
+    return 0;
+}

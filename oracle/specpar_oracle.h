@@ -9,8 +9,9 @@
  * and tests/test_oracle.py checks this file against them (config-1 traces and model/prior
  * serialisations by sha256, the 100-config acceptance set, lookup known-answer cases).
  *
- * Greedy (temperature 0) only: in greedy mode the reference consumes a distribution solely through
- * argmax_token (model.cpp:70-81), so models enter the loop as "argmax row" callbacks.
+ * The decode loop is greedy (temperature 0): there the reference consumes a distribution solely
+ * through argmax_token (model.cpp:70-81), so models enter the loop as "argmax row" callbacks.  The
+ * verifier functions (verification.cpp:19-132) are restated for T >= 0 over explicit rows.
  */
 #ifndef SPECPAR_ORACLE_H
 #define SPECPAR_ORACLE_H
@@ -94,6 +95,19 @@ void orc_replay_free(orc_replay* r);
 void orc_replay_reset(orc_replay* r);
 int orc_replay_draft(void* replay, const int* ctx, int L, const int* cands, int c, int* out);
 int orc_replay_target(void* replay, const int* ctx, int L, const int* cands, int c, int* out);
+
+/* ---- verification.cpp:19-132 (T >= 0): ragged rows row r = probs[off[r] .. off[r+1]);
+ *      returns 0, -1 (std::invalid_argument) or -2 (std::runtime_error) ---- */
+int orc_accept_prob(const double* p, int np, const double* q, int nq, int x, double* out);
+int orc_residual_sample(const double* p, int np, const double* q, int nq, orc_mt64* g, int* out);
+int orc_residual_point_mass(const double* p, int np, int x, orc_mt64* g, int* out);
+int orc_verify_against_target(const int* draft, int n_draft, const double* dp, const int64_t* doff, int n_dp,
+                              const double* tp, const int64_t* toff, int n_tp, double temperature, orc_mt64* g,
+                              int* first_reject);
+int orc_guided_output(const int* draft, int n_draft, const double* dp, const int64_t* doff, int n_dp,
+                      const int* gtok, int n_gtok, const double* gp, const int64_t* goff, int n_gp,
+                      int first_reject, double temperature, orc_mt64* g, int* committed, int cap,
+                      int* n_committed, int* accepted_len, int* kind);
 
 const char* orc_last_error(void);
 void orc_free(void* p);

@@ -89,6 +89,18 @@ PROTOTYPES = {
     "dbl_debug_gemm_trace": [C.POINTER(C.c_uint64), C.c_int64, I32P, I64P, C.POINTER(C.c_int)],
     "dbl_debug_fwd_trace": [C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "dbl_debug_gemm_bench": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, F64P],
+    "dbl_rng_create": [C.c_uint64, C.c_int, C.POINTER(VP)],
+    "dbl_rng_derive": [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(VP)],
+    "dbl_rng_uniform": [VP, F64P, C.c_int],
+    "dbl_rng_destroy": [VP],
+    "dbl_accept_prob": [F64P, C.c_int, F64P, C.c_int, C.c_int32, F64P],
+    "dbl_residual_sample": [F64P, C.c_int, F64P, C.c_int, VP, I32P],
+    "dbl_residual_sample_point_mass": [F64P, C.c_int, C.c_int32, VP, I32P],
+    "dbl_verify_against_target": [I32P, C.c_int, F64P, I64P, C.c_int, F64P, I64P, C.c_int, C.c_double, VP,
+                                  C.POINTER(C.c_int)],
+    "dbl_guided_output": [I32P, C.c_int, F64P, I64P, C.c_int, I32P, C.c_int, F64P, I64P, C.c_int, C.c_int,
+                          C.c_double, VP, I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                          C.POINTER(C.c_int)],
     "dbl_debug_gemm": [C.c_int, U16P, C.c_int, C.c_int, U16P, C.c_int, C.c_int, C.c_int, F32P,
                        I32P],
 }

@@ -9,6 +9,7 @@
 #include "table_model.cuh"
 #include "transformer.cuh"
 #include "fwd.cuh"
+#include "verify.cuh"
 #include "gemm.cuh"
 #include "lane.cuh"
 #include "tf_kernels.cuh"
@@ -375,6 +376,90 @@ int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t*
 }
 
 // --------------------------------------------------------------------------- kernel checks
+// ------------------------------------------------------------------------ verifier + RNG
+struct dbl_rng_s {
+    std::unique_ptr<dbl::DeviceRng> impl;
+};
+
+int dbl_rng_create(uint64_t seed, int device, dbl_rng_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = new dbl_rng_s{std::make_unique<dbl::DeviceRng>(seed, device)};
+    });
+}
+int dbl_rng_derive(uint64_t seed, uint64_t round, uint64_t lane, int device, dbl_rng_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = new dbl_rng_s{std::make_unique<dbl::DeviceRng>(dbl::DeviceRng::derive(seed, round, lane, device))};
+    });
+}
+int dbl_rng_uniform(dbl_rng_t r, double* out, int n) {
+    return guarded([&] {
+        need(r, "rng");
+        r->impl->uniform(out, n);
+    });
+}
+int dbl_rng_destroy(dbl_rng_t r) {
+    return guarded([&] { delete r; });
+}
+int dbl_accept_prob(const double* p, int np, const double* q, int nq, int32_t x, double* out) {
+    return guarded([&] {
+        need(p, "p");
+        need(q, "q");
+        need(out, "out");
+        *out = dbl::accept_prob(p, np, q, nq, x, 0);
+    });
+}
+int dbl_residual_sample(const double* p, int np, const double* q, int nq, dbl_rng_t r, int32_t* out) {
+    return guarded([&] {
+        need(p, "p");
+        need(q, "q");
+        need(r, "rng");
+        need(out, "out");
+        *out = dbl::residual_sample(p, np, q, nq, *r->impl);
+    });
+}
+int dbl_residual_sample_point_mass(const double* p, int np, int32_t x, dbl_rng_t r, int32_t* out) {
+    return guarded([&] {
+        need(p, "p");
+        need(r, "rng");
+        need(out, "out");
+        *out = dbl::residual_sample_point_mass(p, np, x, *r->impl);
+    });
+}
+int dbl_verify_against_target(const int32_t* draft, int n_draft, const double* draft_probs, const int64_t* draft_off,
+                              int n_draft_rows, const double* target_probs, const int64_t* target_off,
+                              int n_target_rows, double temperature, dbl_rng_t r, int* first_reject) {
+    return guarded([&] {
+        need(r, "rng");
+        need(first_reject, "first_reject");
+        *first_reject = dbl::verify_against_target(draft, n_draft, draft_probs, draft_off, n_draft_rows, target_probs,
+                                                   target_off, n_target_rows, temperature, *r->impl);
+    });
+}
+int dbl_guided_output(const int32_t* draft, int n_draft, const double* draft_probs, const int64_t* draft_off,
+                      int n_draft_rows, const int32_t* guide_tokens, int n_guide, const double* guide_probs,
+                      const int64_t* guide_off, int n_guide_rows, int first_reject, double temperature, dbl_rng_t r,
+                      int32_t* committed, int cap, int* n_committed, int* accepted_len, int* kind) {
+    return guarded([&] {
+        need(r, "rng");
+        need(n_committed, "n_committed");
+        need(accepted_len, "accepted_len");
+        need(kind, "kind");
+        const dbl::VerifyOutcome o =
+            dbl::guided_output(draft, n_draft, draft_probs, draft_off, n_draft_rows, guide_tokens, n_guide,
+                               guide_probs, guide_off, n_guide_rows, first_reject, temperature, *r->impl);
+        *n_committed = static_cast<int>(o.committed.size());
+        *accepted_len = o.accepted_len;
+        *kind = o.kind;
+        if (static_cast<int>(o.committed.size()) > cap) dbl::throw_invalid("committed buffer too small");
+        if (!o.committed.empty()) {
+            need(committed, "committed");
+            std::memcpy(committed, o.committed.data(), o.committed.size() * 4);
+        }
+    });
+}
+
 int dbl_debug_fwd_trace(uint64_t* stamps, int64_t cap, int* n_ph, int* grid) {
     return guarded([&] {
         need(n_ph, "n_ph");

@@ -1,0 +1,352 @@
+// The verifier API (verification.hpp:30-53) and the reference's deterministic RNG
+// (rng.hpp:8-35) on the device.
+//
+// These are API-completeness entry points over explicit probability vectors (the decode loop itself
+// is greedy and never materialises distributions).  They run as single-thread fp64 kernels so every
+// sum is accumulated in the reference's order and every decision — including each mt19937_64 draw —
+// is bit-identical to specpar::guided_output & co.  Ragged rows (the reference's ProbVector is a
+// std::vector<double> per position) are passed flattened with row offsets.
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "verify.cuh"
+
+namespace dbl {
+
+namespace {
+
+// std::mt19937_64, standard parameters (the engine behind specpar::Rng, rng.hpp:19-30)
+__host__ __device__ inline void mt_seed(DevRng& g, uint64_t seed) {
+    g.mt[0] = seed;
+    for (int i = 1; i < 312; ++i) g.mt[i] = 6364136223846793005ULL * (g.mt[i - 1] ^ (g.mt[i - 1] >> 62)) + i;
+    g.idx = 312;
+}
+__device__ inline uint64_t mt_next(DevRng& g) {
+    if (g.idx >= 312) {
+        for (int i = 0; i < 312; ++i) {
+            const uint64_t x = (g.mt[i] & 0xFFFFFFFF80000000ULL) | (g.mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+            uint64_t xa = x >> 1;
+            if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
+            g.mt[i] = g.mt[(i + 156) % 312] ^ xa;
+        }
+        g.idx = 0;
+    }
+    uint64_t y = g.mt[g.idx++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+}
+// Rng::uniform (rng.hpp:23): the top 53 bits of one word
+__device__ inline double mt_uniform(DevRng& g) { return static_cast<double>(mt_next(g) >> 11) * 0x1.0p-53; }
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // rng.hpp:8-13
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d49bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+struct Rows {  // ragged fp64 rows: row r = data[off[r], off[r+1])
+    const double* data;
+    const int64_t* off;
+    int n;
+    __device__ const double* row(int r) const { return data + off[r]; }
+    __device__ int len(int r) const { return static_cast<int>(off[r + 1] - off[r]); }
+};
+
+__device__ int argmax_row(const double* p, int n, int* err) {  // model.cpp:70-81 (ties -> lowest id)
+    int best = 0;
+    double bp = -1.0;
+    for (int i = 0; i < n; ++i)
+        if (p[i] > bp) { bp = p[i]; best = i; }
+    if (bp <= 0.0) *err = kErrDegenerate;
+    return best;
+}
+// sample_from (verification.cpp:25-38): u = uniform * total, first prefix sum exceeding u
+__device__ int sample_from(const double* w, int n, double total, DevRng& g) {
+    const double u = mt_uniform(g) * total;
+    double acc = 0.0;
+    int last = -1;
+    for (int i = 0; i < n; ++i) {
+        if (w[i] <= 0.0) continue;
+        last = i;
+        acc += w[i];
+        if (u < acc) return last;
+    }
+    return last;
+}
+// residual_sample (verification.cpp:40-50): max(0, p - q), then sample_from; q covers p's length
+__device__ int residual_sample_dev(const double* p, int np, const double* q, int nq, DevRng& g, int* err) {
+    if (nq < np) { *err = kErrArgument; return -1; }
+    double total = 0.0;
+    for (int i = 0; i < np; ++i) total += fmax(0.0, p[i] - q[i]);
+    if (total <= 0.0) { *err = kErrResidualZero; return -1; }
+    const double u = mt_uniform(g) * total;
+    double acc = 0.0;
+    int last = -1;
+    for (int i = 0; i < np; ++i) {
+        const double r = fmax(0.0, p[i] - q[i]);
+        if (r <= 0.0) continue;
+        last = i;
+        acc += r;
+        if (u < acc) return last;
+    }
+    return last;
+}
+// residual_sample_point_mass (verification.cpp:52-58): p with p[x] removed
+__device__ int residual_point_dev(const double* p, int np, int x, DevRng& g, int* err) {
+    if (x < 0 || x >= np) { *err = kErrArgument; return -1; }
+    double total = 0.0;
+    for (int i = 0; i < np; ++i) total += i == x ? 0.0 : p[i];
+    if (total <= 0.0) { *err = kErrResidualZero; return -1; }
+    const double u = mt_uniform(g) * total;
+    double acc = 0.0;
+    int last = -1;
+    for (int i = 0; i < np; ++i) {
+        const double w = i == x ? 0.0 : p[i];
+        if (w <= 0.0) continue;
+        last = i;
+        acc += w;
+        if (u < acc) return last;
+    }
+    return last;
+}
+// accept_prob (verification.cpp:19-23)
+__device__ double accept_prob_dev(const double* p, int np, const double* q, int nq, int x, int* err) {
+    if (x < 0 || x >= nq || x >= np) { *err = kErrArgument; return 0.0; }
+    const double qx = q[x];
+    if (qx <= 0.0) { *err = kErrDraftMassZero; return 0.0; }
+    return fmin(1.0, p[x] / qx);
+}
+
+__global__ void rng_seed_kernel(DevRng* g, uint64_t seed) { mt_seed(*g, seed); }
+__global__ void rng_uniform_kernel(DevRng* g, double* out, int n) {
+    for (int i = 0; i < n; ++i) out[i] = mt_uniform(*g);
+}
+
+struct VerifyIO {  // results written by the kernels
+    int err;
+    int first_reject;  // -1 = none
+    int accepted_len;
+    int kind;
+    int n_committed;
+    int token;
+    double value;
+};
+
+__global__ void accept_prob_kernel(Rows p, Rows q, int x, VerifyIO* io) {
+    io->err = 0;
+    io->value = accept_prob_dev(p.row(0), p.len(0), q.row(0), q.len(0), x, &io->err);
+}
+__global__ void residual_kernel(Rows p, Rows q, int x, DevRng* g, VerifyIO* io) {
+    io->err = 0;
+    io->token = x >= 0 ? residual_point_dev(p.row(0), p.len(0), x, *g, &io->err)
+                       : residual_sample_dev(p.row(0), p.len(0), q.row(0), q.len(0), *g, &io->err);
+}
+
+// verify_against_target (verification.cpp:60-78)
+__device__ void verify_dev(const int32_t* draft, int n_draft, Rows dp, Rows tp, double temperature, DevRng& g,
+                           VerifyIO* io) {
+    io->first_reject = -1;
+    if (tp.n < n_draft) { io->err = kErrArgument; return; }
+    for (int k = 0; k < n_draft; ++k) {
+        if (temperature == 0.0) {
+            if (draft[k] != argmax_row(tp.row(k), tp.len(k), &io->err) || io->err) {
+                if (!io->err) io->first_reject = k;
+                return;
+            }
+        } else {
+            if (k >= dp.n) { io->err = kErrArgument; return; }
+            const double a = accept_prob_dev(tp.row(k), tp.len(k), dp.row(k), dp.len(k), draft[k], &io->err);
+            if (io->err) return;
+            if (mt_uniform(g) >= a) {
+                io->first_reject = k;
+                return;
+            }
+        }
+    }
+}
+__global__ void verify_kernel(const int32_t* draft, int n_draft, Rows dp, Rows tp, double temperature, DevRng* g,
+                              VerifyIO* io) {
+    io->err = 0;
+    verify_dev(draft, n_draft, dp, tp, temperature, *g, io);
+}
+
+// guided_output (verification.cpp:80-132)
+__global__ void guided_kernel(const int32_t* draft, int n_draft, Rows dp, const int32_t* gtok, int n_gtok, Rows gp,
+                              int first_reject, double temperature, DevRng* g, int32_t* committed, int cap,
+                              VerifyIO* io) {
+    io->err = 0;
+    int n = 0;
+    auto push = [&](int32_t t) {
+        if (n < cap) committed[n] = t;
+        ++n;
+    };
+    if (first_reject < 0) {
+        io->accepted_len = n_draft;
+        for (int i = 0; i < n_draft; ++i) push(draft[i]);
+        io->kind = kAllAccepted;
+        bool covers = temperature == 0.0 && n_gtok > n_draft;
+        for (int i = 0; covers && i < n_draft; ++i) covers = draft[i] == gtok[i];
+        if (covers) {
+            for (int i = n_draft; i < n_gtok; ++i) push(gtok[i]);
+            io->kind = kExtension;
+        }
+        io->n_committed = n;
+        return;
+    }
+    const int i = first_reject;
+    if (i > n_draft) { io->err = kErrArgument; return; }
+    io->accepted_len = i;
+    for (int k = 0; k < i; ++k) push(draft[k]);
+    if (temperature == 0.0) {
+        if (i < n_gtok) {
+            for (int k = i; k < n_gtok; ++k) push(gtok[k]);
+        } else if (i < gp.n) {
+            push(argmax_row(gp.row(i), gp.len(i), &io->err));
+        } else {
+            io->err = kErrUncovered;
+            return;
+        }
+        io->kind = kCorrection;
+        io->n_committed = n;
+        return;
+    }
+    if (i >= gp.n) { io->err = kErrUncovered; return; }
+    if (i >= dp.n) { io->err = kErrArgument; return; }
+    push(residual_sample_dev(gp.row(i), gp.len(i), dp.row(i), dp.len(i), *g, &io->err));
+    io->kind = kResidualCorrection;
+    io->n_committed = n;
+}
+
+// ---------------------------------------------------------------- host side
+struct DevRows {  // device copy of ragged rows
+    DevBuf<double> data;
+    DevBuf<int64_t> off;
+    Rows view{nullptr, nullptr, 0};
+    DevRows(const double* d, const int64_t* offsets, int n) {
+        if (n < 0) throw_invalid("negative row count");
+        if (n > 0 && (!d || !offsets)) throw_invalid("null probability rows");
+        const int64_t total = n > 0 ? offsets[n] : 0;
+        if (n > 0 && offsets[0] != 0) throw_invalid("row offsets must start at 0");
+        for (int r = 0; r < n; ++r)
+            if (offsets[r + 1] < offsets[r]) throw_invalid("row offsets must be non-decreasing");
+        data.alloc(static_cast<size_t>(std::max<int64_t>(total, 1)));
+        off.alloc(static_cast<size_t>(n) + 1);
+        if (total > 0) CUDA_CHECK(cudaMemcpy(data.p, d, total * sizeof(double), cudaMemcpyHostToDevice));
+        std::vector<int64_t> o(offsets ? offsets : nullptr, offsets ? offsets + n + 1 : nullptr);
+        if (o.empty()) o.assign(1, 0);
+        CUDA_CHECK(cudaMemcpy(off.p, o.data(), o.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        view = Rows{data.p, off.p, n};
+    }
+};
+
+void raise(int err) {
+    switch (err) {
+        case 0: return;
+        case kErrDegenerate: throw_runtime("degenerate distribution");                   // model.cpp:79
+        case kErrResidualZero: throw_runtime("residual distribution is zero");           // verification.cpp:47,56
+        case kErrDraftMassZero: throw_invalid("draft mass zero on emitted token");       // verification.cpp:21
+        case kErrUncovered: throw_invalid("guided_output: reject position uncovered");   // verification.cpp:119,126
+        default: throw_invalid("invalid argument");
+    }
+}
+
+VerifyIO run_io(const std::function<void(VerifyIO*)>& launch) {
+    DevBuf<VerifyIO> io(1);
+    io.zero();
+    launch(io.p);
+    CUDA_LAUNCH_CHECK();
+    VerifyIO h{};
+    CUDA_CHECK(cudaMemcpy(&h, io.p, sizeof h, cudaMemcpyDeviceToHost));
+    raise(h.err);
+    return h;
+}
+
+}  // namespace
+
+DeviceRng::DeviceRng(uint64_t seed, int device) : device_(device) {
+    require_device(device);
+    DeviceGuard gd(device);
+    state_.alloc(1);
+    rng_seed_kernel<<<1, 1>>>(state_.p, seed);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaDeviceSynchronize());
+}
+DeviceRng DeviceRng::derive(uint64_t seed, uint64_t round, uint64_t lane, int device) {  // rng.hpp:33-35
+    return DeviceRng(splitmix64(seed ^ splitmix64(round * 4 + lane + 1)), device);
+}
+void DeviceRng::uniform(double* out, int n) {
+    if (n < 0 || (n > 0 && !out)) throw_invalid("bad uniform request");
+    if (n == 0) return;
+    DeviceGuard gd(device_);
+    DevBuf<double> d(n);
+    rng_uniform_kernel<<<1, 1>>>(state_.p, d.p, n);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaMemcpy(out, d.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+double accept_prob(const double* p, int np, const double* q, int nq, int x, int device) {
+    require_device(device);
+    DeviceGuard gd(device);
+    const int64_t op[2] = {0, np}, oq[2] = {0, nq};
+    DevRows P(p, op, 1), Q(q, oq, 1);
+    return run_io([&](VerifyIO* io) { accept_prob_kernel<<<1, 1>>>(P.view, Q.view, x, io); }).value;
+}
+
+int residual_sample(const double* p, int np, const double* q, int nq, DeviceRng& rng) {
+    DeviceGuard gd(rng.device());
+    const int64_t op[2] = {0, np}, oq[2] = {0, nq};
+    DevRows P(p, op, 1), Q(q, oq, 1);
+    return run_io([&](VerifyIO* io) { residual_kernel<<<1, 1>>>(P.view, Q.view, -1, rng.state(), io); }).token;
+}
+
+int residual_sample_point_mass(const double* p, int np, int x, DeviceRng& rng) {
+    DeviceGuard gd(rng.device());
+    const int64_t op[2] = {0, np};
+    DevRows P(p, op, 1), Q(p, op, 1);
+    if (x < 0) throw_invalid("token out of range");
+    return run_io([&](VerifyIO* io) { residual_kernel<<<1, 1>>>(P.view, Q.view, x, rng.state(), io); }).token;
+}
+
+int verify_against_target(const int32_t* draft, int n_draft, const double* dprobs, const int64_t* doff, int n_dp,
+                          const double* tprobs, const int64_t* toff, int n_tp, double temperature, DeviceRng& rng) {
+    DeviceGuard gd(rng.device());
+    if (n_draft < 0 || (n_draft > 0 && !draft)) throw_invalid("bad draft slice");
+    DevBuf<int32_t> d(std::max(n_draft, 1));
+    if (n_draft > 0) CUDA_CHECK(cudaMemcpy(d.p, draft, n_draft * 4, cudaMemcpyHostToDevice));
+    DevRows DP(dprobs, doff, n_dp), TP(tprobs, toff, n_tp);
+    return run_io([&](VerifyIO* io) {
+               verify_kernel<<<1, 1>>>(d.p, n_draft, DP.view, TP.view, temperature, rng.state(), io);
+           }).first_reject;
+}
+
+VerifyOutcome guided_output(const int32_t* draft, int n_draft, const double* dprobs, const int64_t* doff, int n_dp,
+                            const int32_t* gtok, int n_gtok, const double* gprobs, const int64_t* goff, int n_gp,
+                            int first_reject, double temperature, DeviceRng& rng) {
+    DeviceGuard gd(rng.device());
+    if (n_draft < 0 || (n_draft > 0 && !draft) || n_gtok < 0 || (n_gtok > 0 && !gtok))
+        throw_invalid("bad token slice");
+    DevBuf<int32_t> d(std::max(n_draft, 1)), gt(std::max(n_gtok, 1));
+    if (n_draft > 0) CUDA_CHECK(cudaMemcpy(d.p, draft, n_draft * 4, cudaMemcpyHostToDevice));
+    if (n_gtok > 0) CUDA_CHECK(cudaMemcpy(gt.p, gtok, n_gtok * 4, cudaMemcpyHostToDevice));
+    DevRows DP(dprobs, doff, n_dp), GP(gprobs, goff, n_gp);
+    const int cap = n_draft + n_gtok + 1;
+    DevBuf<int32_t> out(cap);
+    const VerifyIO h = run_io([&](VerifyIO* io) {
+        guided_kernel<<<1, 1>>>(d.p, n_draft, DP.view, gt.p, n_gtok, GP.view, first_reject, temperature, rng.state(),
+                                out.p, cap, io);
+    });
+    VerifyOutcome r;
+    r.accepted_len = h.accepted_len;
+    r.kind = h.kind;
+    r.committed.resize(h.n_committed);
+    if (h.n_committed > 0)
+        CUDA_CHECK(cudaMemcpy(r.committed.data(), out.p, h.n_committed * 4, cudaMemcpyDeviceToHost));
+    return r;
+}
+
+}  // namespace dbl

@@ -432,3 +432,123 @@ def run_serial_sd(draft: _Model, target: _Model, store: HierarchicalDatastore, p
                                  C.byref(n), C.byref(m), js, len(js) if js is not None else 0,
                                  C.byref(jl))
     return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+# ------------------------------------------------------------------------------ verifier + RNG
+# specpar::Rng / derive_rng (rng.hpp:19-35) and the verifier interface (verification.hpp:30-53),
+# computed on the device (verify.cu) with the reference's draw order and fp64 summation order.
+class Rng:  # rng.hpp:19-30 — the mt19937_64 stream lives on the device
+    def __init__(self, seed: int = 0, device: int = 0, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            check(lib().dbl_rng_create(C.c_uint64(seed), device, C.byref(h)))
+            _handle = h
+        self._h = _handle
+
+    def uniform(self, n: int | None = None):
+        k = 1 if n is None else n
+        out = np.zeros(max(k, 1), np.float64)
+        check(lib().dbl_rng_uniform(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), k))
+        return float(out[0]) if n is None else out[:k]
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().dbl_rng_destroy(self._h)
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+
+def derive_rng(seed: int, round_: int, lane: int, device: int = 0) -> Rng:  # rng.hpp:33-35
+    h = C.c_void_p()
+    check(lib().dbl_rng_derive(C.c_uint64(seed), C.c_uint64(round_), C.c_uint64(lane), device, C.byref(h)))
+    return Rng(_handle=h)
+
+
+def _rows(rows):
+    """ragged fp64 rows (list of ProbVector) -> (flat, offsets, n)"""
+    rows = [np.asarray(r, np.float64).reshape(-1) for r in (rows or [])]
+    off = np.zeros(len(rows) + 1, np.int64)
+    for i, r in enumerate(rows):
+        off[i + 1] = off[i] + len(r)
+    flat = np.ascontiguousarray(np.concatenate(rows) if rows else np.zeros(1), np.float64)
+    return flat, off, len(rows)
+
+
+def _f64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+VERIFY_KINDS = ["all_accepted", "correction", "extension", "residual_correction"]  # to_string(VerifyKind)
+
+
+@dataclass
+class GuidanceChain:  # verification.hpp:13-17
+    tokens: list = field(default_factory=list)
+    probs: list = field(default_factory=list)
+    matched_len: int = 0
+
+
+@dataclass
+class VerifyOutcome:  # verification.hpp:22-26
+    accepted_len: int
+    committed: list
+    kind: str
+
+
+def accept_prob(p, q, x: int) -> float:  # verification.cpp:19-23
+    p = np.ascontiguousarray(p, np.float64)
+    q = np.ascontiguousarray(q, np.float64)
+    out = C.c_double()
+    check(lib().dbl_accept_prob(_f64(p), len(p), _f64(q), len(q), x, C.byref(out)))
+    return out.value
+
+
+def residual_sample(p, q, rng: Rng) -> int:  # verification.cpp:40-50
+    p = np.ascontiguousarray(p, np.float64)
+    q = np.ascontiguousarray(q, np.float64)
+    out = C.c_int32()
+    check(lib().dbl_residual_sample(_f64(p), len(p), _f64(q), len(q), rng._h, C.byref(out)))
+    return out.value
+
+
+def residual_sample_point_mass(p, x: int, rng: Rng) -> int:  # verification.cpp:52-58
+    p = np.ascontiguousarray(p, np.float64)
+    out = C.c_int32()
+    check(lib().dbl_residual_sample_point_mass(_f64(p), len(p), x, rng._h, C.byref(out)))
+    return out.value
+
+
+def verify_against_target(draft_tokens, draft_probs, target_probs, temperature: float, rng: Rng):
+    """verification.cpp:60-78: the first rejected index, or None (std::nullopt)"""
+    d = _i32(draft_tokens)
+    dp, doff, nd = _rows(draft_probs)
+    tp, toff, nt = _rows(target_probs)
+    out = C.c_int()
+    check(lib().dbl_verify_against_target(_p32(d), len(d), _f64(dp), _i64(doff), nd, _f64(tp), _i64(toff), nt,
+                                          float(temperature), rng._h, C.byref(out)))
+    return None if out.value < 0 else out.value
+
+
+def guided_output(draft_tokens, draft_probs, guidance: GuidanceChain, first_reject, temperature: float,
+                  rng: Rng) -> VerifyOutcome:  # verification.cpp:80-132
+    d = _i32(draft_tokens)
+    dp, doff, nd = _rows(draft_probs)
+    gt = _i32(guidance.tokens)
+    gp, goff, ng = _rows(guidance.probs)
+    cap = len(d) + len(gt) + 1
+    out = np.zeros(cap, np.int32)
+    n, acc, kind = C.c_int(), C.c_int(), C.c_int()
+    check(lib().dbl_guided_output(_p32(d), len(d), _f64(dp), _i64(doff), nd, _p32(gt), len(gt), _f64(gp),
+                                  _i64(goff), ng, -1 if first_reject is None else int(first_reject),
+                                  float(temperature), rng._h, _p32(out), cap, C.byref(n), C.byref(acc),
+                                  C.byref(kind)))
+    return VerifyOutcome(acc.value, out[:n.value].tolist(), VERIFY_KINDS[kind.value])
+
+
+__all__ += ["Rng", "derive_rng", "GuidanceChain", "VerifyOutcome", "accept_prob", "residual_sample",
+            "residual_sample_point_mass", "verify_against_target", "guided_output", "VERIFY_KINDS"]

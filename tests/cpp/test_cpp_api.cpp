@@ -105,6 +105,31 @@ int main() {
         bad.gamma = 0;
         CHECK(throws<std::invalid_argument>([&] { run(draft, target, store, prompt, 8, bad); }));
     }
+    {  // verifier: test_verification.cpp:187-245 through the C++ mirror
+        const SamplerConfig greedy{0.0, 0}, stoch{1.0, 0};
+        Rng rng(1);
+        const TokenSeq draft{3, 4};
+        GuidanceChain longer;
+        longer.tokens = {3, 4, 7, 8};
+        VerifyOutcome o = guided_output(draft, {}, longer, std::nullopt, greedy, rng);
+        CHECK(o.kind == VerifyKind::Extension && (o.committed == TokenSeq{3, 4, 7, 8}));
+        GuidanceChain g;
+        g.tokens = {3};
+        g.probs = {{0.9, 0.1}, {0.1, 0.9}};
+        o = guided_output(draft, {}, g, 1, greedy, rng);
+        CHECK(o.kind == VerifyKind::Correction && (o.committed == TokenSeq{3, 1}));
+        CHECK(throws<std::invalid_argument>([&] { guided_output(draft, {}, GuidanceChain{}, 1, greedy, rng); }));
+        Rng rng8(8);
+        const std::vector<ProbVector> qp = {{0.9, 0.1}, {0.2, 0.5, 0.3}};
+        GuidanceChain s;
+        s.tokens = {0, 2, 4};
+        s.probs = {{0.9, 0.1}, {0.6, 0.1, 0.3}};
+        o = guided_output(TokenSeq{0, 1}, qp, s, 1, stoch, rng8);
+        CHECK(o.kind == VerifyKind::ResidualCorrection && o.accepted_len == 1 && (o.committed == TokenSeq{0, 0}));
+        CHECK(accept_prob({0.5, 0.5}, {0.25, 0.75}, 0) == 1.0);
+        CHECK(throws<std::invalid_argument>([&] { accept_prob({0.5, 0.5}, {0.0, 1.0}, 0); }));
+        CHECK(throws<std::runtime_error>([&] { residual_sample({0.5, 0.5}, {0.5, 0.5}, rng); }));
+    }
     std::printf("test_cpp_api: %d failure(s)\n", g_fail);
     return g_fail;
 }
