@@ -95,8 +95,14 @@ typedef struct {
     uint64_t seed;       /* weights are a pure function of (seed, tensor, index) */
     int tp_rank, tp_size;/* tensor parallel shard (1 = unsharded) */
 } dbl_transformer_config;
-/* nccl_comm: an ncclComm_t for tp_size > 1 (else NULL) */
+/* One shard (cfg->tp_rank of cfg->tp_size) or the whole model (tp_size 1) on `device`.  nccl_comm is
+ * unused (kept for ABI stability): the tensor-parallel exchange runs inside the forward kernel over
+ * peer memory (fwd.cuh), driven by dbl_tp_transformer_create. */
 int dbl_transformer_create(const dbl_transformer_config* cfg, int device, void* nccl_comm, dbl_model_t* out);
+/* Tensor-parallel target: `world` shards (2..8) of cfg on devices[0..world) — distinct
+ * GPUs over NVLink, or repeated devices (shards co-reside) — behind one model handle: forward_batch,
+ * run, run_vanilla_ar etc. work unchanged; every shard ends each forward with identical argmax rows. */
+int dbl_tp_transformer_create(const dbl_transformer_config* cfg, const int* devices, int world, dbl_model_t* out);
 int dbl_model_destroy(dbl_model_t m);
 int dbl_model_vocab(dbl_model_t m, int* vocab);
 /* bytes of weights streamed per forward on this rank (the roofline numerator's static part) */

@@ -71,6 +71,7 @@ PROTOTYPES = {
     "dbl_store_stats": [VP, I64P],
     "dbl_table_create": [C.c_int, C.c_int, C.c_int64, I32P, F64P, F64P, C.c_int, C.POINTER(VP)],
     "dbl_transformer_create": [C.POINTER(TransformerConfig), C.c_int, VP, C.POINTER(VP)],
+    "dbl_tp_transformer_create": [C.POINTER(TransformerConfig), I32P, C.c_int, C.POINTER(VP)],
     "dbl_model_destroy": [VP],
     "dbl_model_vocab": [VP, C.POINTER(C.c_int)],
     "dbl_model_weight_bytes": [VP, I64P],

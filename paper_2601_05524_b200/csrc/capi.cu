@@ -8,6 +8,7 @@
 #include "store.cuh"
 #include "table_model.cuh"
 #include "transformer.cuh"
+#include "tp.cuh"
 #include "fwd.cuh"
 #include "verify.cuh"
 #include "gemm.cuh"
@@ -214,6 +215,17 @@ int dbl_transformer_create(const dbl_transformer_config* cfg, int device, void* 
         need(out, "out");
         auto m = std::make_unique<dbl_model_s>();
         m->impl = std::make_unique<dbl::Transformer>(*cfg, device, nccl_comm);
+        *out = m.release();
+    });
+}
+int dbl_tp_transformer_create(const dbl_transformer_config* cfg, const int* devices, int world, dbl_model_t* out) {
+    return guarded([&] {
+        need(cfg, "config");
+        need(devices, "devices");
+        need(out, "out");
+        if (world < 2 || world > dbl::kMaxTpRanks) dbl::throw_invalid("tensor parallel: 2..8 shards");
+        auto m = std::make_unique<dbl_model_s>();
+        m->impl = std::make_unique<dbl::TpTransformer>(*cfg, std::vector<int>(devices, devices + world));
         *out = m.release();
     });
 }

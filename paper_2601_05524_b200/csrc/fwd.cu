@@ -296,8 +296,25 @@ struct FwdSmem {
     int sidx[128];
     float qv[512];
     float pv[256];
+    TpPeers peers;  // copy of FwdArgs::peers (dynamic indexing of kernel parameters would use local memory)
+    float pre[16 * 128];  // a finisher's presummed split-K partials, parked across the accumulator wait
 };
 static_assert(sizeof(FwdSmem) <= kFwdMiscBytes, "misc shared state exceeds its budget");
+
+// one attention phase of this warp
+template <int HD>
+__device__ __forceinline__ void attn_phase(const FwdArgs& a, const FwdPhase& P, int start, int T, int gw, int GW,
+                                        float* q_s, float* p_s, int lane) {
+    const int nh = a.nh;
+    const int nch_max = (start + T - 1) / kAttnChunk + 1;
+    const int items = T * nh * nch_max;
+    for (int item = gw; item < items; item += GW) {
+        const int j = item % nch_max, rest = item / nch_max;
+        const int hq = rest % nh, t = rest / nh;
+        if (j * kAttnChunk > start + t) continue;
+        attn_item<HD>(a, P, t, hq, j, start, q_s, p_s, lane);
+    }
+}
 
 // ------------------------------------------------------------------ GEMM tile finisher
 // The last contributor of an output tile sums the split-K partials (fixed contributor order) and
@@ -314,7 +331,9 @@ struct TileCtx {
     float *rs, *red, *sval;
     int* sidx;
     unsigned long long tag;  // slot-flag value of this (forward, phase)
-    const float* pre;        // presummed partials of the other contributors (decode), or nullptr
+    bool has_pre;            // pre holds the presummed partials of the other contributors (decode)
+    float* pre;              // shared memory [16][128] (column-major: thread r reads pre[i*128 + r])
+    const TpPeers* peers;    // tensor-parallel exchange buffers (shared-memory copy)
 };
 
 template <int CH>
@@ -412,22 +431,70 @@ __device__ __forceinline__ void presum(const TileCtx& x, int ch, float (&pre)[16
     }
 }
 
-template <int CH>
+template <int CH, bool kTP>
 __device__ __forceinline__ void finish_tile(const TileCtx& x) {
     const FwdArgs& a = *x.a;
     const FwdPhase& P = *x.P;
     const int tp = x.tp, T = x.T, lane = x.lane, q = x.q, et = x.et, r = x.r, m = x.m;
     const int n = m * kBM + r;
     const int h = a.h;
+    const bool tp_resid = kTP && P.epi == kFeResid;
+    const int nth = h / kBM;
+    if constexpr (kTP) if (tp_resid) {  // this rank's partial of tile m -> every rank's exchange slot [my rank][m]
+        for (int ch = 0; ch < tp; ch += CH) {
+            float v[CH];
+            tmem_ld<CH>(x.taddr + ch, v);
+            const int nc = min(CH, tp - ch);
+            if (x.n_contrib > 1) {
+                float pre[16];
+                if (x.has_pre) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pre[i] = x.pre[i * kBM + r];
+                } else {
+                    presum(x, ch, pre);
+                }
+#pragma unroll
+                for (int i = 0; i < CH; ++i) v[i] += pre[i];
+            }
+            for (int rr = 0; rr < a.tp_world; ++rr) {
+                float* dst = x.peers->xch[rr] + (static_cast<long long>(a.tp_rank * nth + m) * 256 + ch) * kBM + r;
+#pragma unroll
+                for (int i = 0; i < CH; ++i)
+                    if (i < nc) dst[i * kBM] = v[i];
+            }
+        }
+        __threadfence_system();
+        named_bar_sync(1, 128);
+        if (et == 0) {
+            for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(x.peers->xflag[rr] + a.tp_rank * nth + m, x.tag);
+            for (int src = 0; src < a.tp_world; ++src) {  // every rank's partial of this tile has arrived
+                const unsigned long long* f = x.peers->xflag[a.tp_rank] + src * nth + m;
+                Spin sp;
+                while (ld_acquire_sys_u64(f) != x.tag) sp.tick(a.err, 9, x.p);
+            }
+        }
+        named_bar_sync(1, 128);
+    }
     for (int ch = 0; ch < tp; ch += CH) {
         float v[CH];
-        tmem_ld<CH>(x.taddr + ch, v);
         const int nc = min(CH, tp - ch);
-        if (x.n_contrib > 1) {  // own + (p_1 + p_2 + ...): fixed contributor order (per shape)
-            float pre[16];
-            if (x.pre) {
+        if (kTP && tp_resid) {  // sum of the ranks' partials, rank order (identical on every rank)
+            const float* src0 = x.peers->xch[a.tp_rank] + (static_cast<long long>(m) * 256 + ch) * kBM + r;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) pre[i] = x.pre[i];
+            for (int i = 0; i < CH; ++i) v[i] = i < nc ? __ldcg(src0 + i * kBM) : 0.f;
+            for (int src = 1; src < a.tp_world; ++src) {
+                const float* s1 = src0 + static_cast<long long>(src) * nth * 256 * kBM;
+#pragma unroll
+                for (int i = 0; i < CH; ++i) v[i] += i < nc ? __ldcg(s1 + i * kBM) : 0.f;
+            }
+        } else {
+            tmem_ld<CH>(x.taddr + ch, v);
+        }
+        if (x.n_contrib > 1 && !tp_resid) {  // own + (p_1 + p_2 + ...): fixed contributor order (per shape)
+            float pre[16];
+            if (x.has_pre) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) pre[i] = x.pre[i * kBM + r];
             } else {
                 presum(x, ch, pre);
             }
@@ -543,7 +610,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
             int id[CH];
 #pragma unroll
             for (int i = 0; i < CH; ++i) {
-                id[i] = ok ? n : 0x7fffffff;
+                id[i] = ok ? n + a.vocab_off : 0x7fffffff;
                 if (!ok) v[i] = -INFINITY;
             }
             warp_colmax<CH>(v, id, lane);
@@ -564,6 +631,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
 }
 
 // ------------------------------------------------------------------ the kernel
+template <bool kTP>  // tensor-parallel exchange compiled in only where used (register pressure)
 __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_constant__ FwdArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ FwdSmem sm;  // static: the compiler keeps these in the shared address space (LDS/STS)
@@ -606,6 +674,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             mbar_init(&tempty[b], 128);
         }
         fence_barrier_init();
+        if constexpr (kTP) sm.peers = a.peers;
     }
     if (warp == 1) tmem_alloc(tslot, ncols);
     tc_fence_before();
@@ -808,13 +877,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     const int buf = it % a.nacc;
                     const uint32_t taddr = tmem + static_cast<uint32_t>(buf * a.acc_cols) + (static_cast<uint32_t>(q * 32) << 16);
                     const bool finisher = my == 0;
-                    const TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
-                                     q, lane, et, r, rs, red, sval, sidx, tag, nullptr};
-                    float pre[16];
+                    TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
+                               q, lane, et, r, rs, red, sval, sidx, tag, false, sm.pre, &sm.peers};
                     const bool early = finisher && n_contrib > 1 && tp == 16;
                     if (early) {  // the other contributors are (nearly always) done: sum them now
                         wait_partials(tc);
+                        float pre[16];
                         presum(tc, 0, pre);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) sm.pre[i * kBM + r] = pre[i];  // own thread's row only
+                        tc.has_pre = true;
                     }
                     mbar_wait_wd(&tfull[buf], static_cast<uint32_t>((it / a.nacc) & 1), a.err, 6, p);
                     tc_fence_after();
@@ -833,9 +905,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     } else {
                         if (et == 0) stamp(a, p, 8);
                         if (n_contrib > 1 && !early) wait_partials(tc);
-                        TileCtx tf = tc;
-                        tf.pre = early ? pre : nullptr;
-                        finish_tile<16>(tf);  // 16-column chunks: no spills
+                        finish_tile<16, kTP>(tc);  // 16-column chunks
                     }
                     if (et == 0 && finisher) stamp(a, p, 10);
                     tc_fence_before();
@@ -849,18 +919,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             } else if (P.kind == kPhAttn) {  // ------------------------- split-KV causal attention
                 acquire(P.dep);
                 stamp(a, p, 3);
-                const int nh = a.nh;
-                const int nch_max = (start + T - 1) / kAttnChunk + 1;
-                const int items = T * nh * nch_max;
-                float* q_s = qv + ew * 128;
-                float* p_s = pv + ew * 64;
-                for (int item = gw; item < items; item += GW) {
-                    const int j = item % nch_max, rest = item / nch_max;
-                    const int hq = rest % nh, t = rest / nh;
-                    if (j * kAttnChunk > start + t) continue;
-                    if (a.hd == 128) attn_item<128>(a, P, t, hq, j, start, q_s, p_s, lane);
-                    else attn_item<64>(a, P, t, hq, j, start, q_s, p_s, lane);
-                }
+                if (a.hd == 128) attn_phase<128>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane);
+                else attn_phase<64>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane);
                 if (lane == 0) stamp(a, p, 8 + ew);  // each aux warp's last item done
                 signal(p);
             } else {  // kPhArgmax ----------------------------------------- final argmax + cursor
@@ -880,11 +940,38 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
                         if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
                     }
-                    if (lane == 0) a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                    if (lane == 0) {
+                        if constexpr (!kTP) {
+                            a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                        } else {  // this rank's shard winner -> every rank's exchange slot [my rank][t]
+                            for (int rr = 0; rr < a.tp_world; ++rr)
+                                sm.peers.axch[rr][a.tp_rank * 256 + t] = make_float2(bv, __int_as_float(bi));
+                        }
+                    }
                 }
+                if constexpr (kTP) __threadfence_system();
                 signal(p);
                 if (c == 0 && et == 0) {  // the forward is complete once every CTA has signalled
                     wait_dep(a, p, ep, 7);
+                    if constexpr (kTP) {  // vocab-parallel argmax: (max, lowest global id) over ranks
+                        const unsigned long long tag = (ep << 12) | static_cast<unsigned long long>(p + 1);
+                        __threadfence_system();
+                        for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(sm.peers.aflag[rr] + a.tp_rank, tag);
+                        for (int src = 0; src < a.tp_world; ++src) {
+                            Spin sp;
+                            while (ld_acquire_sys_u64(sm.peers.aflag[a.tp_rank] + src) != tag) sp.tick(a.err, 10, p);
+                        }
+                        for (int t = 0; t < T; ++t) {
+                            float bv = -INFINITY;
+                            int bi = 0x7fffffff;
+                            for (int src = 0; src < a.tp_world; ++src) {
+                                const float2 w = __ldcg(sm.peers.axch[a.tp_rank] + src * 256 + t);
+                                const int wi = __float_as_int(w.y);
+                                if (w.x > bv || (w.x == bv && wi < bi)) { bv = w.x; bi = wi; }
+                            }
+                            a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                        }
+                    }
                     a.lane->start = start;
                     a.lane->kv_len = sint[2];
                     __threadfence();
@@ -906,7 +993,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
 void fwd_prepare() {
     static std::once_flag once;
     std::call_once(once, [] {
-        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kFwdMiscBytes));
+        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024 - kFwdMiscBytes));
+        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024 - kFwdMiscBytes));
     });
 }
 
@@ -967,9 +1057,23 @@ void fwd_trace_read(unsigned long long* dst, long long cap, int* n_ph, int* grid
 }
 
 void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s) {
+    // Cooperative launch: the forward's CTAs wait on each other (phase counters), so they must be
+    // co-resident — gang scheduling guarantees it even when a draft forward or another shard's
+    // forward shares the GPU (a partially resident persistent grid could otherwise spin forever).
     fwd_prepare();
-    fwd_kernel<<<grid, kFwdThreads, smem, s>>>(a);
-    CUDA_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kFwdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (a.tp_world > 1) CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<true>, a));
+    else CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<false>, a));
+    ++launch_counter();
 }
 
 }  // namespace dbl

@@ -20,6 +20,12 @@
 // QKV epilogue (each 128-row tile holds whole heads; rows are permuted at init so RoPE partners
 // d, d + hd/2 sit in lanes l, l ^ 16 of one warp).
 //
+// Tensor parallel (tp_world > 1): QKV / gate|up are column-parallel and O / down row-parallel, so the
+// O and down tiles are partial sums.  The tile's finisher pushes its partial into every rank's
+// exchange slot (peer stores) and releases a per-(source, tile) flag at system scope; every rank then
+// sums the ranks' partials in rank order — identical residual streams on all ranks, no NCCL call.
+// The LM head is vocab-parallel; ranks exchange per-token (max, lowest global id) the same way.
+//
 // Batch invariance (the lossless identity with target-only AR) holds as in gemm.cu: every split /
 // reduction order is a function of the model shape and the SM count, never of the token count.
 #pragma once
@@ -49,6 +55,16 @@ struct FwdPhase {
     __nv_bfloat16* vc;
     const __nv_bfloat16* qn;  // q/k RMSNorm weights (nullable)
     const __nv_bfloat16* kn;
+};
+
+// Tensor parallel: every rank's exchange buffers, addressed directly (same device, peer device over
+// NVLink, or an IPC mapping).  Written remotely, read locally.
+constexpr int kMaxTpRanks = 8;
+struct TpPeers {
+    float* xch[kMaxTpRanks];                 // [src rank][h/128 tiles][256 cols][128 rows] fp32 partial tiles
+    unsigned long long* xflag[kMaxTpRanks];  // [src rank][h/128 tiles] tags
+    float2* axch[kMaxTpRanks];               // [src rank][256] (max logit, global id) per token
+    unsigned long long* aflag[kMaxTpRanks];  // [src rank] tags
 };
 
 struct FwdArgs {
@@ -84,11 +100,13 @@ struct FwdArgs {
     unsigned long long* done;   // [n_ph] monotone completion counters
     unsigned long long* epoch;  // forwards completed on this cache
     int* err;                   // watchdog code (0 = fine)
-    unsigned long long* trace;  // optional [n_ph][G][8] %globaltimer stamps
+    unsigned long long* trace;  // optional [n_ph][G][16] %globaltimer stamps
+    int tp_world, tp_rank, vocab_off;  // tensor parallel (world 1: none); vocab_off = rank * vocab_l
+    TpPeers peers;
 };
 
 constexpr int kFwdThreads = 192;  // warp 0 TMA producer, warp 1 MMA, warps 2..5 epilogue / aux work
-constexpr int kFwdMiscBytes = 8 * 1024;     // static shared state (barriers, reductions, attention)
+constexpr int kFwdMiscBytes = 16 * 1024;     // static shared state (barriers, reductions, attention)
 constexpr int kFwdMaxStages = 24;
 constexpr int kFwdSmemBudget = 113 * 1024;  // two CTAs per SM: a draft and a target forward co-reside
 constexpr int kFwdMinUnits = 4;             // smallest stream-K range worth a CTA (4 x 16 KiB)

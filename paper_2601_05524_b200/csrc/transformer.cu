@@ -20,7 +20,6 @@
 #include "fwd.cuh"
 #include "gemm.cuh"
 #include "tf_kernels.cuh"
-#include "tp.cuh"
 #include "transformer.cuh"
 
 namespace dbl {
@@ -48,7 +47,6 @@ struct Transformer::Impl {
     // forward streams through five tensor maps (kernel parameters, not global-memory descriptors)
     DevBuf<__nv_bfloat16> w_qkv, w_o, w_gu, w_down;
     CUtensorMap t_qkv, t_o, t_gu, t_down, t_lm;
-    std::unique_ptr<TpComm> comm;
     GemmProfiler* prof = nullptr;
 };
 
@@ -65,7 +63,13 @@ struct TfCache final : LaneCache {
     DevBuf<FwdPhase> phases;
     CUtensorMap xmaps[3][5];  // xb, attn, act x boxes of 1, 2, 4, 8, 16 token rows
     DevBuf<unsigned long long> done, epoch, slot_flag;
+    // tensor parallel: this rank's exchange buffers (written by every rank) and all ranks' addresses
+    DevBuf<float> xch;
+    DevBuf<unsigned long long> xflag, aflag;
+    DevBuf<float2> axch;
+    TpPeers peers{};
     int n_ph = 0;
+    int grid = 0;  // CTAs per forward (the phase table's split is built for this grid)
     GemmWorkspace ws;
     size_t layer_stride = 0;
 };
@@ -100,10 +104,8 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
     m.ffn_l = c.ffn / world;
     m.vocab_l = c.vocab / world;
     if (m.q_dim % 64) throw_invalid("transformer: per-rank q dim must be a multiple of 64");
-    if (world > 1) {
-        if (!nccl_comm) throw_invalid("transformer: tp_size > 1 needs an NCCL communicator");
-        m.comm = std::make_unique<TpComm>(nccl_comm, m.rank, world, device);
-    }
+    (void)nccl_comm;  // the tensor-parallel exchange runs inside fwd_kernel over peer memory (tp.cu)
+    if (world > kMaxTpRanks) throw_invalid("transformer: tp_size > 8");
     cudaStream_t s = 0;
     const uint64_t seed = c.seed;
     const float sd = c.init_std;
@@ -168,12 +170,13 @@ Transformer::~Transformer() {
     delete impl_;
 }
 
-int64_t Transformer::weight_bytes() const {
-    const Impl& m = *impl_;
+int64_t Transformer::weight_bytes() const { return weight_bytes_of(*impl_); }
+
+int64_t Transformer::weight_bytes_of(const Impl& m) {
     const int64_t per_layer = (static_cast<int64_t>(m.qkv_rows) * m.h + static_cast<int64_t>(m.h) * m.q_dim +
                                2LL * m.ffn_l * m.h + static_cast<int64_t>(m.h) * m.ffn_l) * 2 +
-                              2LL * m.h * 2 + (cfg_.qk_norm ? 4LL * m.hd : 0);
-    return per_layer * cfg_.n_layers + static_cast<int64_t>(m.vocab_l) * m.h * 2 + m.h * 2;
+                              2LL * m.h * 2 + (m.c.qk_norm ? 4LL * m.hd : 0);
+    return per_layer * m.c.n_layers + static_cast<int64_t>(m.vocab_l) * m.h * 2 + m.h * 2;
 }
 
 int64_t Transformer::kv_bytes_per_token() const {
@@ -185,7 +188,6 @@ int Transformer::max_forward_tokens() const { return kMaxTp; }
 
 std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     const Impl& m = *impl_;
-    if (m.world > 1) throw_runtime("tensor-parallel stream forward not available yet");
     DeviceGuard g(device_);
     auto cp = std::make_unique<TfCache>();
     TfCache& c = *cp;
@@ -229,7 +231,10 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     }
     const int max_tiles = std::max({(m.qkv_rows + 127) / 128, (2 * m.ffn_l + 127) / 128, (m.vocab_l + 127) / 128,
                                     (m.h + 127) / 128});
-    const int sms = num_sms(device_);
+    // CTAs of this model's forward: one per SM, or 1/k of the SMs when k tensor-parallel shards share
+    // the GPU (every shard's grid must be resident at once)
+    const int sms = std::max(1, num_sms(device_) / std::max(1, shards_per_device_));
+    c.grid = sms;
     c.ws.ensure(sms, kMaxTp, max_tiles);
     // ---- the forward's phase list (fwd.cuh); tensor maps: W 0..4 = qkv, o, gate|up, down, lm head;
     // X 0..2 = xb, attn, act
@@ -312,16 +317,27 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     if (ph.size() >= 4095) throw_invalid("stream forward: too many phases for the slot-flag tag");
     c.slot_flag.alloc(2 * static_cast<size_t>(sms) + 2);
     c.slot_flag.zero();
+    if (m.world > 1) {
+        const size_t nth = static_cast<size_t>(m.h / 128);
+        c.xch.alloc(kMaxTpRanks * nth * kMaxTp * 128);
+        c.xflag.alloc(kMaxTpRanks * nth);
+        c.xflag.zero();
+        c.axch.alloc(static_cast<size_t>(kMaxTpRanks) * kMaxTp);
+        c.aflag.alloc(kMaxTpRanks);
+        c.aflag.zero();
+    }
     CUDA_CHECK(cudaDeviceSynchronize());
     return cp;
 }
 
 namespace {
-void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits, int ld_logits, cudaStream_t s) {
+void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32_t* buf, int32_t* argmax,
+                 LaneCache* cache, int max_tokens, float* logits, int ld_logits, cudaStream_t s) {
     if (max_tokens < 1) max_tokens = 1;
     if (max_tokens > kMaxTp) throw_runtime("forward exceeds 256 token columns (decoder must chunk)");
     const int tp = (max_tokens + 15) / 16 * 16;
-    TfCache& c = *static_cast<TfCache*>(lane.cache.get());
+    TfCache& c = *static_cast<TfCache*>(cache);
+    if (m.world > 1 && !c.peers.xch[m.world - 1]) throw_logic("tensor-parallel lane cache not linked to its peers");
     FwdArgs a{};
     a.ph = c.phases.p;
     a.n_ph = c.n_ph;
@@ -341,9 +357,9 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     a.stages = fwd_stages(tp, &smem);
     a.acc_cols = tp <= 32 ? 32 : tp <= 64 ? 64 : tp <= 128 ? 128 : 256;
     a.nacc = tp <= 128 ? 2 : 1;
-    a.lane = lane.state;
-    a.buf = lane.buf.p;
-    a.argmax = lane.argmax.p;
+    a.lane = state;
+    a.buf = buf;
+    a.argmax = argmax;
     a.embed = m.embed.p;
     a.h = m.h;
     a.nh = m.nh;
@@ -375,21 +391,50 @@ void run_forward(Transformer::Impl& m, Lane& lane, int max_tokens, float* logits
     a.done = c.done.p;
     a.epoch = c.epoch.p;
     a.err = c.err.p;
-    a.trace = fwd_trace_buffer(c.n_ph, num_sms(lane.model.device()));
+    a.trace = fwd_trace_buffer(c.n_ph, c.grid);
+    a.tp_world = m.world;
+    a.tp_rank = m.rank;
+    a.vocab_off = m.rank * m.vocab_l;
+    a.peers = c.peers;
+    // vocab-parallel logits: this rank's columns of the caller's [rows][vocab] buffer
+    if (logits) a.logits = logits + static_cast<size_t>(m.rank) * m.vocab_l;
     if (m.prof) m.prof->next(s);
-    fwd_launch(a, num_sms(lane.model.device()), smem, s);
+    fwd_launch(a, c.grid, smem, s);
     if (m.prof) {
         m.prof->next(s);
-        m.prof->bytes.push_back(static_cast<double>(lane.model.weight_bytes()));
+        m.prof->bytes.push_back(static_cast<double>(Transformer::weight_bytes_of(m)));
     }
 }
 }  // namespace
 
-void Transformer::forward(Lane& lane, int max_tokens, cudaStream_t s) { run_forward(*impl_, lane, max_tokens, nullptr, 0, s); }
+void Transformer::forward(Lane& lane, int max_tokens, cudaStream_t s) {
+    run_forward(*impl_, device_, lane.state, lane.buf.p, lane.argmax.p, lane.cache.get(), max_tokens, nullptr, 0, s);
+}
 
 void Transformer::logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) {
     // logits rows are written for every processed position; the caller's row0 == start here
-    run_forward(*impl_, lane, max_tokens, out_dev, cfg_.vocab, s);
+    run_forward(*impl_, device_, lane.state, lane.buf.p, lane.argmax.p, lane.cache.get(), max_tokens, out_dev,
+                cfg_.vocab, s);
+}
+
+void Transformer::forward_raw(LaneState* state, const int32_t* buf, int32_t* argmax, LaneCache* cache,
+                              int max_tokens, float* logits_dev, cudaStream_t s) {
+    DeviceGuard g(device_);
+    run_forward(*impl_, device_, state, buf, argmax, cache, max_tokens, logits_dev, logits_dev ? cfg_.vocab : 0, s);
+}
+
+void Transformer::link_tp(const std::vector<LaneCache*>& caches) {
+    if (caches.size() > static_cast<size_t>(kMaxTpRanks) || caches.empty()) throw_invalid("link_tp: 1..8 caches");
+    TpPeers p{};
+    for (size_t r = 0; r < caches.size(); ++r) {
+        TfCache& c = *static_cast<TfCache*>(caches[r]);
+        if (!c.xch.p) throw_logic("link_tp: cache of a tp_size == 1 model");
+        p.xch[r] = c.xch.p;
+        p.xflag[r] = c.xflag.p;
+        p.axch[r] = c.axch.p;
+        p.aflag[r] = c.aflag.p;
+    }
+    for (LaneCache* lc : caches) static_cast<TfCache*>(lc)->peers = p;
 }
 
 void Transformer::get_weight(const std::string& name, int layer, uint16_t* out, int64_t numel) {

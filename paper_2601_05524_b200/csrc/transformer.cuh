@@ -21,13 +21,24 @@ class Transformer final : public Model {
     std::string kind() const override { return "transformer"; }
     void set_profiler(GemmProfiler* p) override;
     void get_weight(const std::string& name, int layer, uint16_t* out, int64_t numel);
+    int tp_rank() const { return cfg_.tp_rank; }
+    int tp_size() const { return cfg_.tp_size < 1 ? 1 : cfg_.tp_size; }
+    // one forward over explicit lane pieces (a tensor-parallel shard's mirror of the decoder's lane)
+    void forward_raw(LaneState* state, const int32_t* buf, int32_t* argmax, LaneCache* cache, int max_tokens,
+                     float* logits_dev, cudaStream_t s);
+    // tensor parallel: make every rank's lane cache address all ranks' exchange buffers (rank order)
+    static void link_tp(const std::vector<LaneCache*>& caches);
+    // tensor-parallel shards sharing one GPU: each forward takes 1/k of the SMs (set before make_cache)
+    void set_shards_per_device(int k) { shards_per_device_ = k; }
 
     struct Impl;
+    static int64_t weight_bytes_of(const Impl& m);
 
   private:
     Impl* impl_ = nullptr;
     dbl_transformer_config cfg_;
     int device_;
+    int shards_per_device_ = 1;
 };
 
 }  // namespace dbl

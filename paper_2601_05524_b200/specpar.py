@@ -31,7 +31,7 @@ from ._capi import (DoubleError, InvalidArgument, LogicError, PipelineOptions as
 SOURCES = ["prior", "dynamic", "rejected", "context", "miss"]
 PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
-__all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer",
+__all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "run", "run_vanilla_ar",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
            "parse_model_v1", "parse_dstore_v1"]
@@ -313,6 +313,20 @@ class Transformer(_Model):
         check(lib().dbl_transformer_get_weight(self._h, name.encode(), int(layer),
                                                out.ctypes.data_as(C.POINTER(C.c_uint16)), numel))
         return (out.astype(np.uint32) << 16).view(np.float32).reshape(shape)
+
+
+class TpTransformer(_Model):
+    """Tensor-parallel target: len(devices) shards of `cfg` (column-parallel QKV /
+    gate|up, row-parallel O / down, vocab-parallel LM head) exchanging partial sums inside the forward
+    kernel.  Devices may repeat (shards co-reside on one GPU) or be distinct GPUs over NVLink."""
+
+    def __init__(self, cfg: TransformerConfig, devices=(0, 0)):
+        h = C.c_void_p()
+        dv = _i32(devices)
+        check(lib().dbl_tp_transformer_create(C.byref(cfg), _p32(dv), len(dv), C.byref(h)))
+        self._h = h
+        self.cfg = cfg
+        self.devices = list(devices)
 
 
 def forward_batch(model: _Model, context, candidates) -> list:
