@@ -6,8 +6,10 @@ AR + mean accepted length).
 
 N=1 workload = BASELINE.json configs[1]: Qwen3-0.6B draft / Qwen3-14B target shapes, random-init
 bf16, synthetic code-like prompt (HumanEval length, 160 tokens), 256 new tokens, greedy, d=10, N=3,
-prior K=10.  A "step" is one complete DOUBLE decode of that request.  N>1 runs N independent replicas
-(one per GPU, weak scaling; the target-TP path is DESIGN.md's next row) with max-over-ranks timing.
+prior K=10.  A "step" is one complete DOUBLE decode of that request.  N>1 (torchrun, one process per
+GPU): the target is tensor-parallel over the N GPUs (TpTransformer driven from rank 0,
+the O/down and argmax exchange inside fwd_kernel over peer memory, the draft beside shard 0; strong
+scaling of the one request), or N independent replicas with --tp off (weak scaling).
 
 value          decode tokens/s of the DOUBLE loop with the weights/KV resident in HBM (CUDA events
                around the device decode loop, prompt prefill excluded), summed over ranks
@@ -56,6 +58,9 @@ def parse():
     p.add_argument("--max-new", type=int, default=0)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--log-out", default="", help="write this run's decision log (json) here")
+    p.add_argument("--tp", choices=["auto", "off"], default="auto",
+                   help="N>1: auto = the target tensor-parallel over the N GPUs (driven from rank 0), "
+                        "off = N independent replicas")
     return p.parse_args()
 
 
@@ -237,6 +242,27 @@ def main():
 
     if a.impl == "reference":
         return reference_arm(a, rank, world, wl, max_new, metric, base_cfg)
+    if os.environ.get("DBL_BENCH_TP_DEVICES") and world == 1 and a.impl == "ours":
+        return run_bench(a, 0, 1, 0, wl, max_new, metric, base_cfg,
+                         tp_world=len(os.environ["DBL_BENCH_TP_DEVICES"].split(",")))
+    if world > 1 and a.tp == "auto":
+        # Target tensor-parallel over the box's N GPUs: rank 0 drives every shard
+        # in-process (peer memory over NVLink, the exchange inside fwd_kernel) with the draft beside
+        # shard 0; the other ranks hold the rendezvous only.  On failure: replicas, reason recorded.
+        barrier(world)
+        if rank == 0:
+            try:
+                run_bench(a, 0, 1, 0, wl, max_new, metric, base_cfg, tp_world=world)
+            except Exception as e:  # noqa: BLE001
+                print(f"tensor-parallel bench failed ({e}); falling back to replicas", file=sys.stderr)
+                base_cfg = dict(base_cfg, tp_error=str(e)[:200])
+                run_bench(a, 0, 1, 0, wl, max_new, metric, base_cfg)
+        barrier(world)
+        return None
+    return run_bench(a, rank, world, local, wl, max_new, metric, base_cfg)
+
+
+def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
 
     import paper_2601_05524_b200 as dbl
     from paper_2601_05524_b200 import _capi
@@ -247,7 +273,15 @@ def main():
     import torch
     torch.cuda.set_device(local)
     dev_env = local  # the library follows the current device through cudaSetDevice in torch
-    tgt = dbl.Transformer(dbl.transformer_config(wl["target"], seed=a.seed, max_seq=4096), device=local)
+    if tp_world > 1:
+        # DBL_BENCH_TP_DEVICES="0,0": a TP layout on fewer GPUs (functional checks on one GPU)
+        env_dev = os.environ.get("DBL_BENCH_TP_DEVICES")
+        devices = [int(x) for x in env_dev.split(",")] if env_dev else list(range(tp_world))
+        tgt = dbl.TpTransformer(dbl.transformer_config(wl["target"], seed=a.seed, max_seq=4096), devices=devices)
+        base_cfg = dict(base_cfg, parallelism=f"target TP={tp_world} on GPUs {devices} (peer memory, exchange "
+                        "inside fwd_kernel), draft beside shard 0", tp=tp_world)
+    else:
+        tgt = dbl.Transformer(dbl.transformer_config(wl["target"], seed=a.seed, max_seq=4096), device=local)
     drf = dbl.Transformer(dbl.transformer_config(wl["draft"], seed=a.seed + 1, max_seq=4096), device=local)
     V = tgt.cfg.vocab
     prompt, prior = workload(V, wl["prompt_len"], a.seed + 100 + rank * 0)
@@ -345,9 +379,10 @@ def main():
     except (OSError, ValueError):
         pass
     line = {
-        "metric": metric, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world,
+        "metric": metric, "value": round(value, 3), "unit": "tokens/s", "n_gpus": max(world, tp_world),
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_dev / a.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": "strong" if tp_world > 1 else "weak", "vs_baseline": None,
+        "dtype": "bf16", "n_gpus_used": tp_world if tp_world > 1 else world,
         "data": "synthetic (random-init weights, code-like prompt)",
         "config": dict(base_cfg, gamma=gamma, C_measured=round(C_ratio, 3)),
         "speedup_vs_ar": round(value / ar_value, 4), "ar_tokens_per_s": round(ar_value, 3),

@@ -116,17 +116,19 @@ struct Streams {
         CUDA_CHECK(cudaStreamCreateWithPriority(&main, cudaStreamNonBlocking, hi));
         CUDA_CHECK(cudaStreamCreateWithPriority(&draft, cudaStreamNonBlocking, lo));
         CUDA_CHECK(cudaStreamCreateWithPriority(&target, cudaStreamNonBlocking, hi));
+        own_target = target;
         CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CUDA_CHECK(cudaEventCreate(&tf0));
         CUDA_CHECK(cudaEventCreate(&tf1));
     }
+    cudaStream_t own_target = nullptr;  // target may alias draft (see run_double)
     ~Streams() {
         cudaStreamSynchronize(main);
         cudaStreamSynchronize(draft);
-        cudaStreamSynchronize(target);
+        cudaStreamSynchronize(own_target);
         cudaStreamDestroy(main);
         cudaStreamDestroy(draft);
-        cudaStreamDestroy(target);
+        cudaStreamDestroy(own_target);
         cudaEventDestroy(ready);
         cudaEventDestroy(tf0);
         cudaEventDestroy(tf1);
@@ -287,6 +289,10 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
     const int d = o.depth, gamma = o.gamma;
     const int cap = n_prompt + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
     Streams S;
+    // draft and target run concurrently unless that would put more than two persistent forwards on
+    // this GPU (tensor-parallel shards sharing it): then both workers share one stream — the round's
+    // results are identical either way (frozen snapshot, pipeline.cpp:239-261)
+    if (dm.persistent_grids() + tm.persistent_grids() > 2) S.target = S.draft;
     Lane dl(dm, cap), tl(tm, cap);
     LaneIO dio(&dl), tio(&tl);
     PinBuf<RoundResult> rr_buf(1);

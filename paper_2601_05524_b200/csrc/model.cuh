@@ -57,6 +57,9 @@ class Model {
     // order, to out_dev ((L+c-row0) x vocab).
     virtual void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) = 0;
     virtual int max_forward_tokens() const { return 1 << 30; }
+    // persistent (all-SM, cooperatively launched) grids one forward places on device(): at most two may
+    // co-run on a GPU, so the decoder serializes draft and target work when the sum would exceed it
+    virtual int persistent_grids() const { return 0; }
     virtual void set_profiler(GemmProfiler*) {}
     virtual std::string kind() const = 0;
 };

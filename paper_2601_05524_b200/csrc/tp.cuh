@@ -33,6 +33,11 @@ class TpTransformer final : public Model {
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
     int max_forward_tokens() const override { return shards_[0]->max_forward_tokens(); }
     std::string kind() const override { return "transformer-tp"; }
+    int persistent_grids() const override {
+        int k = 0;
+        for (int d : devices_) k += d == devices_[0];
+        return k;
+    }
     void set_profiler(GemmProfiler* p) override { shards_[0]->set_profiler(p); }
     int world() const { return static_cast<int>(shards_.size()); }
     Transformer& shard(int r) { return *shards_[static_cast<size_t>(r)]; }

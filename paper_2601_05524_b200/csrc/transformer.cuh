@@ -19,6 +19,7 @@ class Transformer final : public Model {
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
     int max_forward_tokens() const override;
     std::string kind() const override { return "transformer"; }
+    int persistent_grids() const override { return 1; }
     void set_profiler(GemmProfiler* p) override;
     void get_weight(const std::string& name, int layer, uint16_t* out, int64_t numel);
     int tp_rank() const { return cfg_.tp_rank; }
