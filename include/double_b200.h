@@ -113,6 +113,9 @@ int dbl_model_weight_bytes(dbl_model_t m, int64_t* bytes);
 int dbl_forward_argmax(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, int32_t* out_argmax);
 /* same rows as fp32 logits (transformer) or fp64 probabilities cast to fp32 (table), (c+1) x vocab */
 int dbl_forward_logits(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, float* out);
+/* the ProbVector rows themselves, fp64 (c+1) x vocab: tables return their rows exactly, transformers
+ * softmax(logits) — the same rows the sampled (temperature > 0) decode loop consumes */
+int dbl_forward_dists(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, double* out);
 /* copies a named weight tensor to host (bf16 bits as uint16); for the fp32 torch reference in tests */
 int dbl_transformer_get_weight(dbl_model_t m, const char* name, int layer, uint16_t* out, int64_t numel);
 
@@ -125,6 +128,8 @@ typedef struct {
     int concurrent;          /* Engine::Concurrent; the device loop always overlaps draft and target */
     double t_target, t_draft, t_lookup, t_sync; /* LatencyConfig, pipeline.hpp:15-29 */
     int use_graphs;          /* capture the draft chain / target forward in CUDA graphs */
+    double temperature;      /* SamplerConfig (model.hpp:11-14): 0 = greedy, > 0 = sampled */
+    uint64_t rng_seed;       /* SamplerConfig::rng_seed: per-round streams derive_rng(seed, round, 0/1/2) */
 } dbl_pipeline_options;
 
 typedef struct { /* RunMetrics (pipeline.hpp:73-82) + device timing */
@@ -153,6 +158,11 @@ int dbl_last_run_log(int32_t* buf, int64_t cap, int64_t* len);
 int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
                int64_t jsonl_cap, int64_t* jsonl_len);
+/* run_vanilla_ar with a SamplerConfig (harness.cpp:233-258): temperature 0 = dbl_run_ar; > 0 samples
+ * each token with Rng(splitmix64(seed ^ 0x6172000000000000)) exactly as the reference */
+int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
+                       double temperature, uint64_t seed, int32_t* out, int cap, int* n_out,
+                       dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len);
 /* run_serial_sd (harness.cpp:264-369): draft-then-verify, use_retrieval = draft_retrieval method */
 int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
                       int n_prompt, int max_new, const dbl_pipeline_options* opts, int use_retrieval,

@@ -155,10 +155,16 @@ inline TokenSeq forward_batch_argmax(const Model& m, std::span<const TokenId> ct
     return out;
 }
 
+struct SamplerConfig {  // model.hpp:11-14
+    double temperature = 0.0;
+    std::uint64_t rng_seed = 0;
+};
+
 struct PipelineOptions {  // pipeline.hpp:36-44 (+ LatencyConfig :15-29)
     int gamma = 4, depth = 10;
     bool draft_retrieval = true, target_retrieval = true;
     double t_target = 1.0, t_draft = 0.25, t_lookup = 0.0, t_sync = 0.0;
+    SamplerConfig sampler{};
 };
 
 struct RunResult {  // pipeline.hpp:84-88 (traces as the traces_to_jsonl text)
@@ -171,7 +177,8 @@ struct RunResult {  // pipeline.hpp:84-88 (traces as the traces_to_jsonl text)
 inline RunResult run(const Model& draft, const Model& target, HierarchicalDatastore& store, const TokenSeq& prompt,
                      int max_new_tokens, const PipelineOptions& o) {
     dbl_pipeline_options c{o.gamma, o.depth, o.draft_retrieval, o.target_retrieval, 1,
-                           o.t_target, o.t_draft, o.t_lookup, o.t_sync, 1};
+                           o.t_target, o.t_draft, o.t_lookup, o.t_sync, 1, o.sampler.temperature,
+                           o.sampler.rng_seed};
     RunResult r;
     r.output.resize(static_cast<size_t>(max_new_tokens > 0 ? max_new_tokens : 1));
     int n = 0;
@@ -184,13 +191,15 @@ inline RunResult run(const Model& draft, const Model& target, HierarchicalDatast
 }
 
 // run_vanilla_ar (harness.cpp:233-258)
-inline RunResult run_vanilla_ar(const Model& target, const TokenSeq& prompt, int max_new_tokens, double t_target = 1.0) {
+inline RunResult run_vanilla_ar(const Model& target, const TokenSeq& prompt, int max_new_tokens, double t_target = 1.0,
+                                const SamplerConfig& sampler = {}) {
     RunResult r;
     r.output.resize(static_cast<size_t>(max_new_tokens > 0 ? max_new_tokens : 1));
     int n = 0;
     int64_t jl = 0;
-    check(dbl_run_ar(target.handle(), prompt.data(), static_cast<int>(prompt.size()), max_new_tokens, t_target,
-                     r.output.data(), static_cast<int>(r.output.size()), &n, &r.metrics, nullptr, 0, &jl));
+    check(dbl_run_ar_sampled(target.handle(), prompt.data(), static_cast<int>(prompt.size()), max_new_tokens,
+                             t_target, sampler.temperature, sampler.rng_seed, r.output.data(),
+                             static_cast<int>(r.output.size()), &n, &r.metrics, nullptr, 0, &jl));
     r.output.resize(static_cast<size_t>(n));
     return r;
 }
@@ -225,10 +234,6 @@ inline Rng derive_rng(std::uint64_t seed, std::uint64_t round, std::uint64_t lan
     return Rng::derived(seed, round, lane);
 }
 
-struct SamplerConfig {  // model.hpp:11-14
-    double temperature = 0.0;
-    std::uint64_t rng_seed = 0;
-};
 struct GuidanceChain {  // verification.hpp:13-17
     TokenSeq tokens;
     std::vector<ProbVector> probs;

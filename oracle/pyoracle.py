@@ -21,6 +21,8 @@ SOURCES = ["prior", "dynamic", "rejected", "context", "miss"]
 ARGMAX_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
                         C.c_int, C.POINTER(C.c_int))
 IntP = C.POINTER(C.c_int)
+PROBS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
+                       C.c_int, C.POINTER(C.c_double))
 
 
 def _ints(xs):
@@ -254,6 +256,25 @@ class Store:
         return list(s)
 
 
+def make_probs_callback(fn, vocab):
+    """Wrap ``fn(ctx, cands) -> float64 array (|cands|+1, vocab)`` as the reference's proxy forward."""
+    import numpy as np
+
+    def cb(_user, ctx, L, cands, c, out):
+        try:
+            rows = np.ascontiguousarray(fn([ctx[i] for i in range(L)], [cands[i] for i in range(c)]),
+                                        dtype=np.float64)
+            assert rows.shape == (c + 1, vocab), rows.shape
+            C.memmove(out, rows.ctypes.data, rows.nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 — reported through the C status
+            import traceback
+            traceback.print_exc()
+            return -1
+
+    return PROBS_FN(cb)
+
+
 class Reference:
     """The unmodified reference (oracle/_ref).  Raises FileNotFoundError when not built."""
 
@@ -277,6 +298,12 @@ class Reference:
                                        C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                        C.c_double, C.c_double, C.c_double, IntP, C.c_int, IntP,
                                        C.c_char_p, C.c_long, C.POINTER(C.c_double)]
+        L.ref_run_callback_probs.argtypes = [C.c_int, PROBS_FN, C.c_void_p, PROBS_FN, C.c_void_p,
+                                             C.c_int, C.c_int, IntP, IntP, IntP, C.c_int, C.c_int,
+                                             C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                             C.c_double, C.c_double, C.c_double, C.c_double,
+                                             C.c_ulonglong, C.c_char_p, IntP, C.c_int, IntP,
+                                             C.c_char_p, C.c_long, C.POINTER(C.c_double)]
 
     def _err(self):
         raise OracleError(self.lib.ref_last_error().decode())
@@ -350,6 +377,29 @@ class Reference:
                                      t_draft, t_lookup, t_sync, out, cap, C.byref(n), js, jcap, m):
             self._err()
         return list(out[:n.value]), js.value.decode(), list(m)
+
+
+def _run_callback_probs(self, vocab, draft_cb, target_cb, prior, prompt, max_new, temperature, seed,
+                        method="double", max_order=3, gamma=4, depth=10, draft_retrieval=True,
+                        target_retrieval=True, rejected_enabled=True, t_target=1.0, t_draft=0.25,
+                        t_lookup=0.0, t_sync=0.0, cap=1 << 16, jcap=1 << 24):
+    """The reference loop at temperature > 0 over callback distributions (ref_run_callback_probs)."""
+    out = (C.c_int * cap)()
+    n = C.c_int()
+    js = C.create_string_buffer(jcap)
+    m = (C.c_double * 8)()
+    flat = [t for s in prior for t in s]
+    if self.lib.ref_run_callback_probs(vocab, draft_cb, None, target_cb, None, max_order, len(prior),
+                                       _ints(len(s) for s in prior), _ints(flat), _ints(prompt),
+                                       len(prompt), max_new, gamma, depth, int(draft_retrieval),
+                                       int(target_retrieval), int(rejected_enabled), t_target, t_draft,
+                                       t_lookup, t_sync, float(temperature), int(seed), method.encode(),
+                                       out, cap, C.byref(n), js, jcap, m):
+        self._err()
+    return list(out[:n.value]), js.value.decode(), list(m)
+
+
+Reference.run_callback_probs = _run_callback_probs
 
 
 def reference_or_none():

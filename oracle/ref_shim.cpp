@@ -27,6 +27,8 @@ using namespace specpar;
 
 extern "C" {
 typedef int (*ref_argmax_fn)(void* user, const int* ctx, int L, const int* cands, int c, int* out);
+// full rows: out[(c+1) * vocab] fp64 next-token distributions
+typedef int (*ref_probs_fn)(void* user, const int* ctx, int L, const int* cands, int c, double* out);
 }
 
 namespace {
@@ -34,6 +36,7 @@ namespace {
 struct Proxy {
     ref_argmax_fn fn;
     void* user;
+    ref_probs_fn pfn = nullptr;  // when set, rows are the callback's distributions (sampled runs)
 };
 std::mutex g_mu;
 std::map<const TableModel*, Proxy> g_proxies;
@@ -48,6 +51,18 @@ bool find_proxy(const TableModel* m, Proxy* out) {
 
 std::vector<ProbVector> proxy_rows(const TableModel& model, const Proxy& p,
                                    std::span<const TokenId> ctx, std::span<const TokenId> cands) {
+    if (p.pfn) {
+        const size_t V = static_cast<size_t>(model.vocab_size);
+        std::vector<double> flat((cands.size() + 1) * V);
+        if (p.pfn(p.user, ctx.data(), static_cast<int>(ctx.size()), cands.data(),
+                  static_cast<int>(cands.size()), flat.data()) != 0) {
+            throw std::runtime_error("proxy forward callback failed");
+        }
+        std::vector<ProbVector> rows;
+        for (size_t r = 0; r <= cands.size(); ++r)
+            rows.emplace_back(flat.begin() + static_cast<long>(r * V), flat.begin() + static_cast<long>((r + 1) * V));
+        return rows;
+    }
     std::vector<int> ids(cands.size() + 1);
     if (p.fn(p.user, ctx.data(), static_cast<int>(ctx.size()), cands.data(),
              static_cast<int>(cands.size()), ids.data()) != 0) {
@@ -356,4 +371,77 @@ int ref_guided_output(const int* draft, int n_draft, const double* dp, const lon
         for (int i = 0; i < *n_committed && i < cap; ++i) committed[i] = o.committed[static_cast<size_t>(i)];
     });
 }
+// The same loop at temperature > 0: proxy models return full fp64 rows from the callbacks and the
+// reference's own accept_with_model / finish_round / derive_rng run unmodified (SamplerConfig
+// {temperature, seed}).  method "double" = run() with the given retrieval flags; "vanilla_ar", "sd",
+// "draft_retrieval" = the harness entry points (harness.cpp:233-369) through run_method_on, with the
+// prior rebuilt by build_store from the same sequences.
+int ref_run_callback_probs(int vocab, ref_probs_fn draft_fn, void* draft_user, ref_probs_fn target_fn,
+                           void* target_user, int max_order, int n_prior, const int* prior_lens,
+                           const int* prior_tokens, const int* prompt, int n_prompt, int max_new, int gamma,
+                           int depth, int draft_retrieval, int target_retrieval, int rejected_enabled,
+                           double t_target, double t_draft, double t_lookup, double t_sync, double temperature,
+                           unsigned long long seed, const char* method, int* out_tokens, int cap, int* n_out,
+                           char* jsonl, long jsonl_cap, double* metrics) {
+    ExperimentSetup setup;
+    setup.draft_model.vocab_size = setup.target_model.vocab_size = vocab;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_proxies[&setup.draft_model] = {nullptr, draft_user, draft_fn};
+        g_proxies[&setup.target_model] = {nullptr, target_user, target_fn};
+    }
+    int rc = 0;
+    try {
+        setup.prompt.assign(prompt, prompt + n_prompt);
+        int at = 0;
+        for (int i = 0; i < n_prior; ++i) {
+            setup.corpus.emplace_back(prior_tokens + at, prior_tokens + at + prior_lens[i]);
+            at += prior_lens[i];
+        }
+        RunResult res;
+        if (std::string(method) == "double") {
+            HierarchicalDatastore store(max_order, depth);
+            store.prior.max_order = max_order;
+            for (int i = 0; i < n_prior; ++i) store.prior.insert(setup.corpus[static_cast<size_t>(i)], i);
+            store.rejected_enabled = rejected_enabled != 0;
+            PipelineOptions opts;
+            opts.gamma = gamma;
+            opts.depth = depth;
+            opts.draft_retrieval = draft_retrieval != 0;
+            opts.target_retrieval = target_retrieval != 0;
+            opts.latency = {t_target, t_draft, t_lookup, t_sync};
+            opts.sampler = SamplerConfig{temperature, seed};
+            res = run(setup.draft_model, setup.target_model, store, setup.prompt, max_new, opts);
+        } else {
+            ExperimentConfig cfg;
+            cfg.vocab = vocab;
+            cfg.gamma = gamma;
+            cfg.depth = depth;
+            cfg.ngram = max_order;
+            cfg.prior_rounds = n_prior;
+            cfg.rejected_cache = rejected_enabled != 0;
+            cfg.latency = {t_target, t_draft, t_lookup, t_sync};
+            cfg.temperature = temperature;
+            cfg.seed = seed;
+            cfg.max_new_tokens = max_new;
+            run_method_on(cfg, setup, parse_method(method), &res);
+        }
+        if (static_cast<int>(res.output.size()) > cap) {
+            rc = -2;
+        } else {
+            std::memcpy(out_tokens, res.output.data(), res.output.size() * sizeof(int));
+            *n_out = static_cast<int>(res.output.size());
+            fill_metrics(res.metrics, metrics);
+            rc = copy_str(traces_to_jsonl(res.traces), jsonl, jsonl_cap);
+        }
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        rc = -1;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_proxies.erase(&setup.draft_model);
+    g_proxies.erase(&setup.target_model);
+    return rc;
+}
+
 }  // extern "C"

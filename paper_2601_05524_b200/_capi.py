@@ -33,7 +33,7 @@ class PipelineOptions(C.Structure):
     _fields_ = [("gamma", C.c_int), ("depth", C.c_int), ("draft_retrieval", C.c_int),
                 ("target_retrieval", C.c_int), ("concurrent", C.c_int), ("t_target", C.c_double),
                 ("t_draft", C.c_double), ("t_lookup", C.c_double), ("t_sync", C.c_double),
-                ("use_graphs", C.c_int)]
+                ("use_graphs", C.c_int), ("temperature", C.c_double), ("rng_seed", C.c_uint64)]
 
 
 class RunMetrics(C.Structure):
@@ -77,11 +77,14 @@ PROTOTYPES = {
     "dbl_model_weight_bytes": [VP, I64P],
     "dbl_forward_argmax": [VP, I32P, C.c_int, I32P, C.c_int, I32P],
     "dbl_forward_logits": [VP, I32P, C.c_int, I32P, C.c_int, F32P],
+    "dbl_forward_dists": [VP, I32P, C.c_int, I32P, C.c_int, F64P],
     "dbl_transformer_get_weight": [VP, C.c_char_p, C.c_int, U16P, C.c_int64],
     "dbl_run": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), I32P, C.c_int,
                 C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
     "dbl_run_ar": [VP, I32P, C.c_int, C.c_int, C.c_double, I32P, C.c_int, C.POINTER(C.c_int),
                    C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
+    "dbl_run_ar_sampled": [VP, I32P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, I32P, C.c_int,
+                           C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
     "dbl_run_serial_sd": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), C.c_int,
                           I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p,
                           C.c_int64, I64P],

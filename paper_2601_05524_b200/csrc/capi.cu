@@ -253,6 +253,14 @@ int dbl_forward_logits(dbl_model_t m, const int32_t* ctx, int L, const int32_t* 
         dbl::forward_stateless(*m->impl, ctx, L, cands, c, am.data(), out);
     });
 }
+int dbl_forward_dists(dbl_model_t m, const int32_t* ctx, int L, const int32_t* cands, int c, double* out) {
+    return guarded([&] {
+        need(m, "model");
+        need(out, "out");
+        std::vector<int32_t> am(c + 1);
+        dbl::forward_stateless(*m->impl, ctx, L, cands, c, am.data(), nullptr, out);
+    });
+}
 int dbl_transformer_get_weight(dbl_model_t m, const char* name, int layer, uint16_t* out, int64_t numel) {
     return guarded([&] {
         need(m, "model");
@@ -294,7 +302,18 @@ int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_
     return guarded([&] {
         need(target, "target");
         if (n_prompt > 0) need(prompt, "prompt");
-        const dbl::RunOutput r = dbl::run_ar(*target->impl, prompt, n_prompt, max_new, t_target);
+        const dbl::RunOutput r = dbl::run_ar(*target->impl, prompt, n_prompt, max_new, t_target, 0.0, 0);
+        copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
+    });
+}
+int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
+                       double temperature, uint64_t seed, int32_t* out, int cap, int* n_out,
+                       dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len) {
+    return guarded([&] {
+        need(target, "target");
+        if (n_prompt > 0) need(prompt, "prompt");
+        const dbl::RunOutput r =
+            dbl::run_ar(*target->impl, prompt, n_prompt, max_new, t_target, temperature, seed);
         copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
     });
 }

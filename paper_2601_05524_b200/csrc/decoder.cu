@@ -16,6 +16,8 @@
 
 #include "accept.cuh"
 #include "decoder.cuh"
+#include "rng.cuh"
+#include "sampling.cuh"
 
 namespace dbl {
 
@@ -152,6 +154,35 @@ void validate_opts(const dbl_pipeline_options& o) {  // pipeline.cpp:267-272, pi
     if (o.gamma > kMaxSegs) throw_invalid("gamma exceeds the device chain record");
     if (o.t_target < 0.0 || o.t_draft <= 0.0 || o.t_lookup < 0.0 || o.t_sync < 0.0)
         throw_invalid("latency values out of range");
+    if (!(o.temperature >= 0.0)) throw_invalid("temperature must be >= 0");  // harness.cpp:50
+}
+
+// Device buffers of the sampled (temperature > 0) loop: the per-round RNG lanes, the draft's and
+// target's fp64 distribution rows, and the draft chain's eff rows (double-buffered: the rows kept as
+// the next round's spec_probs, pipeline.cpp:166-169, stay readable while the next chain is drafted).
+struct Sampled {
+    double T;
+    uint64_t seed;
+    size_t V;
+    int chain_rows;
+    DevBuf<DevRng> rng;  // rng_d, rng_t, rng_v (run_round, pipeline.cpp:227-231)
+    DevBuf<double> ddist, tdist, chain[2], dscratch, tscratch;
+    int cur = 0;
+    const double* spec_probs = nullptr;
+    Sampled(double temp, uint64_t sd, int vocab, int draft_rows, int chain_rows_, int target_rows)
+        : T(temp), seed(sd), V(static_cast<size_t>(vocab)), chain_rows(chain_rows_) {
+        rng.alloc(3);
+        ddist.alloc(V * std::max(draft_rows, 1));
+        tdist.alloc(V * std::max(target_rows, 1));
+        for (auto& c : chain) c.alloc(V * std::max(chain_rows, 1));
+        dscratch.alloc(V);
+        tscratch.alloc(3 * V);
+    }
+};
+
+void check_round_errors(const RoundResult* rr) {
+    if (rr->draft_error) raise_sample_error(rr->draft_error);
+    if (rr->target_error) raise_sample_error(rr->target_error);
 }
 
 // record_accepted_run / record_rejected_run (pipeline.cpp:72-89)
@@ -298,6 +329,12 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
     PinBuf<RoundResult> rr_buf(1);
     RoundResult* rr = rr_buf.p;
     RoundResult* rr_dev = rr_buf.dev();
+    std::unique_ptr<Sampled> smp;
+    if (o.temperature != 0.0) {
+        if (dm.vocab() != tm.vocab()) throw_invalid("draft and target vocabularies differ");
+        smp = std::make_unique<Sampled>(o.temperature, o.rng_seed, tm.vocab(), d + 1, gamma * (d + 1),
+                                        gamma * (d + 1) + d + 2);
+    }
 
     long base_lookups, base_hits;
     device_counts(st, S.main, &base_lookups, &base_hits);
@@ -343,22 +380,38 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
         rr->draft_L = L;
         rr->n_segs = 0;
         rr->draft_error = rr->target_error = 0;
+        if (smp) launch_derive_rngs(smp->rng.p, smp->seed, static_cast<uint64_t>(round), S.main);
         S.fork();
         // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
         for (int j = 0; j < gamma; ++j) {
             if (o.draft_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.draft);
             const int c_max = o.draft_retrieval ? d : 0;
             const int bound = j == 0 ? L + c_max - std::min(dl.kv_len, L - 1) : 1 + c_max;
-            dm.forward(dl, bound, S.draft);
-            launch_draft_accept(dl, rr_dev, j, S.draft);
+            if (smp) {
+                dm.dists(dl, bound, c_max + 1, smp->ddist.p, S.draft);
+                launch_draft_accept_sampled(dl, rr_dev, j, L, smp->ddist.p, smp->chain[smp->cur].p, smp->chain_rows,
+                                            smp->rng.p, smp->T, smp->dscratch.p, S.draft);
+            } else {
+                dm.forward(dl, bound, S.draft);
+                launch_draft_accept(dl, rr_dev, j, S.draft);
+            }
         }
         // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
         if (o.target_retrieval) st.lookup_lane(tl.buf.p, tl.state, d, S.target);
         CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
         const int tc_max = o.target_retrieval ? d : 0;
-        tm.forward(tl, L + tc_max - std::min(tl.kv_len, nc - 1), S.target);
-        CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
-        launch_target_accept(tl, nc, rr_dev, S.target);
+        const int tbound = L + tc_max - std::min(tl.kv_len, nc - 1);
+        if (smp) {
+            // verify forward + finish_round's verification (rng_v) + the target's own acceptance (rng_t)
+            tm.dists(tl, tbound, ns + tc_max + 1, smp->tdist.p, S.target);
+            CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
+            launch_target_accept_sampled(tl, nc, rr_dev, smp->tdist.p, smp->spec_probs, smp->rng.p + 1,
+                                         smp->rng.p + 2, smp->T, false, smp->tscratch.p, S.target);
+        } else {
+            tm.forward(tl, tbound, S.target);
+            CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
+            launch_target_accept(tl, nc, rr_dev, S.target);
+        }
         CUDA_CHECK(cudaStreamSynchronize(S.draft));
         CUDA_CHECK(cudaStreamSynchronize(S.target));
         {
@@ -367,8 +420,7 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
             tfwd_ms += ms;
             ++tfwd_n;
         }
-        if (rr->draft_error == 2) throw_runtime("draft chain exceeds the round record");
-        if (rr->draft_error || rr->target_error) throw_runtime("degenerate distribution");
+        check_round_errors(rr);
         const int c_t = rr->ext_c;
         trows += L + c_t - (nc - 1);
 
@@ -389,6 +441,7 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
 
         const std::vector<int32_t> committed_before = committed;
         std::vector<int32_t> add, new_spec;
+        if (smp) smp->spec_probs = nullptr;
         if (rr->tgt_rej >= 0) {
             const int k = rr->tgt_rej;
             tr.accepted_pending = k;
@@ -412,6 +465,10 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
             if (j == ne && n_chain > ne) {
                 tr.kind = "extend_keep_draft";
                 new_spec.assign(chain + ne, chain + n_chain);
+                if (smp) {  // new_spec_probs = chain.probs[ne:] (pipeline.cpp:168-169)
+                    smp->spec_probs = smp->chain[smp->cur].p + static_cast<size_t>(ne) * smp->V;
+                    smp->cur ^= 1;
+                }
             } else if (j == cmp) {
                 tr.kind = "extend_draft_subsumed";
             } else {
@@ -525,12 +582,14 @@ __global__ void ar_append_kernel(const int32_t* __restrict__ argmax, int32_t* bu
 }
 }  // namespace
 
-RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, double t_target) {
-    // run_vanilla_ar, harness.cpp:233-258 (greedy).  The device runs ahead in blocks of kBlock
-    // tokens between EOS checks; tokens past an EOS are discarded exactly as the reference never
-    // produces them.
+RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, double t_target,
+                 double temperature, uint64_t seed) {
+    // run_vanilla_ar, harness.cpp:233-258.  The device runs ahead in blocks of kBlock tokens between
+    // EOS checks; tokens past an EOS are discarded exactly as the reference never produces them (at
+    // temperature > 0 the extra draws come after every kept token's, so kept tokens are unaffected).
     if (n_prompt <= 0) throw_invalid("prompt must be nonempty");
     if (max_new < 0) throw_invalid("max_new_tokens must be >= 0");
+    if (!(temperature >= 0.0)) throw_invalid("temperature must be >= 0");
     DeviceGuard g(tm.device());
     constexpr int kBlock = 16;
     const int cap = n_prompt + max_new + kBlock + 8;
@@ -546,6 +605,11 @@ RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, do
     catch_up(tl, n_prompt - 1, S.main);
     CUDA_CHECK(cudaEventRecord(pre.b, S.main));
     tl.set_state(n_prompt, 0, tl.kv_len, n_prompt - 1, S.main);
+    std::unique_ptr<Sampled> smp;
+    if (temperature != 0.0) {
+        smp = std::make_unique<Sampled>(temperature, seed, tm.vocab(), 0, 0, 1);
+        launch_seed_rng(smp->rng.p, splitmix64(seed ^ 0x6172000000000000ULL), S.main);  // harness.cpp:235
+    }
     CUDA_CHECK(cudaEventRecord(loop.a, S.main));
     const long long launches0 = launch_counter();
     RunOutput res;
@@ -555,14 +619,20 @@ RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, do
     while (!done) {
         const int n = std::min(kBlock, max_new - produced);
         for (int i = 0; i < n; ++i) {
-            tm.forward(tl, 1, S.main);
-            ar_append_kernel<<<1, 1, 0, S.main>>>(tl.argmax.p, tl.buf.p, tl.state, out_dev, produced + i);
-            CUDA_LAUNCH_CHECK();
+            if (smp) {
+                tm.dists(tl, 1, 1, smp->tdist.p, S.main);
+                launch_ar_sample(tl, smp->tdist.p, smp->rng.p, smp->T, smp->tscratch.p, out_dev, produced + i,
+                                 S.main);
+            } else {
+                tm.forward(tl, 1, S.main);
+                ar_append_kernel<<<1, 1, 0, S.main>>>(tl.argmax.p, tl.buf.p, tl.state, out_dev, produced + i);
+                CUDA_LAUNCH_CHECK();
+            }
         }
         CUDA_CHECK(cudaStreamSynchronize(S.main));
         for (int i = 0; i < n; ++i) {
             const int32_t tok = outp.p[produced + i];
-            if (tok < 0) throw_runtime("degenerate distribution");
+            if (tok < 0) raise_sample_error(smp ? -tok - 1 : kSampDegenerate);
             res.output.push_back(tok);
             Trace t;
             t.round = produced + i;
@@ -605,6 +675,12 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
     PinBuf<RoundResult> rr_buf(1);
     RoundResult* rr = rr_buf.p;
     RoundResult* rr_dev = rr_buf.dev();
+    std::unique_ptr<Sampled> smp;
+    if (o.temperature != 0.0) {
+        if (dm.vocab() != tm.vocab()) throw_invalid("draft and target vocabularies differ");
+        smp = std::make_unique<Sampled>(o.temperature, o.rng_seed, tm.vocab(), d + 1, gamma * (d + 1),
+                                        gamma * (d + 1) + 1);
+    }
     long base_lookups, base_hits;
     device_counts(st, S.main, &base_lookups, &base_hits);
     st.record(1, prompt, n_prompt, S.main);
@@ -627,14 +703,23 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
         rr->draft_L0 = rr->draft_L = nc;
         rr->n_segs = 0;
         rr->draft_error = rr->target_error = 0;
+        // rng_d / rng_v = derive_rng(seed, round, 0 / 2) (harness.cpp:281-282)
+        if (smp) launch_derive_rngs(smp->rng.p, smp->seed, static_cast<uint64_t>(round), S.main);
         for (int j = 0; j < gamma; ++j) {
             if (use_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.main);
             const int c_max = use_retrieval ? d : 0;
-            dm.forward(dl, j == 0 ? nc + c_max - std::min(dl.kv_len, nc - 1) : 1 + c_max, S.main);
-            launch_draft_accept(dl, rr_dev, j, S.main);
+            const int bound = j == 0 ? nc + c_max - std::min(dl.kv_len, nc - 1) : 1 + c_max;
+            if (smp) {
+                dm.dists(dl, bound, c_max + 1, smp->ddist.p, S.main);
+                launch_draft_accept_sampled(dl, rr_dev, j, nc, smp->ddist.p, smp->chain[0].p, smp->chain_rows,
+                                            smp->rng.p, smp->T, smp->dscratch.p, S.main);
+            } else {
+                dm.forward(dl, bound, S.main);
+                launch_draft_accept(dl, rr_dev, j, S.main);
+            }
         }
         CUDA_CHECK(cudaStreamSynchronize(S.main));
-        if (rr->draft_error) throw_runtime(rr->draft_error == 2 ? "draft chain too long" : "degenerate distribution");
+        if (rr->draft_error) raise_sample_error(rr->draft_error);
         const int n_chain = rr->draft_L - rr->draft_L0;
         std::vector<int32_t> chain(rr->draft_tokens, rr->draft_tokens + n_chain);
         // target lane: chain as the "speculative" tail, no candidates
@@ -643,10 +728,17 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
         const int lcp = tio.sync_tokens(X, S.main);
         tl.kv_len = std::min(tl.kv_len, lcp);
         tl.set_state(nc + n_chain, 0, tl.kv_len, nc - 1, S.main);
-        tm.forward(tl, nc + n_chain - std::min(tl.kv_len, nc - 1), S.main);
-        launch_target_accept(tl, nc, rr_dev, S.main);
+        const int tbound = nc + n_chain - std::min(tl.kv_len, nc - 1);
+        if (smp) {
+            tm.dists(tl, tbound, n_chain + 1, smp->tdist.p, S.main);
+            launch_target_accept_sampled(tl, nc, rr_dev, smp->tdist.p, smp->chain[0].p, smp->rng.p + 1,
+                                         smp->rng.p + 2, smp->T, true, smp->tscratch.p, S.main);
+        } else {
+            tm.forward(tl, tbound, S.main);
+            launch_target_accept(tl, nc, rr_dev, S.main);
+        }
         CUDA_CHECK(cudaStreamSynchronize(S.main));
-        if (rr->target_error) throw_runtime("degenerate distribution");
+        if (rr->target_error) raise_sample_error(rr->target_error);
         tl.kv_len = nc + n_chain;
         dl.mirror.resize(nc);
         dl.mirror.insert(dl.mirror.end(), chain.begin(), chain.end());
@@ -719,7 +811,7 @@ __global__ void gather_rows_kernel(const int32_t* argmax, int from, int n, int32
 }  // namespace
 
 void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,
-                       int32_t* out_argmax, float* out_logits) {
+                       int32_t* out_argmax, float* out_logits, double* out_dists) {
     if (L <= 0) throw_invalid("forward_batch: empty context");  // model.cpp:41
     if (c < 0) throw_invalid("negative candidate count");
     DeviceGuard g(m.device());
@@ -732,7 +824,11 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     catch_up(lane, L - 1, S.main);
     lane.set_state(L, c, lane.kv_len, L - 1, S.main);
     DevBuf<float> lg;
-    if (out_logits) {
+    DevBuf<double> dd;
+    if (out_dists) {  // the rows the sampled loop consumes (Model::dists)
+        dd.alloc(static_cast<size_t>(c + 1) * m.vocab());
+        m.dists(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), c + 1, dd.p, S.main);
+    } else if (out_logits) {
         lg.alloc(static_cast<size_t>(c + 1) * m.vocab());
         m.logits(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), lg.p, S.main);
     } else {
@@ -742,7 +838,9 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     gather_rows_kernel<<<1, 256, 0, S.main>>>(lane.argmax.p, L - 1, c + 1, rows.p);
     CUDA_LAUNCH_CHECK();
     CUDA_CHECK(cudaMemcpyAsync(out_argmax, rows.p, (c + 1) * 4, cudaMemcpyDeviceToHost, S.main));
-    if (out_logits)
+    if (out_dists)
+        CUDA_CHECK(cudaMemcpyAsync(out_dists, dd.p, dd.bytes(), cudaMemcpyDeviceToHost, S.main));
+    else if (out_logits)
         CUDA_CHECK(cudaMemcpyAsync(out_logits, lg.p, lg.bytes(), cudaMemcpyDeviceToHost, S.main));
     CUDA_CHECK(cudaStreamSynchronize(S.main));
     for (int i = 0; i <= c; ++i)

@@ -39,7 +39,8 @@ void compute_metrics(const std::vector<Trace>& traces, double t_target, dbl_run_
 
 RunOutput run_double(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
                      int n_prompt, int max_new, const dbl_pipeline_options& o);
-RunOutput run_ar(Model& target, const int32_t* prompt, int n_prompt, int max_new, double t_target);
+RunOutput run_ar(Model& target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
+                 double temperature, uint64_t seed);
 RunOutput run_serial_sd(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
                         int n_prompt, int max_new, const dbl_pipeline_options& o, bool use_retrieval);
 
@@ -48,6 +49,6 @@ void profile_forward(Model& m, int ctx_len, int rows, int iters, double* out);
 
 // forward_batch as a stateless call (fresh lane / KV): argmax rows (c+1) and optionally logits
 void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,
-                       int32_t* out_argmax, float* out_logits);
+                       int32_t* out_argmax, float* out_logits, double* out_dists = nullptr);
 
 }  // namespace dbl

@@ -56,6 +56,10 @@ class Model {
     // Like forward, and also write fp32 logits (tables: probabilities) of rows [row0, L+c), in
     // order, to out_dev ((L+c-row0) x vocab).
     virtual void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) = 0;
+    // Like forward, and also write the fp64 next-token distributions of rows [row0, L+c), in order,
+    // to out_dev ((L+c-row0) x vocab, at most max_rows): the ProbVector rows of forward_batch
+    // (model.cpp:37-53) the sampled (temperature > 0) loop consumes.  Default: softmax of logits.
+    virtual void dists(Lane& lane, int max_tokens, int max_rows, double* out_dev, cudaStream_t s);
     virtual int max_forward_tokens() const { return 1 << 30; }
     // persistent (all-SM, cooperatively launched) grids one forward places on device(): at most two may
     // co-run on a GPU, so the decoder serializes draft and target work when the sum would exceed it
@@ -74,6 +78,7 @@ class Lane {
     DevBuf<int32_t> buf, argmax;
     LaneState* state = nullptr;   // device
     std::unique_ptr<LaneCache> cache;
+    DevBuf<float> logit_scratch;  // fp32 logits behind Model::dists (grown on demand)
     // host-side mirror (kept exact by the orchestrator)
     std::vector<int32_t> mirror;  // tokens the device buffer holds in [0, mirror.size())
     int kv_len = 0;               // host view of the valid KV prefix

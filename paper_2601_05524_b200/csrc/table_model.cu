@@ -32,7 +32,8 @@ struct TableDev {
 
 // rows p in [row_from, L+c): argmax of the distribution after buf[0..p]
 __global__ void table_forward_kernel(TableDev t, const int32_t* __restrict__ buf, LaneState* lane,
-                                     int32_t* __restrict__ argmax, float* __restrict__ probs_out) {
+                                     int32_t* __restrict__ argmax, float* __restrict__ probs_out,
+                                     double* __restrict__ dist_out) {
     const int L = lane->L, c = lane->c;
     const int row_from = lane->row0;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, ln = threadIdx.x & 31;
@@ -76,6 +77,8 @@ __global__ void table_forward_kernel(TableDev t, const int32_t* __restrict__ buf
         if (probs_out)
             for (int v = ln; v < t.vocab; v += 32)
                 probs_out[static_cast<long>(p - row_from) * t.vocab + v] = static_cast<float>(pr[v]);
+        if (dist_out)  // the ProbVector itself (row_for, model.cpp:23-35): exact fp64 copy
+            for (int v = ln; v < t.vocab; v += 32) dist_out[static_cast<long>(p - row_from) * t.vocab + v] = pr[v];
     }
 }
 
@@ -120,23 +123,27 @@ TableModel::TableModel(int order, int vocab, int64_t n_rows, const int32_t* wind
     CUDA_CHECK(cudaMemcpy(fallback_.p, fallback, vocab * 8, cudaMemcpyHostToDevice));
 }
 
-void TableModel::launch(Lane& lane, int max_tokens, float* probs_out, cudaStream_t s) {
+void TableModel::launch(Lane& lane, int max_tokens, float* probs_out, double* dist_out, cudaStream_t s) {
     TableDev t{windows_.p, slots_.p, probs_.p, fallback_.p, order_, vocab_, cap_mask_};
     const int rows = std::max(max_tokens, 1);
     const int threads = 256, warps_per_block = threads / 32;
     table_forward_kernel<<<(rows + warps_per_block - 1) / warps_per_block, threads, 0, s>>>(
-        t, lane.buf.p, lane.state, lane.argmax.p, probs_out);
+        t, lane.buf.p, lane.state, lane.argmax.p, probs_out, dist_out);
     CUDA_LAUNCH_CHECK();
     table_finish_kernel<<<1, 1, 0, s>>>(lane.state);
     CUDA_LAUNCH_CHECK();
 }
 
 void TableModel::forward(Lane& lane, int max_tokens, cudaStream_t s) {
-    launch(lane, max_tokens, nullptr, s);
+    launch(lane, max_tokens, nullptr, nullptr, s);
 }
 
 void TableModel::logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) {
-    launch(lane, max_tokens, out_dev, s);
+    launch(lane, max_tokens, out_dev, nullptr, s);
+}
+
+void TableModel::dists(Lane& lane, int max_tokens, int, double* out_dev, cudaStream_t s) {
+    launch(lane, max_tokens, nullptr, out_dev, s);
 }
 
 }  // namespace dbl

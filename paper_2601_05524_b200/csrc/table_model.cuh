@@ -17,10 +17,11 @@ class TableModel final : public Model {
     std::unique_ptr<LaneCache> make_cache(int) override { return nullptr; }
     void forward(Lane& lane, int max_tokens, cudaStream_t s) override;
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
+    void dists(Lane& lane, int max_tokens, int max_rows, double* out_dev, cudaStream_t s) override;
     std::string kind() const override { return "table"; }
 
   private:
-    void launch(Lane& lane, int max_tokens, float* probs_out, cudaStream_t s);
+    void launch(Lane& lane, int max_tokens, float* probs_out, double* dist_out, cudaStream_t s);
     int device_, order_, vocab_, cap_mask_ = 0;
     int64_t n_rows_;
     DevBuf<int32_t> windows_, slots_;

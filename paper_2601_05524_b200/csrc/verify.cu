@@ -10,44 +10,12 @@
 #include <memory>
 #include <vector>
 
+#include "rng.cuh"
 #include "verify.cuh"
 
 namespace dbl {
 
 namespace {
-
-// std::mt19937_64, standard parameters (the engine behind specpar::Rng, rng.hpp:19-30)
-__host__ __device__ inline void mt_seed(DevRng& g, uint64_t seed) {
-    g.mt[0] = seed;
-    for (int i = 1; i < 312; ++i) g.mt[i] = 6364136223846793005ULL * (g.mt[i - 1] ^ (g.mt[i - 1] >> 62)) + i;
-    g.idx = 312;
-}
-__device__ inline uint64_t mt_next(DevRng& g) {
-    if (g.idx >= 312) {
-        for (int i = 0; i < 312; ++i) {
-            const uint64_t x = (g.mt[i] & 0xFFFFFFFF80000000ULL) | (g.mt[(i + 1) % 312] & 0x7FFFFFFFULL);
-            uint64_t xa = x >> 1;
-            if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
-            g.mt[i] = g.mt[(i + 156) % 312] ^ xa;
-        }
-        g.idx = 0;
-    }
-    uint64_t y = g.mt[g.idx++];
-    y ^= (y >> 29) & 0x5555555555555555ULL;
-    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
-    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-    y ^= y >> 43;
-    return y;
-}
-// Rng::uniform (rng.hpp:23): the top 53 bits of one word
-__device__ inline double mt_uniform(DevRng& g) { return static_cast<double>(mt_next(g) >> 11) * 0x1.0p-53; }
-
-__host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // rng.hpp:8-13
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d49bb133111ebULL;
-    return x ^ (x >> 31);
-}
 
 struct Rows {  // ragged fp64 rows: row r = data[off[r], off[r+1])
     const double* data;
@@ -277,7 +245,7 @@ DeviceRng::DeviceRng(uint64_t seed, int device) : device_(device) {
     CUDA_CHECK(cudaDeviceSynchronize());
 }
 DeviceRng DeviceRng::derive(uint64_t seed, uint64_t round, uint64_t lane, int device) {  // rng.hpp:33-35
-    return DeviceRng(splitmix64(seed ^ splitmix64(round * 4 + lane + 1)), device);
+    return DeviceRng(derived_seed(seed, round, lane), device);
 }
 void DeviceRng::uniform(double* out, int n) {
     if (n < 0 || (n > 0 && !out)) throw_invalid("bad uniform request");

@@ -32,7 +32,8 @@ SOURCES = ["prior", "dynamic", "rejected", "context", "miss"]
 PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
 __all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
-           "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "run", "run_vanilla_ar",
+           "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
+           "run_vanilla_ar",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
            "parse_model_v1", "parse_dstore_v1"]
 
@@ -346,6 +347,16 @@ def forward_logits(model: _Model, context, candidates) -> np.ndarray:
     return out
 
 
+def forward_dists(model: _Model, context, candidates) -> np.ndarray:
+    """forward_batch's ProbVector rows (model.cpp:37-53), (|cands|+1) x vocab fp64: the rows the
+    sampled decode loop consumes (tables exact; transformers softmax of the logits)."""
+    ctx, cands = _i32(context), _i32(candidates)
+    out = np.zeros((len(cands) + 1, model.vocab_size), np.float64)
+    check(lib().dbl_forward_dists(model._h, _p32(ctx), len(ctx), _p32(cands), len(cands),
+                                  out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
+
+
 @dataclass
 class PipelineOptions:  # pipeline.hpp:36-44 (+ LatencyConfig, :15-29)
     gamma: int = 4
@@ -358,11 +369,13 @@ class PipelineOptions:  # pipeline.hpp:36-44 (+ LatencyConfig, :15-29)
     t_lookup: float = 0.0
     t_sync: float = 0.0
     use_graphs: bool = True
+    temperature: float = 0.0  # SamplerConfig (model.hpp:11-14): 0 = greedy
+    rng_seed: int = 0
 
     def _c(self) -> _Opts:
         return _Opts(self.gamma, self.depth, int(self.draft_retrieval), int(self.target_retrieval),
                      int(self.engine == "concurrent"), self.t_target, self.t_draft, self.t_lookup,
-                     self.t_sync, int(self.use_graphs))
+                     self.t_sync, int(self.use_graphs), float(self.temperature), int(self.rng_seed))
 
 
 @dataclass
@@ -413,8 +426,8 @@ def last_run_log() -> np.ndarray:
 
 
 def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float = 1.0,
-                   want_jsonl: bool = True) -> RunResult:
-    """run_vanilla_ar (harness.cpp:233-258), greedy."""
+                   want_jsonl: bool = True, temperature: float = 0.0, rng_seed: int = 0) -> RunResult:
+    """run_vanilla_ar (harness.cpp:233-258); temperature > 0 samples with the reference's AR stream."""
     p = _i32(prompt)
     cap = max(int(max_new_tokens), 1)
     out = np.zeros(cap, np.int32)
@@ -422,9 +435,9 @@ def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float 
     m = RunMetrics()
     js = _jsonl_buf(max_new_tokens) if want_jsonl else None
     jl = C.c_int64()
-    rc = lib().dbl_run_ar(target._h, _p32(p), len(p), int(max_new_tokens), float(t_target), _p32(out),
-                          cap, C.byref(n), C.byref(m), js, len(js) if js is not None else 0,
-                          C.byref(jl))
+    rc = lib().dbl_run_ar_sampled(target._h, _p32(p), len(p), int(max_new_tokens), float(t_target),
+                                  float(temperature), C.c_uint64(int(rng_seed)), _p32(out), cap, C.byref(n),
+                                  C.byref(m), js, len(js) if js is not None else 0, C.byref(jl))
     return _finish(rc, out, n, m, js, jl, want_jsonl)
 
 

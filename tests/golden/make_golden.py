@@ -62,9 +62,44 @@ def cfg_text(d: dict) -> str:
     return "".join(f"{k}={v}\n" for k, v in d.items())
 
 
+# the config's seed also drives build_setup (corpus, models, prompt), so config 1 keeps seed=11 and
+# varies the temperature; the randomized set below covers other seeds with their own setups
+SAMPLED = [(1.0, 11), (0.7, 11), (1.6, 11), (0.35, 11)]
+
+
+def sampled_vectors(ref: Reference, orc: Oracle):
+    """The temperature > 0 decode paths (accept_with_model, finish_round's residual correction, the
+    per-round derive_rng lanes, the AR stream): config 1 at several (temperature, seed) pairs for every
+    method, plus 30 randomized Double configs at temperature 1 with their AR outputs."""
+    text = open(CFG1).read()
+    out_c1 = []
+    for temp, seed in SAMPLED:
+        t = text.replace("temperature=0", f"temperature={temp}").replace("seed=11", f"seed={seed}")
+        case = {"temperature": temp, "seed": seed, "methods": {}}
+        for m in METHODS:
+            out, js, met = ref.run_config(t, m)
+            case["methods"][m] = {"output": out, "jsonl_sha256": sha(js),
+                                  "metrics": dict(zip(METRIC_KEYS, met))}
+        out_c1.append(case)
+    rand = []
+    for d in criterion1_configs(orc)[:30]:
+        d = dict(d, temperature=1.0)
+        t = cfg_text(d)
+        out, js, met = ref.run_config(t, "double")
+        ar, _, _ = ref.run_config(t, "vanilla_ar")
+        rand.append({"config": d, "output": out, "ar_output": ar, "jsonl_sha256": sha(js),
+                     "metrics": dict(zip(METRIC_KEYS, met))})
+    json.dump({"config1": out_c1, "random": rand}, open(os.path.join(HERE, "sampled.json"), "w"))
+
+
 def main():
     ref = Reference()
     orc = Oracle()
+    if "--sampled" in sys.argv:
+        sampled_vectors(ref, orc)
+        print("sampled vectors written to", HERE)
+        return
+    sampled_vectors(ref, orc)
     # ---- config 1 (ceiling_break.cfg) -------------------------------------------------------
     text = open(CFG1).read()
     draft_v1, target_v1, prior_v1, prompt = ref.export_setup(text)
