@@ -1,6 +1,8 @@
 // The extern "C" boundary (include/double_b200.h): status codes + thread-local last error; the
 // C++ exceptions of the engine never cross it.
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 
@@ -80,15 +82,61 @@ bool pdl_enabled() {
     return on;
 }
 void require_device(int device) {
+    static std::mutex mu;
+    static std::vector<int> ok;  // per device: 0 unknown, 1 sm_100, 2 other
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
         cudaGetLastError();
         throw Error(DBL_CUDA_ERROR, "no CUDA device visible (libdouble_b200 has no CPU fallback)");
     }
     if (device < 0 || device >= n) throw Error(DBL_INVALID_ARGUMENT, "device index out of range");
-    cudaDeviceProp p{};
-    CUDA_CHECK(cudaGetDeviceProperties(&p, device));
-    if (p.major != 10) throw Error(DBL_CUDA_ERROR, "libdouble_b200 is built for sm_100a (B200) only");
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_cast<int>(ok.size()) < n) ok.resize(n, 0);
+    if (!ok[device]) {
+        int major = 0;
+        CUDA_CHECK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        ok[device] = major == 10 ? 1 : 2;
+    }
+    if (ok[device] != 1) throw Error(DBL_CUDA_ERROR, "libdouble_b200 is built for sm_100a (B200) only");
+}
+
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;  // size class -> cached mapped pinned blocks
+size_t g_pin_cached = 0;
+constexpr size_t kPinCacheMax = size_t(512) << 20;
+}  // namespace
+
+void* pinned_get(size_t bytes, size_t* got) {
+    size_t cls = 4096;
+    while (cls < bytes) cls <<= 1;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.find(cls);
+        if (it != g_pin_free.end()) {
+            void* p = it->second;
+            g_pin_free.erase(it);
+            g_pin_cached -= cls;
+            *got = cls;
+            return p;
+        }
+    }
+    void* p = nullptr;
+    CUDA_CHECK(cudaHostAlloc(&p, cls, cudaHostAllocMapped | cudaHostAllocPortable));
+    *got = cls;
+    return p;
+}
+
+void pinned_put(void* p, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        if (g_pin_cached + bytes <= kPinCacheMax) {
+            g_pin_free.emplace(bytes, p);
+            g_pin_cached += bytes;
+            return;
+        }
+    }
+    cudaFreeHost(p);
 }
 }  // namespace dbl
 

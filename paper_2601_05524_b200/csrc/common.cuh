@@ -62,21 +62,32 @@ struct DevBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
-// RAII pinned host buffer
+// Process-wide cache of mapped pinned host blocks (power-of-two size classes).  Pinning pages costs
+// milliseconds per MiB; every run()/store call needs a few such buffers, so freed blocks are kept
+// for reuse (callers only release a block after the device is done with it).
+void* pinned_get(size_t bytes, size_t* got);
+void pinned_put(void* p, size_t bytes);
+
+// RAII pinned host buffer (mapped: dev() aliases it on the device)
 template <class T>
 struct PinBuf {
     T* p = nullptr;
     size_t n = 0;
+    size_t cap_bytes = 0;
     PinBuf() = default;
     explicit PinBuf(size_t count) { alloc(count); }
     PinBuf(const PinBuf&) = delete;
     PinBuf& operator=(const PinBuf&) = delete;
-    ~PinBuf() { if (p) cudaFreeHost(p); }
-    void alloc(size_t count) {
-        if (p) cudaFreeHost(p);
+    ~PinBuf() { release(); }
+    void release() {
+        if (p) pinned_put(p, cap_bytes);
         p = nullptr;
-        if (count) CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&p), count * sizeof(T),
-                                            cudaHostAllocMapped | cudaHostAllocPortable));
+        n = 0;
+        cap_bytes = 0;
+    }
+    void alloc(size_t count) {
+        release();
+        if (count) p = static_cast<T*>(pinned_get(count * sizeof(T), &cap_bytes));
         n = count;
     }
     T* dev() const {  // device alias of the mapped pinned allocation

@@ -252,7 +252,7 @@ DeviceStore::DeviceStore(int max_order, int depth, int device)
     DeviceGuard g(device);
     CUDA_CHECK(cudaMalloc(&desc_dev_, sizeof(StoreDesc)));
     CUDA_CHECK(cudaMemset(desc_dev_, 0, sizeof(StoreDesc)));
-    staging_.alloc(1 << 20);
+    staging_.alloc(1 << 16);  // grown on demand (insert)
     CUDA_CHECK(cudaEventCreateWithFlags(&staging_done_, cudaEventDisableTiming));
     for (int l = 0; l < 3; ++l) {
         layers_[l].max_order = max_order;
@@ -339,9 +339,14 @@ void DeviceStore::insert(int l, const int32_t* tokens, int n, long step, cudaStr
         throw_runtime("datastore layer exceeds 2^24 tokens/sequences");
     DeviceGuard g(device_);
     grow(l, h.n_tokens + n, h.n_seqs + 1, s);
-    if (static_cast<size_t>(n) > staging_.n) throw_invalid("insert longer than the staging ring");
-    if (staging_at_ + n > staging_.n) {  // ring wrap: previous payloads must have been consumed
-        CUDA_CHECK(cudaStreamSynchronize(s));
+    if (static_cast<size_t>(n) > staging_.n || staging_at_ + n > staging_.n) {
+        // ring wrap / growth: every payload in flight (any stream) must have been consumed first
+        CUDA_CHECK(cudaDeviceSynchronize());
+        if (static_cast<size_t>(n) > staging_.n) {
+            size_t cap = staging_.n;
+            while (cap < static_cast<size_t>(n)) cap *= 2;
+            staging_.alloc(cap);
+        }
         staging_at_ = 0;
     }
     int32_t* host = staging_.p + staging_at_;

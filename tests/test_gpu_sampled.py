@@ -152,3 +152,37 @@ def test_sampled_streams_follow_the_seed(dbl):
     assert outs[0] != outs[2]
     with pytest.raises(dbl.InvalidArgument):
         dbl.run(drf, tgt, dbl.HierarchicalDatastore(3, 10), [1, 2], 5, dbl.PipelineOptions(temperature=-1.0))
+
+
+def test_output_law_equals_target_chain_law(dbl):
+    """test_pipeline.cpp:300-354 on the device: V=3 (EOS=2) order-1 tables, 20000 sampled Double runs
+    with varied seeds; the empirical law of the <=3-token outputs is within TV 0.02 of the target
+    chain's exact law."""
+    import numpy as np
+    trow = {0: [0.5, 0.3, 0.2], 1: [0.2, 0.3, 0.5]}
+    tfb = [0.6, 0.3, 0.1]
+    target = dbl.TableModel(1, 3, np.array([0, 1], np.int32), np.array([trow[0], trow[1]]), np.array(tfb))
+    draft = dbl.TableModel(1, 3, np.array([0, 1], np.int32), np.array([[0.3, 0.4, 0.3], [0.4, 0.4, 0.2]]),
+                           np.array([0.3, 0.4, 0.3]))
+    exact = {}
+
+    def expand(ctx, out, p):
+        if len(out) == 3 or (out and out[-1] == 2):
+            exact[tuple(out)] = exact.get(tuple(out), 0.0) + p
+            return
+        dist = trow.get(ctx[-1], tfb)
+        for t in range(3):
+            if dist[t] > 0:
+                expand(ctx + [t], out + [t], p * dist[t])
+    expand([1], [], 1.0)
+    runs = 20000
+    emp = {}
+    for r in range(runs):
+        st = dbl.HierarchicalDatastore(3, 10)
+        st.prior.insert([1, 0, 1, 0, 0, 1], 0)
+        opts = dbl.PipelineOptions(gamma=2, t_target=1.0, t_draft=0.25, temperature=1.0, rng_seed=1000 + r)
+        out = tuple(dbl.run(draft, target, st, [1], 3, opts, want_jsonl=False).output)
+        emp[out] = emp.get(out, 0.0) + 1.0 / runs
+    tv = sum(abs(p - emp.get(s, 0.0)) for s, p in exact.items()) + sum(p for s, p in emp.items() if s not in exact)
+    assert tv / 2.0 < 0.02, tv / 2.0
+    assert abs(sum(exact.values()) - 1.0) < 1e-12
