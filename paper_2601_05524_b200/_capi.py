@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdouble_b200.so")
+LIB_PATH = os.environ.get("DBL_LIB") or os.path.join(PKG, "libdouble_b200.so")  # DBL_LIB: A/B timing of two builds
 
 I32P = C.POINTER(C.c_int32)
 I64P = C.POINTER(C.c_int64)
