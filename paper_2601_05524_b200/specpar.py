@@ -35,7 +35,8 @@ __all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
            "run_vanilla_ar",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
-           "parse_model_v1", "parse_dstore_v1"]
+           "parse_model_v1", "parse_dstore_v1", "serialize_model", "serialize_index", "save_model",
+           "load_model", "save_index", "load_index"]
 
 
 def _i32(xs) -> np.ndarray:
@@ -213,16 +214,81 @@ def build_prior(store: HierarchicalDatastore, corpora, rounds: int):
     return store
 
 
+def save_model(model: "TableModel", path: str):
+    """save_model (model.cpp:230-234)"""
+    with open(path, "w") as f:
+        f.write(model.to_model_v1())
+
+
+def load_model(path: str, device: int = 0) -> "TableModel":
+    """load_model (model.cpp:236-242): model-v1 file -> device TableModel"""
+    with open(path) as f:
+        return TableModel.from_model_v1(f.read(), device)
+
+
 def parse_dstore_v1(text: str):
     """dstore-v1 (datastore.cpp:161-187) -> (max_order, [sequences])."""
     lines = text.split("\n")
-    head = lines[0].split()
+    if lines and lines[-1] == "":  # getline semantics: a trailing newline ends the last line
+        lines.pop()
+    head = lines[0].split() if lines else []
     if len(head) < 3 or head[0] != "dstore-v1":
         raise DoubleError("dstore-v1: bad header")
     n = int(head[2])
     if len(lines) - 1 < n:
         raise DoubleError("dstore-v1: truncated")
     return int(head[1]), [[int(t) for t in lines[1 + i].split()] for i in range(n)]
+
+
+def serialize_index(max_order: int, sequences) -> str:
+    """serialize_index (datastore.cpp:161-169): dstore-v1 text of one layer's sequences."""
+    out = [f"dstore-v1 {int(max_order)} {len(sequences)}\n"]
+    for seq in sequences:
+        out.append(" ".join(str(int(t)) for t in seq) + "\n")
+    return "".join(out)
+
+
+def save_index(layer_or_store, path: str):
+    """save_index (datastore.cpp:189-193) of a device layer (a HierarchicalDatastore saves its prior)."""
+    layer = layer_or_store.prior if isinstance(layer_or_store, HierarchicalDatastore) else layer_or_store
+    with open(path, "w") as f:
+        f.write(serialize_index(layer.max_order, layer.sequences))
+
+
+def load_index(path: str, store: "HierarchicalDatastore | None" = None, layer: int = PRIOR):
+    """load_index (datastore.cpp:195-201) -> (max_order, sequences); with `store`, the sequences are
+    inserted into that layer with step = index, as parse_index does (datastore.cpp:171-187)."""
+    with open(path) as f:
+        mo, seqs = parse_dstore_v1(f.read())
+    if store is not None:
+        lay = (store.prior, store.dynamic, store.rejected)[layer]
+        lay.max_order = mo
+        for i, sq in enumerate(seqs):
+            lay.insert(sq, i)
+    return mo, seqs
+
+
+def _g17(x: float) -> str:  # std::snprintf("%.17g") (model.cpp:155-161, 176)
+    return "%.17g" % float(x)
+
+
+def serialize_model(order: int, vocab: int, windows, probs, fallback, smoothing: float = 0.1) -> str:
+    """serialize_model (model.cpp:174-190): model-v1 text; rows in std::map (lexicographic window) order."""
+    w = np.asarray(windows, np.int64).reshape(-1, order) if order else np.zeros((0, 0), np.int64)
+    pr = np.asarray(probs, np.float64).reshape(-1, vocab)
+    out = [f"model-v1 {int(vocab)} {int(order)} {_g17(smoothing)}\n"]
+    for i in sorted(range(len(w)), key=lambda r: tuple(w[r])):
+        out.append(" ".join(str(int(t)) for t in w[i]) + " :" + "".join(" " + _g17(v) for v in pr[i]) + "\n")
+    out.append("fallback :" + "".join(" " + _g17(v) for v in np.asarray(fallback, np.float64)) + "\n")
+    return "".join(out)
+
+
+def parse_model_v1_smoothing(text: str) -> float:
+    """the smoothing field of a model-v1 header (model.cpp:199-205)"""
+    head = text.split("\n", 1)[0].split()
+    if len(head) < 4 or head[0] != "model-v1":
+        raise DoubleError("model-v1: bad header")
+    return float(head[3])
 
 
 def parse_model_v1(text: str):
@@ -290,11 +356,21 @@ class TableModel(_Model):
                                      f.ctypes.data_as(C.POINTER(C.c_double)), int(device), C.byref(h)))
         self._h = h
         self.order = order
+        # host image for serialize_model / save_model (the device copy is the one the loop reads)
+        self._host = (int(order), int(vocab), w.reshape(-1, order) if order else w, p.reshape(-1, vocab), f)
+        self.smoothing = 0.1
 
     @classmethod
     def from_model_v1(cls, text: str, device: int = 0) -> "TableModel":
         order, vocab, w, p, f = parse_model_v1(text)
-        return cls(order, vocab, w, p, f, device)
+        m = cls(order, vocab, w, p, f, device)
+        m.smoothing = parse_model_v1_smoothing(text)
+        return m
+
+    def to_model_v1(self) -> str:
+        """serialize_model (model.cpp:174-190)"""
+        order, vocab, w, p, f = self._host
+        return serialize_model(order, vocab, w, p, f, self.smoothing)
 
 
 class Transformer(_Model):

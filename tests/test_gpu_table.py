@@ -190,3 +190,22 @@ def test_pipeline_errors_map_to_reference_types(dbl):
         dbl.run(d, t, st, [1, 2], 10, dbl.PipelineOptions(t_draft=0.0))
     r = dbl.run(d, t, st, [2, 2, 4], 1)  # max_new_tokens = 1 (test_pipeline.cpp:229-236)
     assert len(r.output) == 1
+
+
+def test_formats_through_device_objects(dbl, tmp_path):
+    """save_model / save_index / load_index (model.cpp:230-242, datastore.cpp:189-201) on device objects:
+    the files equal the reference-written ones byte for byte."""
+    d, t = _config1_models(dbl)
+    p = tmp_path / "t.model-v1"
+    dbl.save_model(t, str(p))
+    assert p.read_text() == open(os.path.join(GOLDEN, "config1_target.model-v1")).read()
+    t2 = dbl.load_model(str(p))
+    assert dbl.forward_batch(t2, [2, 2, 4], [28, 2]) == dbl.forward_batch(t, [2, 2, 4], [28, 2])
+    st = _config1_store(dbl)
+    q = tmp_path / "prior.dstore-v1"
+    dbl.save_index(st, str(q))
+    assert q.read_text() == open(os.path.join(GOLDEN, "config1_prior.dstore-v1")).read()
+    st2 = dbl.HierarchicalDatastore(3, 10)
+    dbl.load_index(str(q), st2)
+    assert st2.prior.sequences == st.prior.sequences
+    assert st2.lookup([2, 4], 10).candidates == st.lookup([2, 4], 10).candidates
