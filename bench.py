@@ -90,10 +90,31 @@ def workload(vocab, prompt_len, seed):
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clocks + throttle reasons sampled every 200 ms during the timed region.  In-process NVML (one
+    light query per sample) rather than an `nvidia-smi -lms` child: the latter's periodic driver calls
+    stall the decode loop's host-side CUDA calls for up to hundreds of ms, which would show up in the
+    end-to-end (host-API) number.  Falls back to nvidia-smi when NVML is unavailable."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
     def __init__(self, device: int):
-        self.device, self.lines, self.proc = device, [], None
+        self.device, self.lines, self.proc, self.nv = device, [], None, None
+        self.samples, self.stop = [], threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # noqa: BLE001 — no NVML: sample with nvidia-smi instead
+            self.nv = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -107,11 +128,24 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv = self.nv
+        while not self.stop.wait(0.2):
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((float(sm), [n for n, b in zip(self.NAMES, self.bits) if r & b]))
+            except Exception:  # noqa: BLE001
+                pass
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
@@ -121,7 +155,11 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nv is not None:
+            for v, rs in self.samples:
+                sm.append(v)
+                reasons.update(rs)
+            mx = float(self.mx)
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 6:
@@ -131,11 +169,12 @@ class ClockSampler:
                 mx = max(mx, float(f[1]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[2:6]):
+            for n, v in zip(self.NAMES, f[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "sampler": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 # --------------------------------------------------------------------------- distributed plumbing
