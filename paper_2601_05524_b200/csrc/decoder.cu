@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 
 #include "accept.cuh"
 #include "decoder.cuh"
@@ -420,6 +421,9 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
             tfwd_ms += ms;
             ++tfwd_n;
         }
+        if ((rr->draft_error || rr->target_error) && std::getenv("DBL_DEBUG_ROUND"))
+            std::fprintf(stderr, "dbl round %ld: draft_error %d target_error %d L %d nc %d ns %d n_segs %d draft_L %d ext_c %d\n",
+                         round, rr->draft_error, rr->target_error, L, nc, ns, rr->n_segs, rr->draft_L, rr->ext_c);
         check_round_errors(rr);
         const int c_t = rr->ext_c;
         trows += L + c_t - (nc - 1);
