@@ -123,6 +123,11 @@ struct Streams {
         CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CUDA_CHECK(cudaEventCreate(&tf0));
         CUDA_CHECK(cudaEventCreate(&tf1));
+        // The API's store / model calls run on the legacy stream and are asynchronous; these streams
+        // are non-blocking, so order the loop after everything already enqueued there (e.g. the prior's
+        // inserts of build_prior) explicitly.
+        CUDA_CHECK(cudaEventRecord(ready, 0));
+        CUDA_CHECK(cudaStreamWaitEvent(main, ready, 0));
     }
     cudaStream_t own_target = nullptr;  // target may alias draft (see run_double)
     ~Streams() {
