@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--max-new", type=int, default=0)
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--log-out", default="", help="write this run's decision log (json) here")
+    p.add_argument("--no-serving", action="store_true", help="skip the batched-serving side measurement")
     p.add_argument("--tp", choices=["auto", "off"], default="auto",
                    help="N>1: auto = the target tensor-parallel over the N GPUs (driven from rank 0), "
                         "off = N independent replicas")
@@ -409,7 +410,7 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
     rows_per_fwd = max(1, round(m0["target_rows"] / max(1, m0["target_fwd_count"])))
-    pv = profile(tgt, wl["prompt_len"] + max_new // 2, rows_per_fwd, iters=5)
+    pv = profile(tgt, wl["prompt_len"] + max_new // 2, rows_per_fwd, iters=20)
     achieved = pv[2] / (pv[1] / 1e3) / 1e9  # GB/s: algorithmic bytes / event-timed fwd_kernel duration
     traffic = None
     try:
@@ -446,6 +447,19 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
     }
     cs = clk.summary()
     line["clocks"] = {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"]}
+    if tp_world <= 1 and not a.no_serving:
+        # batched serving: B independent sequences of this workload's shape decoded in
+        # lockstep, ONE target forward per step over all of them (run_vanilla_ar_batch; every stream ==
+        # its own single-sequence AR).  Reported beside the headline, not in it.
+        serving = {}
+        for B in (8, 16):
+            ps = [workload(V, wl["prompt_len"], a.seed + 500 + b)[0] for b in range(B)]
+            dbl.run_vanilla_ar_batch(tgt, ps, 4)
+            _, sm = dbl.run_vanilla_ar_batch(tgt, ps, 64)
+            serving[f"B{B}"] = {"tokens_per_s": round(sm["tokens"] / (sm["device_ms"] / 1e3), 1),
+                                "ms_per_step": round(sm["device_ms"] / 64, 3)}
+        line["serving_batch"] = dict(serving, what="target-only greedy decode of B sequences (64 new tokens "
+                                     "each) with one batched fwd_kernel per step; value above is B = 1")
     if a.log_out and rank == 0:
         json.dump({"vocab": V, "prompt": prompt, "prior": prior, "max_new": max_new, "gamma": gamma,
                    "output": results[-1].output, "log": [int(x) for x in log]}, open(a.log_out, "w"))

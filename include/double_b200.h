@@ -163,6 +163,12 @@ int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_
 int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                        double temperature, uint64_t seed, int32_t* out, int cap, int* n_out,
                        dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len);
+/* Batched serving: run_vanilla_ar for n_seq (<= 16) independent prompts in lockstep,
+ * ONE forward over all sequences per step (the weight stream is shared).  prompts: prompt_off[n_seq+1]
+ * into prompt_tokens.  out: n_seq rows of max_new tokens (row b holds out_n[b] tokens, cut after EOS);
+ * every row equals that prompt's own dbl_run_ar output.  device_ms: CUDA-event time of the loop. */
+int dbl_run_ar_batch(dbl_model_t target, int n_seq, const int64_t* prompt_off, const int32_t* prompt_tokens,
+                     int max_new, int32_t* out, int32_t* out_n, double* device_ms, int64_t* kernel_launches);
 /* run_serial_sd (harness.cpp:264-369): draft-then-verify, use_retrieval = draft_retrieval method */
 int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
                       int n_prompt, int max_new, const dbl_pipeline_options* opts, int use_retrieval,

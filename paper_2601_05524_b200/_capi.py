@@ -85,6 +85,7 @@ PROTOTYPES = {
                    C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
     "dbl_run_ar_sampled": [VP, I32P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, I32P, C.c_int,
                            C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
+    "dbl_run_ar_batch": [VP, C.c_int, I64P, I32P, C.c_int, I32P, I32P, F64P, I64P],
     "dbl_run_serial_sd": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), C.c_int,
                           I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p,
                           C.c_int64, I64P],
@@ -122,6 +123,8 @@ def lib() -> C.CDLL:
                               "(there is no CPU fallback)")
         L = C.CDLL(LIB_PATH)
         for name, args in PROTOTYPES.items():
+            if os.environ.get("DBL_LIB") and not hasattr(L, name):
+                continue  # A/B timing against an older build: entry points it predates are absent
             f = getattr(L, name)
             f.argtypes = args
             f.restype = _RESTYPE.get(name, C.c_int)

@@ -365,6 +365,31 @@ int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, 
         copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
     });
 }
+int dbl_run_ar_batch(dbl_model_t target, int n_seq, const int64_t* prompt_off, const int32_t* prompt_tokens,
+                     int max_new, int32_t* out, int32_t* out_n, double* device_ms, int64_t* kernel_launches) {
+    return guarded([&] {
+        need(target, "target");
+        need(prompt_off, "prompt_off");
+        need(prompt_tokens, "prompt_tokens");
+        need(out, "out");
+        need(out_n, "out_n");
+        if (n_seq < 1) dbl::throw_invalid("n_seq must be >= 1");
+        std::vector<std::vector<int32_t>> prompts(n_seq);
+        for (int b = 0; b < n_seq; ++b) {
+            if (prompt_off[b + 1] < prompt_off[b]) dbl::throw_invalid("prompt offsets must be non-decreasing");
+            prompts[b].assign(prompt_tokens + prompt_off[b], prompt_tokens + prompt_off[b + 1]);
+        }
+        double ms = 0.0;
+        long long launches = 0;
+        const auto res = dbl::run_ar_batch(*target->impl, prompts, max_new, 1.0, &ms, &launches);
+        for (int b = 0; b < n_seq; ++b) {
+            out_n[b] = static_cast<int32_t>(res[b].output.size());
+            std::memcpy(out + static_cast<size_t>(b) * max_new, res[b].output.data(), res[b].output.size() * 4);
+        }
+        if (device_ms) *device_ms = ms;
+        if (kernel_launches) *kernel_launches = launches;
+    });
+}
 int dbl_run_serial_sd(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt,
                       int n_prompt, int max_new, const dbl_pipeline_options* opts, int use_retrieval,
                       int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,

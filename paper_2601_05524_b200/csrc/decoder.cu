@@ -47,6 +47,10 @@ Lane::Lane(Model& m, int cap) : model(m), capacity(cap) {
 Lane::~Lane() {
     if (state) cudaFree(state);
 }
+void Model::forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s) {
+    for (Lane* l : lanes) forward(*l, max_tokens, s);  // stateless models: one forward per lane
+}
+
 void Lane::set_state(int L, int c, int kv, int row0, cudaStream_t s) {
     set_lane_state_kernel<<<1, 1, 0, s>>>(state, L, c, kv, row0);
     CUDA_LAUNCH_CHECK();
@@ -665,6 +669,114 @@ RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, do
     res.metrics.prefill_ms = pre.ms();
     res.metrics.target_fwd_count = produced;
     res.metrics.target_rows = produced;
+    return res;
+}
+
+// ------------------------------------------------------------------------- run (batched AR)
+namespace {
+struct AppendBatch {
+    const int32_t* argmax[kMaxBatchSeqs];
+    int32_t* buf[kMaxBatchSeqs];
+    LaneState* st[kMaxBatchSeqs];
+    int n, stride;
+};
+__global__ void ar_append_batch_kernel(AppendBatch ab, int32_t* out_host, int i) {
+    const int b = threadIdx.x;
+    if (b >= ab.n) return;
+    LaneState* lane = ab.st[b];
+    const int L = lane->L;
+    const int tok = ab.argmax[b][L - 1];
+    ab.buf[b][L] = tok;
+    out_host[b * ab.stride + i] = tok;
+    if (tok < 0) lane->error = 1;
+    lane->L = L + 1;
+    lane->c = 0;
+    lane->kv_len = L;
+    lane->row0 = L;
+}
+}  // namespace
+
+std::vector<RunOutput> run_ar_batch(Model& tm, const std::vector<std::vector<int32_t>>& prompts, int max_new,
+                                    double t_target, double* device_ms, long long* launches) {
+    // run_vanilla_ar (harness.cpp:233-258) for B independent sequences in lockstep: every step is ONE
+    // forward over the B lanes (one row each) — the weight stream is shared, so B sequences cost about
+    // one.  Each output equals that sequence's own run_vanilla_ar (greedy, bitwise: a row's arithmetic
+    // never depends on the other rows).
+    const int B = static_cast<int>(prompts.size());
+    if (B < 1 || B > kMaxBatchSeqs) throw_invalid("run_ar_batch: 1.." + std::to_string(kMaxBatchSeqs) + " sequences");
+    if (max_new < 0) throw_invalid("max_new_tokens must be >= 0");
+    size_t longest = 0;
+    for (const auto& p : prompts) {
+        if (p.empty()) throw_invalid("prompt must be nonempty");
+        longest = std::max(longest, p.size());
+    }
+    DeviceGuard g(tm.device());
+    constexpr int kBlock = 16;
+    const int cap = static_cast<int>(longest) + max_new + kBlock + 8;
+    Streams S;
+    std::vector<std::unique_ptr<Lane>> lanes;
+    std::vector<std::unique_ptr<LaneIO>> ios;
+    std::vector<Lane*> lp;
+    AppendBatch ab{};
+    ab.n = B;
+    const int stride = std::max(max_new + kBlock, 1);
+    ab.stride = stride;
+    for (int b = 0; b < B; ++b) {
+        lanes.push_back(std::make_unique<Lane>(tm, cap));
+        Lane& l = *lanes.back();
+        ios.push_back(std::make_unique<LaneIO>(&l));
+        ios.back()->sync_tokens(prompts[b], S.main);
+        catch_up(l, static_cast<int>(prompts[b].size()) - 1, S.main);
+        const int n = static_cast<int>(prompts[b].size());
+        l.set_state(n, 0, l.kv_len, n - 1, S.main);
+        lp.push_back(&l);
+        ab.argmax[b] = l.argmax.p;
+        ab.buf[b] = l.buf.p;
+        ab.st[b] = l.state;
+    }
+    PinBuf<int32_t> outp(static_cast<size_t>(B) * stride);
+    int32_t* out_dev = outp.dev();
+    Timer loop;
+    CUDA_CHECK(cudaEventRecord(loop.a, S.main));
+    const long long launches0 = launch_counter();
+    std::vector<RunOutput> res(B);
+    std::vector<char> done(B, max_new == 0 ? 1 : 0);
+    const int32_t eos = tm.vocab() - 1;
+    int produced = 0;
+    while (produced < max_new && std::count(done.begin(), done.end(), 0) > 0) {
+        const int n = std::min(kBlock, max_new - produced);
+        for (int i = 0; i < n; ++i) {
+            tm.forward_lanes(lp, B, S.main);
+            ar_append_batch_kernel<<<1, 32, 0, S.main>>>(ab, out_dev, produced + i);
+            CUDA_LAUNCH_CHECK();
+        }
+        CUDA_CHECK(cudaStreamSynchronize(S.main));
+        for (int b = 0; b < B; ++b) {
+            for (int i = 0; i < n && !done[b]; ++i) {
+                const int32_t tok = outp.p[static_cast<size_t>(b) * stride + produced + i];
+                if (tok < 0) throw_runtime("degenerate distribution");
+                res[b].output.push_back(tok);
+                Trace t;
+                t.round = produced + i;
+                t.mode = "ar";
+                t.committed_count = 1;
+                t.kind = "ar_step";
+                t.clock_delta = t_target;
+                res[b].traces.push_back(std::move(t));
+                if (tok == eos) done[b] = 1;
+            }
+        }
+        produced += n;
+    }
+    CUDA_CHECK(cudaEventRecord(loop.b, S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.main));
+    for (auto& r : res) {
+        compute_metrics(r.traces, t_target, &r.metrics);
+        r.metrics.clock = static_cast<double>(r.metrics.tokens) * t_target;
+        r.metrics.speedup = 1.0;
+    }
+    if (device_ms) *device_ms = loop.ms();
+    if (launches) *launches = launch_counter() - launches0;
     return res;
 }
 

@@ -41,6 +41,10 @@ RunOutput run_double(Model& draft, Model& target, DeviceStore& store, const int3
                      int n_prompt, int max_new, const dbl_pipeline_options& o);
 RunOutput run_ar(Model& target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                  double temperature, uint64_t seed);
+// run_vanilla_ar for up to kMaxBatchSeqs sequences in lockstep, one batched forward per step
+constexpr int kMaxBatchSeqs = 16;
+std::vector<RunOutput> run_ar_batch(Model& target, const std::vector<std::vector<int32_t>>& prompts, int max_new,
+                                    double t_target, double* device_ms, long long* launches);
 RunOutput run_serial_sd(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
                         int n_prompt, int max_new, const dbl_pipeline_options& o, bool use_retrieval);
 

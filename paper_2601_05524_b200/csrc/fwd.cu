@@ -168,15 +168,16 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
 // position combine in chunk order (the last-arriving warp does it), so the result depends on the
 // position only — never on how many tokens the forward carries.
 template <int HD>
-__device__ __forceinline__ void attn_item(const FwdArgs& a, const FwdPhase& P, int t, int hq, int j, int start,
-                                          float* q_s, float* p_s, int lane) {
+__device__ __forceinline__ void attn_item(const FwdArgs& a, int t, int hq, int j, int pos, const int32_t* page_table,
+                                          const __nv_bfloat16* kc, const __nv_bfloat16* vc, float* q_s, float* p_s,
+                                          int lane) {
     constexpr int DPL = HD / 32;
     const int nh = a.nh, kvh = hq / (nh / a.nkv);
-    const int pos = start + t, k0 = j * kAttnChunk;
+    const int k0 = j * kAttnChunk;
     const int nch = pos / kAttnChunk + 1, nk = min(kAttnChunk, pos - k0 + 1);
-    const long long page = a.page_table[j];
-    const __nv_bfloat16* kp = P.kc + (page * a.nkv + kvh) * kPage * HD;
-    const __nv_bfloat16* vp = P.vc + (page * a.nkv + kvh) * kPage * HD;
+    const long long page = page_table[j];
+    const __nv_bfloat16* kp = kc + (page * a.nkv + kvh) * kPage * HD;
+    const __nv_bfloat16* vp = vc + (page * a.nkv + kvh) * kPage * HD;
     const __nv_bfloat16* qs = a.qbuf + (static_cast<long long>(t) * nh + hq) * HD;
 #pragma unroll
     for (int e = 0; e < DPL; ++e) q_s[lane * DPL + e] = __bfloat162float(qs[lane * DPL + e]);
@@ -285,6 +286,20 @@ __device__ __forceinline__ void attn_item(const FwdArgs& a, const FwdPhase& P, i
     for (int e = 0; e < DPL; ++e) out[e] = __float2bfloat16_rn(acc[e] * inv);
 }
 
+struct BatchSmem {  // a batched forward's row -> lane map (the per-lane pointers stay in the
+                   // __grid_constant__ kernel parameter, indexed in place)
+    int n;
+    int off[kMaxBatch + 1];
+    int start[kMaxBatch], lc[kMaxBatch];
+};
+// forward row t -> its lane (return) and position (*pos)
+__device__ __forceinline__ int batch_row(const BatchSmem& B, int t, int* pos) {
+    int b = 0;
+    while (b + 1 < B.n && t >= B.off[b + 1]) ++b;
+    *pos = B.start[b] + (t - B.off[b]);
+    return b;
+}
+
 struct FwdSmem {
     uint64_t full[kFwdMaxStages], empty[kFwdMaxStages], tfull[2], tempty[2];
     unsigned long long ep;
@@ -297,22 +312,36 @@ struct FwdSmem {
     float qv[512];
     float pv[256];
     TpPeers peers;  // copy of FwdArgs::peers (dynamic indexing of kernel parameters would use local memory)
+    BatchSmem bt;   // batched forward only
     float pre[16 * 128];  // a finisher's presummed split-K partials, parked across the accumulator wait
 };
 static_assert(sizeof(FwdSmem) <= kFwdMiscBytes, "misc shared state exceeds its budget");
 
 // one attention phase of this warp
-template <int HD>
+template <int HD, bool kB>
 __device__ __forceinline__ void attn_phase(const FwdArgs& a, const FwdPhase& P, int start, int T, int gw, int GW,
-                                        float* q_s, float* p_s, int lane) {
+                                        float* q_s, float* p_s, int lane, const BatchSmem& B) {
     const int nh = a.nh;
-    const int nch_max = (start + T - 1) / kAttnChunk + 1;
+    int max_pos = start + T - 1;
+    if constexpr (kB) {
+        max_pos = 0;
+        for (int b = 0; b < B.n; ++b) max_pos = max(max_pos, B.lc[b] - 1);
+    }
+    const int nch_max = max_pos / kAttnChunk + 1;
     const int items = T * nh * nch_max;
     for (int item = gw; item < items; item += GW) {
         const int j = item % nch_max, rest = item / nch_max;
         const int hq = rest % nh, t = rest / nh;
-        if (j * kAttnChunk > start + t) continue;
-        attn_item<HD>(a, P, t, hq, j, start, q_s, p_s, lane);
+        if constexpr (kB) {
+            int pos;
+            const int b = batch_row(B, t, &pos);
+            if (j * kAttnChunk > pos) continue;
+            attn_item<HD>(a, t, hq, j, pos, a.batch.page_table[b], P.kc + a.batch.koff[b], P.vc + a.batch.voff[b],
+                          q_s, p_s, lane);
+        } else {
+            if (j * kAttnChunk > start + t) continue;
+            attn_item<HD>(a, t, hq, j, start + t, a.page_table, P.kc, P.vc, q_s, p_s, lane);
+        }
     }
 }
 
@@ -334,6 +363,7 @@ struct TileCtx {
     bool has_pre;            // pre holds the presummed partials of the other contributors (decode)
     float* pre;              // shared memory [16][128] (column-major: thread r reads pre[i*128 + r])
     const TpPeers* peers;    // tensor-parallel exchange buffers (shared-memory copy)
+    const BatchSmem* bt;     // batched forward: rows -> lanes
 };
 
 template <int CH>
@@ -431,7 +461,7 @@ __device__ __forceinline__ void presum(const TileCtx& x, int ch, float (&pre)[16
     }
 }
 
-template <int CH, bool kTP>
+template <int CH, bool kTP, bool kB>
 __device__ __forceinline__ void finish_tile(const TileCtx& x) {
     const FwdArgs& a = *x.a;
     const FwdPhase& P = *x.P;
@@ -570,9 +600,11 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
                     const int dm = dd % half;
                     float2 cs[CH];
 #pragma unroll
-                    for (int i = 0; i < CH; ++i)
-                        cs[i] = ch + i < T ? __ldg(a.rope + static_cast<long long>(x.start + ch + i) * half + dm)
-                                           : make_float2(1.f, 0.f);
+                    for (int i = 0; i < CH; ++i) {
+                        int pos = x.start + ch + i;
+                        if constexpr (kB) if (ch + i < T) batch_row(*x.bt, ch + i, &pos);
+                        cs[i] = ch + i < T ? __ldg(a.rope + static_cast<long long>(pos) * half + dm) : make_float2(1.f, 0.f);
+                    }
 #pragma unroll
                     for (int i = 0; i < CH; ++i) {
                         const float partner = __shfl_xor_sync(0xffffffffu, xv[i], 16);
@@ -584,6 +616,18 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
 #pragma unroll
                     for (int i = 0; i < CH; ++i)
                         if (ch + i < T) dq[static_cast<long long>(i) * a.nh * hd] = __float2bfloat16_rn(xv[i]);
+                } else if constexpr (kB) {  // each row appends to its own lane's cache
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        if (ch + i < T) {
+                            int pos;
+                            const int b = batch_row(*x.bt, ch + i, &pos);
+                            __nv_bfloat16* kvc = is_k ? P.kc + a.batch.koff[b] : P.vc + a.batch.voff[b];
+                            const int pg = __ldg(a.batch.page_table[b] + pos / kPage);
+                            kvc[((static_cast<long long>(pg) * a.nkv + head) * kPage + pos % kPage) * hd + dd] =
+                                __float2bfloat16_rn(xv[i]);
+                        }
+                    }
                 } else {
                     __nv_bfloat16* kvc = is_k ? P.kc : P.vc;
                     int pg[CH];
@@ -631,7 +675,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
 }
 
 // ------------------------------------------------------------------ the kernel
-template <bool kTP>  // tensor-parallel exchange compiled in only where used (register pressure)
+template <bool kTP, bool kB>  // TP exchange / batched lanes compiled in only where used (register pressure)
 __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_constant__ FwdArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ FwdSmem sm;  // static: the compiler keeps these in the shared address space (LDS/STS)
@@ -659,11 +703,29 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
     const uint32_t ncols = static_cast<uint32_t>(a.nacc * a.acc_cols);
 
     if (threadIdx.x == 0) {
-        const LaneState* L = a.lane;
-        const int start = min(L->kv_len, L->row0), Lc = L->L + L->c;
-        sint[0] = start;
-        sint[1] = Lc - start;
-        sint[2] = Lc;
+        if constexpr (kB) {
+            BatchSmem& B = sm.bt;
+            B.n = a.batch.n;
+            int off = 0;
+            for (int b = 0; b < B.n; ++b) {
+                const LaneState* Ls = a.batch.lane[b];
+                const int st = min(Ls->kv_len, Ls->row0), lc = Ls->L + Ls->c;
+                B.off[b] = off;
+                B.start[b] = st;
+                B.lc[b] = lc;
+                off += lc - st;
+            }
+            B.off[B.n] = off;
+            sint[0] = 0;
+            sint[1] = off;
+            sint[2] = 0;
+        } else {
+            const LaneState* L = a.lane;
+            const int start = min(L->kv_len, L->row0), Lc = L->L + L->c;
+            sint[0] = start;
+            sint[1] = Lc - start;
+            sint[2] = Lc;
+        }
         *sep = *reinterpret_cast<volatile unsigned long long*>(a.epoch);
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
@@ -685,7 +747,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
     const unsigned long long ep = *sep;
     if (T < 1 || T > tp) {  // host contract violated: nothing consistent to compute
         if (c == 0 && threadIdx.x == 0) {
-            a.lane->error = 2;
+            if constexpr (kB) a.batch.lane[0]->error = 2;
+            else a.lane->error = 2;
             atomicExch(a.err, 100);
         }
         __syncthreads();
@@ -813,14 +876,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             if (et == 0) wait_dep(a, p, ep, 5);
             named_bar_sync(1, 128);
         };
-        {  // warm L2: this forward's embedding rows and RoPE rows (tiny, cold, on the critical path)
+        if constexpr (!kB) {  // warm L2: this forward's embedding rows and RoPE rows (tiny, cold, on the critical path)
             const int gt = c * 128 + et, GT = G * 128;
             for (int t = gt; t < T; t += GT) l2_warm(a.embed + static_cast<long long>(a.buf[start + t]) * h, h * 2, 0, 1);
             if (gt == GT - 1) l2_warm(a.rope + static_cast<long long>(start) * (a.hd / 2), T * (a.hd / 2) * 8LL, 0, 1);
         }
         for (int p = 0; p < a.n_ph; ++p) {
             const FwdPhase& P = a.ph[p];
-            if (P.kind == kPhGemm && P.epi == kFeQkv) {
+            if (!kB && P.kind == kPhGemm && P.epi == kFeQkv) {
                 // warm L2 with this layer's norm weights and the context's K/V (read by ATTN next)
                 const int pages = (start + T + kPage - 1) / kPage;
                 const long long kv_bytes = static_cast<long long>(pages) * a.nkv * kPage * a.hd * 2;
@@ -834,7 +897,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                 const int items = tp * nt;
                 for (int item = gw; item < items; item += GW) {
                     const int t = item / nt, mt = item % nt;
-                    const int tok = t < T ? a.buf[start + t] : 0;
+                    int tok = 0;
+                    if (t < T) {
+                        if constexpr (kB) {
+                            int pos;
+                            const int b = batch_row(sm.bt, t, &pos);
+                            tok = a.batch.buf[b][pos];
+                        } else {
+                            tok = a.buf[start + t];
+                        }
+                    }
                     const int col = mt * kBM + lane * 4;
                     const uint2 raw = *reinterpret_cast<const uint2*>(a.embed + static_cast<long long>(tok) * h + col);
                     const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
@@ -878,7 +950,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     const uint32_t taddr = tmem + static_cast<uint32_t>(buf * a.acc_cols) + (static_cast<uint32_t>(q * 32) << 16);
                     const bool finisher = my == 0;
                     TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
-                               q, lane, et, r, rs, red, sval, sidx, tag, false, sm.pre, &sm.peers};
+                               q, lane, et, r, rs, red, sval, sidx, tag, false, sm.pre, &sm.peers, &sm.bt};
                     const bool early = finisher && n_contrib > 1 && tp == 16;
                     if (early) {  // the other contributors are (nearly always) done: sum them now
                         wait_partials(tc);
@@ -905,7 +977,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     } else {
                         if (et == 0) stamp(a, p, 8);
                         if (n_contrib > 1 && !early) wait_partials(tc);
-                        finish_tile<16, kTP>(tc);  // 16-column chunks
+                        finish_tile<16, kTP, kB>(tc);  // 16-column chunks
                     }
                     if (et == 0 && finisher) stamp(a, p, 10);
                     tc_fence_before();
@@ -919,8 +991,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             } else if (P.kind == kPhAttn) {  // ------------------------- split-KV causal attention
                 acquire(P.dep);
                 stamp(a, p, 3);
-                if (a.hd == 128) attn_phase<128>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane);
-                else attn_phase<64>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane);
+                if (a.hd == 128) attn_phase<128, kB>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane, sm.bt);
+                else attn_phase<64, kB>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane, sm.bt);
                 if (lane == 0) stamp(a, p, 8 + ew);  // each aux warp's last item done
                 signal(p);
             } else {  // kPhArgmax ----------------------------------------- final argmax + cursor
@@ -941,7 +1013,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
                     }
                     if (lane == 0) {
-                        if constexpr (!kTP) {
+                        if constexpr (kB) {
+                            int pos;
+                            const int b = batch_row(sm.bt, t, &pos);
+                            a.batch.argmax[b][pos] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                        } else if constexpr (!kTP) {
                             a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
                         } else {  // this rank's shard winner -> every rank's exchange slot [my rank][t]
                             for (int rr = 0; rr < a.tp_world; ++rr)
@@ -972,8 +1048,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                             a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
                         }
                     }
-                    a.lane->start = start;
-                    a.lane->kv_len = sint[2];
+                    if constexpr (kB) {
+                        for (int b = 0; b < sm.bt.n; ++b) {
+                            a.batch.lane[b]->start = sm.bt.start[b];
+                            a.batch.lane[b]->kv_len = sm.bt.lc[b];
+                        }
+                    } else {
+                        a.lane->start = start;
+                        a.lane->kv_len = sint[2];
+                    }
                     __threadfence();
                     *reinterpret_cast<volatile unsigned long long*>(a.epoch) = ep + 1;
                 }
@@ -993,9 +1076,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
 void fwd_prepare() {
     static std::once_flag once;
     std::call_once(once, [] {
-        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024 - kFwdMiscBytes));
-        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        227 * 1024 - kFwdMiscBytes));
+        CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024 - kFwdMiscBytes));
     });
 }
@@ -1071,8 +1156,14 @@ void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (a.tp_world > 1) CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<true>, a));
-    else CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<false>, a));
+    if (a.batch.n > 0) {
+        if (a.tp_world > 1) throw_invalid("batched forward: tensor-parallel lanes are not supported");
+        CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<false, true>, a));
+    } else if (a.tp_world > 1) {
+        CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<true, false>, a));
+    } else {
+        CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<false, false>, a));
+    }
     ++launch_counter();
 }
 

@@ -67,6 +67,19 @@ struct TpPeers {
     unsigned long long* aflag[kMaxTpRanks];  // [src rank] tags
 };
 
+// Batched forward (several independent sequences in one weight stream): lane b's
+// rows [min(kv_len, row0), L + c) are rows off[b].. of the forward; every lane has its own token
+// buffer, argmax rows, page table and KV cache (same capacity), addressed relative to lane 0's.
+constexpr int kMaxBatch = 16;
+struct FwdBatch {
+    int n;  // 0: single-lane forward (FwdArgs::lane / buf / argmax / page_table)
+    LaneState* lane[kMaxBatch];
+    const int32_t* buf[kMaxBatch];
+    int32_t* argmax[kMaxBatch];
+    const int32_t* page_table[kMaxBatch];
+    long long koff[kMaxBatch], voff[kMaxBatch];  // element offsets of lane b's K / V cache from lane 0's
+};
+
 struct FwdArgs {
     CUtensorMap wmaps[5];  // qkv, o, gate|up, down (all layers stacked), lm head
     CUtensorMap xmaps[3][5];  // xb, attn, act; boxes of 1, 2, 4, 8, 16 token rows
@@ -103,6 +116,7 @@ struct FwdArgs {
     unsigned long long* trace;  // optional [n_ph][G][16] %globaltimer stamps
     int tp_world, tp_rank, vocab_off;  // tensor parallel (world 1: none); vocab_off = rank * vocab_l
     TpPeers peers;
+    FwdBatch batch;
 };
 
 constexpr int kFwdThreads = 192;  // warp 0 TMA producer, warp 1 MMA, warps 2..5 epilogue / aux work

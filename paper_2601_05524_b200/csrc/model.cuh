@@ -61,6 +61,9 @@ class Model {
     // (model.cpp:37-53) the sampled (temperature > 0) loop consumes.  Default: softmax of logits.
     virtual void dists(Lane& lane, int max_tokens, int max_rows, double* out_dev, cudaStream_t s);
     virtual int max_forward_tokens() const { return 1 << 30; }
+    // One forward over several lanes at once (independent sequences sharing one weight stream): lane
+    // b's rows [min(kv_len, row0), L+c) as in forward(); max_tokens bounds the rows of all lanes.
+    virtual void forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s);
     // persistent (all-SM, cooperatively launched) grids one forward places on device(): at most two may
     // co-run on a GPU, so the decoder serializes draft and target work when the sum would exceed it
     virtual int persistent_grids() const { return 0; }

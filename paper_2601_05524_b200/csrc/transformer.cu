@@ -332,7 +332,8 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
 
 namespace {
 void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32_t* buf, int32_t* argmax,
-                 LaneCache* cache, int max_tokens, float* logits, int ld_logits, cudaStream_t s) {
+                 LaneCache* cache, int max_tokens, float* logits, int ld_logits, cudaStream_t s,
+                 const std::vector<Lane*>* batch = nullptr) {
     if (max_tokens < 1) max_tokens = 1;
     if (max_tokens > kMaxTp) throw_runtime("forward exceeds 256 token columns (decoder must chunk)");
     const int tp = (max_tokens + 15) / 16 * 16;
@@ -396,6 +397,25 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
     a.tp_rank = m.rank;
     a.vocab_off = m.rank * m.vocab_l;
     a.peers = c.peers;
+    if (batch) {  // several lanes in one forward; lane 0's cache holds the shared scratch and phase table
+        if (batch->empty() || static_cast<int>(batch->size()) > kMaxBatch)
+            throw_invalid("batched forward: 1.." + std::to_string(kMaxBatch) + " lanes");
+        if (m.world > 1) throw_invalid("batched forward: tensor-parallel models are not supported");
+        a.batch.n = static_cast<int>(batch->size());
+        for (int b = 0; b < a.batch.n; ++b) {
+            Lane& l = *(*batch)[b];
+            TfCache& cb = *static_cast<TfCache*>(l.cache.get());
+            if (cb.capacity != c.capacity) throw_invalid("batched forward: lanes must have equal capacity");
+            a.batch.lane[b] = l.state;
+            a.batch.buf[b] = l.buf.p;
+            a.batch.argmax[b] = l.argmax.p;
+            a.batch.page_table[b] = cb.page_table.p;
+            a.batch.koff[b] = static_cast<long long>(reinterpret_cast<intptr_t>(cb.kbuf.p) -
+                                                     reinterpret_cast<intptr_t>(c.kbuf.p)) / 2;
+            a.batch.voff[b] = static_cast<long long>(reinterpret_cast<intptr_t>(cb.vbuf.p) -
+                                                     reinterpret_cast<intptr_t>(c.vbuf.p)) / 2;
+        }
+    }
     // vocab-parallel logits: this rank's columns of the caller's [rows][vocab] buffer
     if (logits) a.logits = logits + static_cast<size_t>(m.rank) * m.vocab_l;
     if (m.prof) m.prof->next(s);
@@ -409,6 +429,12 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
 
 void Transformer::forward(Lane& lane, int max_tokens, cudaStream_t s) {
     run_forward(*impl_, device_, lane.state, lane.buf.p, lane.argmax.p, lane.cache.get(), max_tokens, nullptr, 0, s);
+}
+
+void Transformer::forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s) {
+    if (lanes.empty()) return;
+    Lane& l0 = *lanes[0];
+    run_forward(*impl_, device_, l0.state, l0.buf.p, l0.argmax.p, l0.cache.get(), max_tokens, nullptr, 0, s, &lanes);
 }
 
 void Transformer::logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) {

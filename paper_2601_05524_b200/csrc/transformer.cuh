@@ -17,6 +17,7 @@ class Transformer final : public Model {
     std::unique_ptr<LaneCache> make_cache(int capacity) override;
     void forward(Lane& lane, int max_tokens, cudaStream_t s) override;
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
+    void forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s) override;
     int max_forward_tokens() const override;
     std::string kind() const override { return "transformer"; }
     int persistent_grids() const override { return 1; }

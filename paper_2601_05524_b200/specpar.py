@@ -33,7 +33,7 @@ PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
 __all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
-           "run_vanilla_ar",
+           "run_vanilla_ar", "run_vanilla_ar_batch",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
            "parse_model_v1", "parse_dstore_v1", "serialize_model", "serialize_index", "save_model",
            "load_model", "save_index", "load_index"]
@@ -515,6 +515,23 @@ def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float 
                                   float(temperature), C.c_uint64(int(rng_seed)), _p32(out), cap, C.byref(n),
                                   C.byref(m), js, len(js) if js is not None else 0, C.byref(jl))
     return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+def run_vanilla_ar_batch(target: _Model, prompts, max_new_tokens: int):
+    """Batched serving: run_vanilla_ar for several prompts in lockstep, one forward per step over all of
+    them.  Returns (outputs, {"device_ms", "tokens", "kernel_launches"})."""
+    ps = [_i32(p) for p in prompts]
+    off = np.zeros(len(ps) + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in ps])
+    toks = np.concatenate(ps) if ps else np.zeros(1, np.int32)
+    n = max(int(max_new_tokens), 1)
+    out = np.zeros(len(ps) * n, np.int32)
+    out_n = np.zeros(max(len(ps), 1), np.int32)
+    ms, launches = C.c_double(), C.c_int64()
+    check(lib().dbl_run_ar_batch(target._h, len(ps), off.ctypes.data_as(C.POINTER(C.c_int64)), _p32(toks),
+                                 int(max_new_tokens), _p32(out), _p32(out_n), C.byref(ms), C.byref(launches)))
+    outs = [out[b * int(max_new_tokens): b * int(max_new_tokens) + out_n[b]].tolist() for b in range(len(ps))]
+    return outs, {"device_ms": ms.value, "tokens": int(sum(out_n[:len(ps)])), "kernel_launches": launches.value}
 
 
 def run_serial_sd(draft: _Model, target: _Model, store: HierarchicalDatastore, prompt,
