@@ -163,6 +163,14 @@ int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_
 int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                        double temperature, uint64_t seed, int32_t* out, int cap, int* n_out,
                        dbl_run_metrics* metrics, char* jsonl, int64_t jsonl_cap, int64_t* jsonl_len);
+/* Batched DOUBLE: run() for n_seq (<= 16) independent sequences, one datastore each
+ * (stores[b]), sharing every draft-segment and verify forward.  out: n_seq rows of max_new tokens
+ * (out_n[b] valid); metrics[b]; jsonl: the sequences' traces_to_jsonl texts back to back, jsonl_lens[b]
+ * bytes each (may be NULL).  Each sequence's result equals its own dbl_run. */
+int dbl_run_batch(dbl_model_t draft, dbl_model_t target, int n_seq, const dbl_store_t* stores,
+                  const int64_t* prompt_off, const int32_t* prompt_tokens, int max_new,
+                  const dbl_pipeline_options* opts, int32_t* out, int32_t* out_n, dbl_run_metrics* metrics,
+                  char* jsonl, int64_t jsonl_cap, int64_t* jsonl_lens);
 /* Batched serving: run_vanilla_ar for n_seq (<= 16) independent prompts in lockstep,
  * ONE forward over all sequences per step (the weight stream is shared).  prompts: prompt_off[n_seq+1]
  * into prompt_tokens.  out: n_seq rows of max_new tokens (row b holds out_n[b] tokens, cut after EOS);

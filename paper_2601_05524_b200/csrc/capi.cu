@@ -365,6 +365,47 @@ int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, 
         copy_run(r, out, cap, n_out, metrics, jsonl, jsonl_cap, jsonl_len);
     });
 }
+int dbl_run_batch(dbl_model_t draft, dbl_model_t target, int n_seq, const dbl_store_t* stores,
+                  const int64_t* prompt_off, const int32_t* prompt_tokens, int max_new,
+                  const dbl_pipeline_options* opts, int32_t* out, int32_t* out_n, dbl_run_metrics* metrics,
+                  char* jsonl, int64_t jsonl_cap, int64_t* jsonl_lens) {
+    return guarded([&] {
+        need(draft, "draft");
+        need(target, "target");
+        need(stores, "stores");
+        need(prompt_off, "prompt_off");
+        need(prompt_tokens, "prompt_tokens");
+        need(opts, "options");
+        need(out, "out");
+        need(out_n, "out_n");
+        if (n_seq < 1) dbl::throw_invalid("n_seq must be >= 1");
+        std::vector<dbl::DeviceStore*> sts(n_seq);
+        std::vector<std::vector<int32_t>> prompts(n_seq);
+        for (int b = 0; b < n_seq; ++b) {
+            need(stores[b], "store");
+            sts[b] = stores[b]->impl.get();
+            if (prompt_off[b + 1] < prompt_off[b]) dbl::throw_invalid("prompt offsets must be non-decreasing");
+            prompts[b].assign(prompt_tokens + prompt_off[b], prompt_tokens + prompt_off[b + 1]);
+        }
+        const auto res = dbl::run_double_multi(*draft->impl, *target->impl, sts, prompts, max_new, *opts);
+        int64_t at = 0;
+        for (int b = 0; b < n_seq; ++b) {
+            copy_run(res[b], out + static_cast<size_t>(b) * max_new, max_new, nullptr, metrics ? metrics + b : nullptr,
+                     nullptr, 0, nullptr);
+            out_n[b] = static_cast<int32_t>(res[b].output.size());
+            if (jsonl || jsonl_lens) {
+                const std::string js = dbl::traces_to_jsonl(res[b].traces);
+                if (jsonl_lens) jsonl_lens[b] = static_cast<int64_t>(js.size());
+                if (jsonl) {
+                    if (at + static_cast<int64_t>(js.size()) + 1 > jsonl_cap) dbl::throw_invalid("jsonl buffer too small");
+                    std::memcpy(jsonl + at, js.data(), js.size());
+                    at += static_cast<int64_t>(js.size());
+                    jsonl[at] = 0;
+                }
+            }
+        }
+    });
+}
 int dbl_run_ar_batch(dbl_model_t target, int n_seq, const int64_t* prompt_off, const int32_t* prompt_tokens,
                      int max_new, int32_t* out, int32_t* out_n, double* device_ms, int64_t* kernel_launches) {
     return guarded([&] {

@@ -319,108 +319,194 @@ std::string traces_to_jsonl(const std::vector<Trace>& traces) {  // pipeline.cpp
 }
 
 // ------------------------------------------------------------------------------- run (DOUBLE)
-RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* prompt, int n_prompt,
-                     int max_new, const dbl_pipeline_options& o) {
+namespace {
+// One sequence of a (possibly batched) DOUBLE run: PipelineState (pipeline.hpp:46-55), its lanes, its
+// datastore and its round record.
+struct Seq {
+    DeviceStore* st = nullptr;
+    std::unique_ptr<Lane> dl, tl;
+    std::unique_ptr<LaneIO> dio, tio;
+    PinBuf<RoundResult> rr_buf;
+    RoundResult* rr = nullptr;
+    RoundResult* rr_dev = nullptr;
+    std::unique_ptr<Sampled> smp;
+    std::vector<int32_t> committed, spec;
+    int n_prompt = 0, mode = 0, prev_tokens = 0;
+    long round = 0, last_committed_len = 0;
+    size_t scanned = 0;
+    bool done = false;
+    long base_lookups = 0, base_hits = 0;
+    int L = 0, nc = 0, ns = 0;  // this round
+    int64_t trows = 0;
+    RunOutput res;
+};
+}  // namespace
+
+// run (pipeline.cpp:264-323) for one or several independent sequences.  With B > 1 every draft
+// segment and every verify step is ONE forward over all active sequences (Model::forward_lanes), and
+// the per-sequence acceptance, finish_round and datastore updates are unchanged — so each sequence's
+// output, traces and metrics equal its own single-sequence run.  B = 1 issues exactly the device
+// work of the single-sequence loop.
+std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<DeviceStore*>& stores,
+                                        const std::vector<std::vector<int32_t>>& prompts, int max_new,
+                                        const dbl_pipeline_options& o) {
+    const int B = static_cast<int>(prompts.size());
+    if (B < 1 || B > kMaxBatchSeqs || static_cast<int>(stores.size()) != B)
+        throw_invalid("run: 1.." + std::to_string(kMaxBatchSeqs) + " sequences, one datastore each");
     if (max_new < 1) throw_invalid("max_new_tokens must be >= 1");
-    if (n_prompt <= 0) throw_invalid("prompt must be nonempty");
+    for (const auto& p : prompts)
+        if (p.empty()) throw_invalid("prompt must be nonempty");
     validate_opts(o);
-    if (dm.device() != st.device() || tm.device() != st.device())
-        throw_invalid("draft, target and datastore must live on the same device");
-    DeviceGuard g(st.device());
+    for (DeviceStore* st : stores)
+        if (dm.device() != st->device() || tm.device() != st->device())
+            throw_invalid("draft, target and datastore must live on the same device");
+    if (B > 1 && o.temperature != 0.0) throw_invalid("batched run: temperature > 0 is single-sequence only");
+    for (int i = 0; i < B; ++i)
+        for (int k = i + 1; k < B; ++k)
+            if (stores[i] == stores[k]) throw_invalid("batched run: every sequence needs its own datastore");
+    DeviceGuard g(stores[0]->device());
     const int d = o.depth, gamma = o.gamma;
-    const int cap = n_prompt + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
+    size_t longest = 0;
+    for (const auto& p : prompts) longest = std::max(longest, p.size());
+    const int cap = static_cast<int>(longest) + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
     Streams S;
     // draft and target run concurrently unless that would put more than two persistent forwards on
     // this GPU (tensor-parallel shards sharing it): then both workers share one stream — the round's
     // results are identical either way (frozen snapshot, pipeline.cpp:239-261)
     if (dm.persistent_grids() + tm.persistent_grids() > 2) S.target = S.draft;
-    Lane dl(dm, cap), tl(tm, cap);
-    LaneIO dio(&dl), tio(&tl);
-    PinBuf<RoundResult> rr_buf(1);
-    RoundResult* rr = rr_buf.p;
-    RoundResult* rr_dev = rr_buf.dev();
-    std::unique_ptr<Sampled> smp;
-    if (o.temperature != 0.0) {
-        if (dm.vocab() != tm.vocab()) throw_invalid("draft and target vocabularies differ");
-        smp = std::make_unique<Sampled>(o.temperature, o.rng_seed, tm.vocab(), d + 1, gamma * (d + 1),
-                                        gamma * (d + 1) + d + 2);
+
+    std::vector<Seq> seqs(B);
+    for (int b = 0; b < B; ++b) {
+        Seq& q = seqs[b];
+        q.st = stores[b];
+        q.dl = std::make_unique<Lane>(dm, cap);
+        q.tl = std::make_unique<Lane>(tm, cap);
+        q.dio = std::make_unique<LaneIO>(q.dl.get());
+        q.tio = std::make_unique<LaneIO>(q.tl.get());
+        q.rr_buf.alloc(1);
+        q.rr = q.rr_buf.p;
+        q.rr_dev = q.rr_buf.dev();
+        if (o.temperature != 0.0) {
+            if (dm.vocab() != tm.vocab()) throw_invalid("draft and target vocabularies differ");
+            q.smp = std::make_unique<Sampled>(o.temperature, o.rng_seed, tm.vocab(), d + 1, gamma * (d + 1),
+                                              gamma * (d + 1) + d + 2);
+        }
+        device_counts(*q.st, S.main, &q.base_lookups, &q.base_hits);
+        q.n_prompt = static_cast<int>(prompts[b].size());
+        q.committed = prompts[b];
+        q.prev_tokens = gamma;
+        q.last_committed_len = q.n_prompt;
+        q.scanned = q.n_prompt;
+        q.st->record(1, prompts[b].data(), q.n_prompt, S.main);  // store.record_accepted(prompt), pipeline.cpp:282
+        // lanes hold the prompt; transformers prefill KV for positions [0, P-1)
+        q.dio->sync_tokens(q.committed, S.main);
+        q.tio->sync_tokens(q.committed, S.main);
     }
-
-    long base_lookups, base_hits;
-    device_counts(st, S.main, &base_lookups, &base_hits);
-
-    std::vector<int32_t> committed(prompt, prompt + n_prompt), spec;
-    int mode = 0, prev_tokens = gamma;  // PipelineState, pipeline.hpp:46-55
-    long round = 0, last_committed_len = n_prompt;
-    st.record(1, prompt, n_prompt, S.main);  // store.record_accepted(prompt), pipeline.cpp:282
-
-    // lanes hold the prompt; transformers prefill KV for positions [0, P-1)
-    dio.sync_tokens(committed, S.main);
-    tio.sync_tokens(committed, S.main);
     Timer pre;
     CUDA_CHECK(cudaEventRecord(pre.a, S.main));
     S.fork();
-    catch_up(dl, n_prompt - 1, S.draft);
-    catch_up(tl, n_prompt - 1, S.target);
+    for (Seq& q : seqs) {
+        catch_up(*q.dl, q.n_prompt - 1, S.draft);
+        catch_up(*q.tl, q.n_prompt - 1, S.target);
+    }
     CUDA_CHECK(cudaEventRecord(S.ready, S.draft));
     CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
     CUDA_CHECK(cudaEventRecord(S.ready, S.target));
     CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
     CUDA_CHECK(cudaEventRecord(pre.b, S.main));
-    dl.set_state(n_prompt, 0, dl.kv_len, n_prompt - 1, S.main);
-    tl.set_state(n_prompt, 0, tl.kv_len, n_prompt - 1, S.main);
+    for (Seq& q : seqs) {
+        q.dl->set_state(q.n_prompt, 0, q.dl->kv_len, q.n_prompt - 1, S.main);
+        q.tl->set_state(q.n_prompt, 0, q.tl->kv_len, q.n_prompt - 1, S.main);
+    }
 
-    RunOutput res;
     Timer loop;
     CUDA_CHECK(cudaEventRecord(loop.a, S.main));
     const long long launches0 = launch_counter();
     double tfwd_ms = 0.0;
-    int64_t tfwd_n = 0, trows = 0;
+    int64_t tfwd_n = 0;
     const int32_t eos = tm.vocab() - 1;
-    size_t scanned = n_prompt;
-    bool done = false;
-    while (!done) {
-        // check_state, pipeline.cpp:208-219
-        if (mode == 0 && !spec.empty()) throw_logic("pre-verify mode with a speculative tail");
-        if (mode == 1 && prev_tokens != static_cast<int>(spec.size()))
-            throw_logic("prev_tokens out of sync with speculative tail");
-        const int nc = static_cast<int>(committed.size()), ns = static_cast<int>(spec.size());
-        const int L = nc + ns;
-        rr->draft_L0 = L;
-        rr->draft_L = L;
-        rr->n_segs = 0;
-        rr->draft_error = rr->target_error = 0;
-        if (smp) launch_derive_rngs(smp->rng.p, smp->seed, static_cast<uint64_t>(round), S.main);
+    const int c_max = o.draft_retrieval ? d : 0, tc_max = o.target_retrieval ? d : 0;
+    // one forward over the given lanes: the lane's own forward for a single lane, else batched when the
+    // rows fit one forward (<= 256), else one forward per lane
+    auto forward_set = [&](Model& m, std::vector<Lane*>& ls, const std::vector<int>& bounds, cudaStream_t s) {
+        if (ls.size() == 1) {
+            m.forward(*ls[0], bounds[0], s);
+            return;
+        }
+        int total = 0;
+        for (int v : bounds) total += v;
+        if (total <= m.max_forward_tokens() && total <= 256) {
+            m.forward_lanes(ls, total, s);
+        } else {
+            for (size_t i = 0; i < ls.size(); ++i) m.forward(*ls[i], bounds[i], s);
+        }
+    };
+    std::vector<Seq*> act;
+    for (;;) {
+        act.clear();
+        for (Seq& q : seqs)
+            if (!q.done) act.push_back(&q);
+        if (act.empty()) break;
+        for (Seq* qp : act) {
+            Seq& q = *qp;
+            // check_state, pipeline.cpp:208-219
+            if (q.mode == 0 && !q.spec.empty()) throw_logic("pre-verify mode with a speculative tail");
+            if (q.mode == 1 && q.prev_tokens != static_cast<int>(q.spec.size()))
+                throw_logic("prev_tokens out of sync with speculative tail");
+            q.nc = static_cast<int>(q.committed.size());
+            q.ns = static_cast<int>(q.spec.size());
+            q.L = q.nc + q.ns;
+            q.rr->draft_L0 = q.L;
+            q.rr->draft_L = q.L;
+            q.rr->n_segs = 0;
+            q.rr->draft_error = q.rr->target_error = 0;
+            if (q.smp) launch_derive_rngs(q.smp->rng.p, q.smp->seed, static_cast<uint64_t>(q.round), S.main);
+        }
         S.fork();
         // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
+        std::vector<Lane*> dls, tls;
+        std::vector<int> bounds;
         for (int j = 0; j < gamma; ++j) {
-            if (o.draft_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.draft);
-            const int c_max = o.draft_retrieval ? d : 0;
-            const int bound = j == 0 ? L + c_max - std::min(dl.kv_len, L - 1) : 1 + c_max;
-            if (smp) {
-                dm.dists(dl, bound, c_max + 1, smp->ddist.p, S.draft);
-                launch_draft_accept_sampled(dl, rr_dev, j, L, smp->ddist.p, smp->chain[smp->cur].p, smp->chain_rows,
-                                            smp->rng.p, smp->T, smp->dscratch.p, S.draft);
+            dls.clear();
+            bounds.clear();
+            for (Seq* qp : act) {
+                Seq& q = *qp;
+                if (o.draft_retrieval) q.st->lookup_lane(q.dl->buf.p, q.dl->state, d, S.draft);
+                dls.push_back(q.dl.get());
+                bounds.push_back(j == 0 ? q.L + c_max - std::min(q.dl->kv_len, q.L - 1) : 1 + c_max);
+            }
+            if (act.size() == 1 && act[0]->smp) {
+                Seq& q = *act[0];
+                Sampled& sm = *q.smp;
+                dm.dists(*q.dl, bounds[0], c_max + 1, sm.ddist.p, S.draft);
+                launch_draft_accept_sampled(*q.dl, q.rr_dev, j, q.L, sm.ddist.p, sm.chain[sm.cur].p, sm.chain_rows,
+                                            sm.rng.p, sm.T, sm.dscratch.p, S.draft);
             } else {
-                dm.forward(dl, bound, S.draft);
-                launch_draft_accept(dl, rr_dev, j, S.draft);
+                forward_set(dm, dls, bounds, S.draft);
+                for (Seq* qp : act) launch_draft_accept(*qp->dl, qp->rr_dev, j, S.draft);
             }
         }
         // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
-        if (o.target_retrieval) st.lookup_lane(tl.buf.p, tl.state, d, S.target);
+        bounds.clear();
+        for (Seq* qp : act) {
+            Seq& q = *qp;
+            if (o.target_retrieval) q.st->lookup_lane(q.tl->buf.p, q.tl->state, d, S.target);
+            tls.push_back(q.tl.get());
+            bounds.push_back(q.L + tc_max - std::min(q.tl->kv_len, q.nc - 1));
+        }
         CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
-        const int tc_max = o.target_retrieval ? d : 0;
-        const int tbound = L + tc_max - std::min(tl.kv_len, nc - 1);
-        if (smp) {
+        if (act.size() == 1 && act[0]->smp) {
             // verify forward + finish_round's verification (rng_v) + the target's own acceptance (rng_t)
-            tm.dists(tl, tbound, ns + tc_max + 1, smp->tdist.p, S.target);
+            Seq& q = *act[0];
+            Sampled& sm = *q.smp;
+            tm.dists(*q.tl, bounds[0], q.ns + tc_max + 1, sm.tdist.p, S.target);
             CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
-            launch_target_accept_sampled(tl, nc, rr_dev, smp->tdist.p, smp->spec_probs, smp->rng.p + 1,
-                                         smp->rng.p + 2, smp->T, false, smp->tscratch.p, S.target);
+            launch_target_accept_sampled(*q.tl, q.nc, q.rr_dev, sm.tdist.p, sm.spec_probs, sm.rng.p + 1,
+                                         sm.rng.p + 2, sm.T, false, sm.tscratch.p, S.target);
         } else {
-            tm.forward(tl, tbound, S.target);
+            forward_set(tm, tls, bounds, S.target);
             CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
-            launch_target_accept(tl, nc, rr_dev, S.target);
+            for (Seq* qp : act) launch_target_accept(*qp->tl, qp->nc, qp->rr_dev, S.target);
         }
         CUDA_CHECK(cudaStreamSynchronize(S.draft));
         CUDA_CHECK(cudaStreamSynchronize(S.target));
@@ -430,153 +516,178 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
             tfwd_ms += ms;
             ++tfwd_n;
         }
-        if ((rr->draft_error || rr->target_error) && std::getenv("DBL_DEBUG_ROUND"))
-            std::fprintf(stderr, "dbl round %ld: draft_error %d target_error %d L %d nc %d ns %d n_segs %d draft_L %d ext_c %d\n",
-                         round, rr->draft_error, rr->target_error, L, nc, ns, rr->n_segs, rr->draft_L, rr->ext_c);
-        check_round_errors(rr);
-        const int c_t = rr->ext_c;
-        trows += L + c_t - (nc - 1);
 
-        // ---- finish_round (pipeline.cpp:91-206)
-        const int n_chain = rr->draft_L - rr->draft_L0;
-        const int32_t* chain = rr->draft_tokens;
-        const int ne = rr->ext_matched + 1;
-        const int32_t* ext = rr->ext_emitted;
-        Trace tr;
-        tr.round = round;
-        tr.mode = mode ? "post_verify" : "pre_verify";
-        tr.pending = ns;
-        tr.draft_len = n_chain;
-        if (o.draft_retrieval)
-            for (int j = 0; j < rr->n_segs; ++j) tr.draft_matched.push_back(rr->segs[j].matched);
-        tr.target_matched = o.target_retrieval ? rr->ext_matched : -1;
-        tr.target_source = source_name(rr->ext_source);
+        for (Seq* qp : act) {
+            Seq& q = *qp;
+            RoundResult* rr = q.rr;
+            DeviceStore& st = *q.st;
+            Lane& dl = *q.dl;
+            Lane& tl = *q.tl;
+            Sampled* smp = q.smp.get();
+            const int L = q.L, nc = q.nc, ns = q.ns;
+            if ((rr->draft_error || rr->target_error) && std::getenv("DBL_DEBUG_ROUND"))
+                std::fprintf(stderr, "dbl round %ld: draft_error %d target_error %d L %d nc %d ns %d n_segs %d draft_L %d ext_c %d\n",
+                             q.round, rr->draft_error, rr->target_error, L, nc, ns, rr->n_segs, rr->draft_L, rr->ext_c);
+            check_round_errors(rr);
+            const int c_t = rr->ext_c;
+            q.trows += L + c_t - (nc - 1);
 
-        const std::vector<int32_t> committed_before = committed;
-        std::vector<int32_t> add, new_spec;
-        if (smp) smp->spec_probs = nullptr;
-        if (rr->tgt_rej >= 0) {
-            const int k = rr->tgt_rej;
-            tr.accepted_pending = k;
-            tr.pending_reject = tr.rejected = true;
-            tr.kind = "pending_reject";
-            add.assign(spec.begin(), spec.begin() + k);
-            add.push_back(rr->tgt_correction);
-            std::vector<int32_t> pre_k = committed_before;
-            pre_k.insert(pre_k.end(), spec.begin(), spec.begin() + k);
-            record_run(st, 2, pre_k, spec.data() + k, spec.size() - k, S.main);
-            std::vector<int32_t> pre_d = committed_before;
-            pre_d.insert(pre_d.end(), spec.begin(), spec.end());
-            record_run(st, 2, pre_d, chain, n_chain, S.main);
-        } else {
-            tr.accepted_pending = ns;
-            add = spec;
-            add.insert(add.end(), ext, ext + ne);
-            const int cmp = std::min(n_chain, ne);
-            int j = 0;
-            while (j < cmp && chain[j] == ext[j]) ++j;
-            if (j == ne && n_chain > ne) {
-                tr.kind = "extend_keep_draft";
-                new_spec.assign(chain + ne, chain + n_chain);
-                if (smp) {  // new_spec_probs = chain.probs[ne:] (pipeline.cpp:168-169)
-                    smp->spec_probs = smp->chain[smp->cur].p + static_cast<size_t>(ne) * smp->V;
-                    smp->cur ^= 1;
-                }
-            } else if (j == cmp) {
-                tr.kind = "extend_draft_subsumed";
+            // ---- finish_round (pipeline.cpp:91-206)
+            const int n_chain = rr->draft_L - rr->draft_L0;
+            const int32_t* chain = rr->draft_tokens;
+            const int ne = rr->ext_matched + 1;
+            const int32_t* ext = rr->ext_emitted;
+            Trace tr;
+            tr.round = q.round;
+            tr.mode = q.mode ? "post_verify" : "pre_verify";
+            tr.pending = ns;
+            tr.draft_len = n_chain;
+            if (o.draft_retrieval)
+                for (int j = 0; j < rr->n_segs; ++j) tr.draft_matched.push_back(rr->segs[j].matched);
+            tr.target_matched = o.target_retrieval ? rr->ext_matched : -1;
+            tr.target_source = source_name(rr->ext_source);
+
+            const std::vector<int32_t> committed_before = q.committed;
+            std::vector<int32_t> add, new_spec;
+            const std::vector<int32_t>& spec = q.spec;
+            if (smp) smp->spec_probs = nullptr;
+            if (rr->tgt_rej >= 0) {
+                const int k = rr->tgt_rej;
+                tr.accepted_pending = k;
+                tr.pending_reject = tr.rejected = true;
+                tr.kind = "pending_reject";
+                add.assign(spec.begin(), spec.begin() + k);
+                add.push_back(rr->tgt_correction);
+                std::vector<int32_t> pre_k = committed_before;
+                pre_k.insert(pre_k.end(), spec.begin(), spec.begin() + k);
+                record_run(st, 2, pre_k, spec.data() + k, spec.size() - k, S.main);
+                std::vector<int32_t> pre_d = committed_before;
+                pre_d.insert(pre_d.end(), spec.begin(), spec.end());
+                record_run(st, 2, pre_d, chain, n_chain, S.main);
             } else {
-                tr.kind = "extend_drop_draft";
-                tr.rejected = true;
-                std::vector<int32_t> pre_j = committed_before;
-                pre_j.insert(pre_j.end(), spec.begin(), spec.end());
-                pre_j.insert(pre_j.end(), chain, chain + j);
-                record_run(st, 2, pre_j, chain + j, n_chain - j, S.main);
+                tr.accepted_pending = ns;
+                add = spec;
+                add.insert(add.end(), ext, ext + ne);
+                const int cmp = std::min(n_chain, ne);
+                int j = 0;
+                while (j < cmp && chain[j] == ext[j]) ++j;
+                if (j == ne && n_chain > ne) {
+                    tr.kind = "extend_keep_draft";
+                    new_spec.assign(chain + ne, chain + n_chain);
+                    if (smp) {  // new_spec_probs = chain.probs[ne:] (pipeline.cpp:168-169)
+                        smp->spec_probs = smp->chain[smp->cur].p + static_cast<size_t>(ne) * smp->V;
+                        smp->cur ^= 1;
+                    }
+                } else if (j == cmp) {
+                    tr.kind = "extend_draft_subsumed";
+                } else {
+                    tr.kind = "extend_drop_draft";
+                    tr.rejected = true;
+                    std::vector<int32_t> pre_j = committed_before;
+                    pre_j.insert(pre_j.end(), spec.begin(), spec.end());
+                    pre_j.insert(pre_j.end(), chain, chain + j);
+                    record_run(st, 2, pre_j, chain + j, n_chain - j, S.main);
+                }
             }
-        }
-        tr.committed_count = static_cast<int>(add.size());
-        record_run(st, 1, committed_before, add.data(), add.size(), S.main);
-        committed.insert(committed.end(), add.begin(), add.end());
-        // rollback(state, |committed|) (pipeline.cpp:15-30)
-        if (static_cast<long>(committed.size()) < last_committed_len)
-            throw_logic("rollback: keep_len below committed boundary");
-        spec = std::move(new_spec);
-        mode = spec.empty() ? 0 : 1;
-        prev_tokens = spec.empty() ? gamma : static_cast<int>(spec.size());
-        last_committed_len = static_cast<long>(committed.size());
-        ++round;
-        const double draft_time = gamma * (o.t_draft + (o.draft_retrieval ? o.t_lookup : 0.0));
-        const double target_time = o.t_target + (o.target_retrieval ? o.t_lookup : 0.0);
-        tr.clock_delta = std::max(draft_time, target_time) + o.t_sync;
-        res.traces.push_back(std::move(tr));
-        {  // decision log (see RunOutput::log)
-            auto& lg = res.log;
-            lg.push_back(rr->n_segs);
-            int at = 0;
-            for (int j = 0; j < rr->n_segs; ++j) {
-                lg.push_back(rr->segs[j].matched);
-                lg.insert(lg.end(), chain + at, chain + at + rr->segs[j].n_emit);
-                at += rr->segs[j].n_emit;
+            tr.committed_count = static_cast<int>(add.size());
+            record_run(st, 1, committed_before, add.data(), add.size(), S.main);
+            q.committed.insert(q.committed.end(), add.begin(), add.end());
+            // rollback(state, |committed|) (pipeline.cpp:15-30)
+            if (static_cast<long>(q.committed.size()) < q.last_committed_len)
+                throw_logic("rollback: keep_len below committed boundary");
+            q.spec = std::move(new_spec);
+            q.mode = q.spec.empty() ? 0 : 1;
+            q.prev_tokens = q.spec.empty() ? gamma : static_cast<int>(q.spec.size());
+            q.last_committed_len = static_cast<long>(q.committed.size());
+            ++q.round;
+            const double draft_time = gamma * (o.t_draft + (o.draft_retrieval ? o.t_lookup : 0.0));
+            const double target_time = o.t_target + (o.target_retrieval ? o.t_lookup : 0.0);
+            tr.clock_delta = std::max(draft_time, target_time) + o.t_sync;
+            q.res.traces.push_back(std::move(tr));
+            {  // decision log (see RunOutput::log)
+                auto& lg = q.res.log;
+                lg.push_back(rr->n_segs);
+                int at = 0;
+                for (int j = 0; j < rr->n_segs; ++j) {
+                    lg.push_back(rr->segs[j].matched);
+                    lg.insert(lg.end(), chain + at, chain + at + rr->segs[j].n_emit);
+                    at += rr->segs[j].n_emit;
+                }
+                lg.push_back(ns);
+                lg.push_back(rr->tgt_rej);
+                lg.push_back(rr->tgt_correction);
+                lg.push_back(rr->ext_matched);
+                lg.insert(lg.end(), ext, ext + ne);
             }
-            lg.push_back(ns);
-            lg.push_back(rr->tgt_rej);
-            lg.push_back(rr->tgt_correction);
-            lg.push_back(rr->ext_matched);
-            lg.insert(lg.end(), ext, ext + ne);
-        }
 
-        // ---- lane cursors for the next round (KV commit by length)
-        std::vector<int32_t> X = committed;
-        X.insert(X.end(), spec.begin(), spec.end());
-        {
-            // the draft lane holds committed_before ⊕ spec ⊕ chain; KV valid below its last token
-            dl.mirror.resize(L);
-            dl.mirror.insert(dl.mirror.end(), chain, chain + n_chain);
-            const int dev_kv = L + n_chain - 1;
-            const int lcp = dio.sync_tokens(X, S.main);
-            dl.kv_len = std::min(dev_kv, lcp);
-            dl.set_state(static_cast<int>(X.size()), 0, dl.kv_len, static_cast<int>(X.size()) - 1, S.main);
-        }
-        {
-            tl.mirror.resize(L);
-            tl.mirror.insert(tl.mirror.end(), rr->ext_cands, rr->ext_cands + c_t);
-            const int dev_kv = L + c_t;
-            const int lcp = tio.sync_tokens(X, S.main);
-            tl.kv_len = std::min(dev_kv, lcp);
-            tl.set_state(static_cast<int>(X.size()), 0, tl.kv_len,
-                         static_cast<int>(committed.size()) - 1, S.main);
-        }
-
-        // ---- EOS / budget (pipeline.cpp:290-306)
-        for (; scanned < committed.size(); ++scanned) {
-            if (committed[scanned] == eos) {
-                committed.resize(scanned + 1);
-                done = true;
-                break;
+            // ---- lane cursors for the next round (KV commit by length)
+            std::vector<int32_t> X = q.committed;
+            X.insert(X.end(), q.spec.begin(), q.spec.end());
+            {
+                // the draft lane holds committed_before ⊕ spec ⊕ chain; KV valid below its last token
+                dl.mirror.resize(L);
+                dl.mirror.insert(dl.mirror.end(), chain, chain + n_chain);
+                const int dev_kv = L + n_chain - 1;
+                const int lcp = q.dio->sync_tokens(X, S.main);
+                dl.kv_len = std::min(dev_kv, lcp);
+                dl.set_state(static_cast<int>(X.size()), 0, dl.kv_len, static_cast<int>(X.size()) - 1, S.main);
             }
+            {
+                tl.mirror.resize(L);
+                tl.mirror.insert(tl.mirror.end(), rr->ext_cands, rr->ext_cands + c_t);
+                const int dev_kv = L + c_t;
+                const int lcp = q.tio->sync_tokens(X, S.main);
+                tl.kv_len = std::min(dev_kv, lcp);
+                tl.set_state(static_cast<int>(X.size()), 0, tl.kv_len,
+                             static_cast<int>(q.committed.size()) - 1, S.main);
+            }
+
+            // ---- EOS / budget (pipeline.cpp:290-306)
+            for (; q.scanned < q.committed.size(); ++q.scanned) {
+                if (q.committed[q.scanned] == eos) {
+                    q.committed.resize(q.scanned + 1);
+                    q.done = true;
+                    break;
+                }
+            }
+            if (q.committed.size() - static_cast<size_t>(q.n_prompt) >= static_cast<size_t>(max_new)) q.done = true;
+            if (q.round > 1000000) throw_runtime("round limit exceeded; pipeline stalled");
         }
-        if (committed.size() - static_cast<size_t>(n_prompt) >= static_cast<size_t>(max_new)) done = true;
-        if (round > 1000000) throw_runtime("round limit exceeded; pipeline stalled");
     }
     CUDA_CHECK(cudaEventRecord(loop.b, S.main));
     CUDA_CHECK(cudaStreamSynchronize(S.main));
 
-    finish_output(committed, n_prompt, max_new, res);
-    compute_metrics(res.traces, o.t_target, &res.metrics);
-    long lk, hits;
-    device_counts(st, S.main, &lk, &hits);
-    res.metrics.lookups = lk - base_lookups;
-    res.metrics.hit_rate = res.metrics.lookups == 0
-                               ? 0.0
-                               : static_cast<double>(hits - base_hits) / static_cast<double>(res.metrics.lookups);
-    res.metrics.device_ms = loop.ms();
-    res.metrics.kernel_launches = launch_counter() - launches0;
-    res.metrics.prefill_ms = pre.ms();
-    res.metrics.target_fwd_ms = tfwd_ms;
-    res.metrics.target_fwd_count = tfwd_n;
-    res.metrics.target_rows = trows;
-    st.flush_session(S.main);  // pipeline.cpp:321
+    std::vector<RunOutput> out;
+    for (Seq& q : seqs) {
+        RunOutput& res = q.res;
+        finish_output(q.committed, q.n_prompt, max_new, res);
+        compute_metrics(res.traces, o.t_target, &res.metrics);
+        long lk, hits;
+        device_counts(*q.st, S.main, &lk, &hits);
+        res.metrics.lookups = lk - q.base_lookups;
+        res.metrics.hit_rate = res.metrics.lookups == 0
+                                   ? 0.0
+                                   : static_cast<double>(hits - q.base_hits) / static_cast<double>(res.metrics.lookups);
+        res.metrics.device_ms = loop.ms();
+        res.metrics.kernel_launches = launch_counter() - launches0;
+        res.metrics.prefill_ms = pre.ms();
+        res.metrics.target_fwd_ms = tfwd_ms;
+        res.metrics.target_fwd_count = tfwd_n;
+        res.metrics.target_rows = q.trows;
+        q.st->flush_session(S.main);  // pipeline.cpp:321
+        out.push_back(std::move(res));
+    }
     CUDA_CHECK(cudaStreamSynchronize(S.main));
-    return res;
+    return out;
+}
+
+RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* prompt, int n_prompt, int max_new,
+                     const dbl_pipeline_options& o) {
+    if (max_new < 1) throw_invalid("max_new_tokens must be >= 1");
+    if (n_prompt <= 0) throw_invalid("prompt must be nonempty");
+    std::vector<RunOutput> r = run_double_multi(dm, tm, {&st}, {std::vector<int32_t>(prompt, prompt + n_prompt)},
+                                                max_new, o);
+    return std::move(r[0]);
 }
 
 // ----------------------------------------------------------------------------------- run (AR)

@@ -9,6 +9,8 @@
 
 namespace dbl {
 
+constexpr int kMaxBatchSeqs = 16;  // sequences per batched forward (FwdBatch, fwd.cuh)
+
 struct Trace {  // RoundTrace, pipeline.hpp:57-71
     long round = 0;
     std::string mode;
@@ -39,10 +41,13 @@ void compute_metrics(const std::vector<Trace>& traces, double t_target, dbl_run_
 
 RunOutput run_double(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
                      int n_prompt, int max_new, const dbl_pipeline_options& o);
+// run for up to kMaxBatchSeqs independent sequences (one datastore each) with batched forwards
+std::vector<RunOutput> run_double_multi(Model& draft, Model& target, const std::vector<DeviceStore*>& stores,
+                                        const std::vector<std::vector<int32_t>>& prompts, int max_new,
+                                        const dbl_pipeline_options& o);
 RunOutput run_ar(Model& target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                  double temperature, uint64_t seed);
 // run_vanilla_ar for up to kMaxBatchSeqs sequences in lockstep, one batched forward per step
-constexpr int kMaxBatchSeqs = 16;
 std::vector<RunOutput> run_ar_batch(Model& target, const std::vector<std::vector<int32_t>>& prompts, int max_new,
                                     double t_target, double* device_ms, long long* launches);
 RunOutput run_serial_sd(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,

@@ -33,7 +33,7 @@ PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
 __all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
-           "run_vanilla_ar", "run_vanilla_ar_batch",
+           "run_vanilla_ar", "run_vanilla_ar_batch", "run_batch",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
            "parse_model_v1", "parse_dstore_v1", "serialize_model", "serialize_index", "save_model",
            "load_model", "save_index", "load_index"]
@@ -515,6 +515,39 @@ def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float 
                                   float(temperature), C.c_uint64(int(rng_seed)), _p32(out), cap, C.byref(n),
                                   C.byref(m), js, len(js) if js is not None else 0, C.byref(jl))
     return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+def run_batch(draft: _Model, target: _Model, stores, prompts, max_new_tokens: int,
+              opts: PipelineOptions | None = None, want_jsonl: bool = True):
+    """Batched DOUBLE: run() for several independent sequences — one datastore each —
+    sharing every draft-segment and verify forward.  Returns one RunResult per sequence, each equal to
+    that sequence's own run()."""
+    import json
+    opts = opts or PipelineOptions()
+    ps = [_i32(p) for p in prompts]
+    B = len(ps)
+    off = np.zeros(B + 1, np.int64)
+    off[1:] = np.cumsum([len(p) for p in ps])
+    toks = np.concatenate(ps) if ps else np.zeros(1, np.int32)
+    n = max(int(max_new_tokens), 1)
+    out = np.zeros(B * n, np.int32)
+    out_n = np.zeros(max(B, 1), np.int32)
+    mets = (RunMetrics * max(B, 1))()
+    hs = (C.c_void_p * max(B, 1))(*[s._h.value if isinstance(s._h, C.c_void_p) else s._h for s in stores])
+    js = C.create_string_buffer(B * max(1 << 16, 512 * (n + 8))) if want_jsonl else None
+    jl = np.zeros(max(B, 1), np.int64)
+    o = opts._c()
+    check(lib().dbl_run_batch(draft._h, target._h, B, hs, off.ctypes.data_as(C.POINTER(C.c_int64)), _p32(toks),
+                              int(max_new_tokens), C.byref(o), _p32(out), _p32(out_n), mets, js,
+                              len(js) if js is not None else 0, jl.ctypes.data_as(C.POINTER(C.c_int64))))
+    res, at = [], 0
+    raw = js.raw if want_jsonl else b""
+    for b in range(B):
+        text = raw[at:at + jl[b]].decode() if want_jsonl else ""
+        at += int(jl[b])
+        res.append(RunResult(out[b * n: b * n + out_n[b]].tolist(), mets[b].as_dict(), text,
+                             [json.loads(x) for x in text.splitlines()] if want_jsonl else []))
+    return res
 
 
 def run_vanilla_ar_batch(target: _Model, prompts, max_new_tokens: int):

@@ -37,3 +37,65 @@ def test_batched_ar_limits(dbl):
         dbl.run_vanilla_ar_batch(m, [[1, 2]] * 17, 4)
     with pytest.raises(dbl.InvalidArgument):
         dbl.run_vanilla_ar_batch(m, [[1, 2], []], 4)
+
+
+KEYS = ("tokens", "rounds", "clock", "m", "amt", "speedup", "hit_rate", "lookups")
+
+
+def _prior(vocab, seed, n=6):
+    rng = random.Random(seed)
+    base = [rng.randrange(1, vocab - 1) for _ in range(40)]
+    out = []
+    for _ in range(n):
+        s = []
+        while len(s) < 48:
+            s += base[rng.randrange(0, 30):][: rng.randrange(4, 12)] if rng.random() < 0.7 else \
+                [rng.randrange(1, vocab - 1) for _ in range(3)]
+        out.append(s[:48])
+    return out
+
+
+def _check_batch_equals_single(dbl, drf, tgt, prior, prompts, n, opts):
+    def store():
+        st = dbl.HierarchicalDatastore(3, opts.depth)
+        dbl.build_prior(st, prior, len(prior))
+        return st
+    batch = dbl.run_batch(drf, tgt, [store() for _ in prompts], prompts, n, opts)
+    for p, r in zip(prompts, batch):
+        one = dbl.run(drf, tgt, store(), p, n, opts)
+        assert r.output == one.output
+        assert r.jsonl == one.jsonl
+        assert [r.metrics[k] for k in KEYS] == [one.metrics[k] for k in KEYS]
+
+
+def test_batched_double_equals_single_runs_tables(dbl):
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_2601_05524_b200.specpar import parse_dstore_v1
+    d = dbl.TableModel.from_model_v1(open(os.path.join(GOLDEN, "config1_draft.model-v1")).read())
+    t = dbl.TableModel.from_model_v1(open(os.path.join(GOLDEN, "config1_target.model-v1")).read())
+    _, seqs = parse_dstore_v1(open(os.path.join(GOLDEN, "config1_prior.dstore-v1")).read())
+    base = json.load(open(os.path.join(GOLDEN, "config1.json")))["prompt"]
+    prompts = [base, base[:5], seqs[3][:12], seqs[7][:3]]
+    _check_batch_equals_single(dbl, d, t, seqs, prompts, 96,
+                               dbl.PipelineOptions(gamma=2, depth=10, t_draft=0.625))
+
+
+@pytest.mark.parametrize("gamma", [1, 3])
+def test_batched_double_equals_single_runs_transformers(dbl, gamma):
+    tgt = dbl.Transformer(dbl.transformer_config("tiny-qwen", seed=11, max_seq=2048))
+    drf = dbl.Transformer(dbl.transformer_config("tiny-qwen-draft", seed=12, max_seq=2048))
+    prior = _prior(tgt.cfg.vocab, 4)
+    prompts = [prior[0][:24], prior[1][:9], prior[2][:40], [5, 6, 7]]
+    _check_batch_equals_single(dbl, drf, tgt, prior, prompts, 64, dbl.PipelineOptions(gamma=gamma, depth=10))
+
+
+def test_batched_double_limits(dbl):
+    tgt = dbl.Transformer(dbl.transformer_config("tiny-qwen", seed=1, max_seq=512))
+    st = dbl.HierarchicalDatastore(3, 10)
+    with pytest.raises(dbl.InvalidArgument):  # one datastore per sequence
+        dbl.run_batch(tgt, tgt, [st, st], [[1, 2], [3, 4]], 4)
+    with pytest.raises(dbl.InvalidArgument):  # sampled batches are not supported
+        dbl.run_batch(tgt, tgt, [st, dbl.HierarchicalDatastore(3, 10)], [[1, 2], [3, 4]], 4,
+                      dbl.PipelineOptions(temperature=1.0))
