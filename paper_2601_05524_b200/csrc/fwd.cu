@@ -163,87 +163,17 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// One (token, q head, 64-key chunk) of split-KV causal attention, one warp.  Scores: lane = key
-// (all of the key row's loads in flight at once); P*V: lane = HD/32 contiguous dims.  Chunks of a
-// position combine in chunk order (the last-arriving warp does it), so the result depends on the
-// position only — never on how many tokens the forward carries.
+// One (q head, 64-key chunk) of split-KV causal attention for up to two consecutive tokens of one
+// sequence, one warp: the chunk's K and V rows are loaded once for both.  Scores: lane = key (the
+// whole key row's loads in flight at once); P*V: lane = HD/32 contiguous dims.  Each token keeps its
+// own causal limit, softmax and partial; chunks of a position combine in chunk order (the
+// last-arriving warp does it), so the result depends on the position only — never on how many
+// tokens the forward carries or how they are paired.
 template <int HD>
-__device__ __forceinline__ void attn_item(const FwdArgs& a, int t, int hq, int j, int pos, const int32_t* page_table,
-                                          const __nv_bfloat16* kc, const __nv_bfloat16* vc, float* q_s, float* p_s,
-                                          int lane) {
+__device__ __forceinline__ void attn_token_out(const FwdArgs& a, int t, int hq, int j, int nch, const float (&o)[HD / 32],
+                                               float mx, float l, int lane) {
     constexpr int DPL = HD / 32;
-    const int nh = a.nh, kvh = hq / (nh / a.nkv);
-    const int k0 = j * kAttnChunk;
-    const int nch = pos / kAttnChunk + 1, nk = min(kAttnChunk, pos - k0 + 1);
-    const long long page = page_table[j];
-    const __nv_bfloat16* kp = kc + (page * a.nkv + kvh) * kPage * HD;
-    const __nv_bfloat16* vp = vc + (page * a.nkv + kvh) * kPage * HD;
-    const __nv_bfloat16* qs = a.qbuf + (static_cast<long long>(t) * nh + hq) * HD;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) q_s[lane * DPL + e] = __bfloat162float(qs[lane * DPL + e]);
-    __syncwarp();
-    const float scale = rsqrtf(static_cast<float>(HD));
-    float sc[2];
-#pragma unroll 1
-    for (int h2 = 0; h2 < 2; ++h2) {
-        const int kk = lane + 32 * h2;
-        sc[h2] = -INFINITY;
-        if (kk < nk) {
-            const uint4* kr = reinterpret_cast<const uint4*>(kp + static_cast<long long>(kk) * HD);
-            float acc = 0.f;
-#pragma unroll
-            for (int hh = 0; hh < HD / 64; ++hh) {  // 128-byte halves of the row: 8 loads in flight
-                uint4 w[8];
-#pragma unroll
-                for (int d8 = 0; d8 < 8; ++d8) w[d8] = kr[hh * 8 + d8];
-#pragma unroll
-                for (int d8 = 0; d8 < 8; ++d8) {
-                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w[d8]);
-#pragma unroll
-                    for (int e2 = 0; e2 < 4; ++e2) {
-                        const float2 kf = __bfloat1622float2(b2[e2]);
-                        acc = fmaf(q_s[(hh * 8 + d8) * 8 + 2 * e2], kf.x, acc);
-                        acc = fmaf(q_s[(hh * 8 + d8) * 8 + 2 * e2 + 1], kf.y, acc);
-                    }
-                }
-            }
-            sc[h2] = acc * scale;
-        }
-    }
-    float mx = fmaxf(sc[0], sc[1]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    const float e0 = lane < nk ? __expf(sc[0] - mx) : 0.f, e1 = lane + 32 < nk ? __expf(sc[1] - mx) : 0.f;
-    p_s[lane] = e0;
-    p_s[lane + 32] = e1;
-    float l = e0 + e1;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-    __syncwarp();
-    float o[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) o[e] = 0.f;
-    const __nv_bfloat16* vl = vp + lane * DPL;
-    using VT = typename std::conditional<DPL == 4, uint2, uint32_t>::type;  // this lane's DPL bf16 of a row
-#pragma unroll 1
-    for (int i0 = 0; i0 < nk; i0 += kVRows) {  // kVRows V rows in flight per round trip
-        VT raw[kVRows];
-#pragma unroll
-        for (int i = 0; i < kVRows; ++i)
-            if (i0 + i < nk) raw[i] = *reinterpret_cast<const VT*>(vl + static_cast<long long>(i0 + i) * HD);
-#pragma unroll
-        for (int i = 0; i < kVRows; ++i) {
-            if (i0 + i >= nk) break;
-            const float pi = p_s[i0 + i];
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
-#pragma unroll
-            for (int e2 = 0; e2 < DPL / 2; ++e2) {
-                const float2 vf = __bfloat1622float2(b2[e2]);
-                o[2 * e2] = fmaf(pi, vf.x, o[2 * e2]);
-                o[2 * e2 + 1] = fmaf(pi, vf.y, o[2 * e2 + 1]);
-            }
-        }
-    }
+    const int nh = a.nh;
     __nv_bfloat16* out = a.attn + static_cast<long long>(t) * a.q_dim + hq * HD + lane * DPL;
     if (nch == 1) {
         const float inv = 1.0f / l;
@@ -286,11 +216,119 @@ __device__ __forceinline__ void attn_item(const FwdArgs& a, int t, int hq, int j
     for (int e = 0; e < DPL; ++e) out[e] = __float2bfloat16_rn(acc[e] * inv);
 }
 
+template <int HD, int NT>  // NT = 1: one token; NT = 2: up to two consecutive tokens
+__device__ __forceinline__ void attn_item(const FwdArgs& a, int t0, int nt, int hq, int j, int pos0,
+                                          const int32_t* page_table, const __nv_bfloat16* kc,
+                                          const __nv_bfloat16* vc, float* q_s, float* p_s, int lane) {
+    constexpr int DPL = HD / 32;
+    const int nh = a.nh, kvh = hq / (nh / a.nkv);
+    const int k0 = j * kAttnChunk;
+    // token tt sits at pos0 + tt and sees keys [k0, k0 + nk[tt]) of this chunk (nk <= 0: none)
+    const int nk0 = min(kAttnChunk, pos0 - k0 + 1);
+    const int nk1 = NT > 1 && nt > 1 ? min(kAttnChunk, pos0 + 1 - k0 + 1) : 0;
+    const int nk = max(nk0, nk1);
+    const long long page = page_table[j];
+    const __nv_bfloat16* kp = kc + (page * a.nkv + kvh) * kPage * HD;
+    const __nv_bfloat16* vp = vc + (page * a.nkv + kvh) * kPage * HD;
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        if (tt < nt) {
+            const __nv_bfloat16* qs = a.qbuf + (static_cast<long long>(t0 + tt) * nh + hq) * HD;
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) q_s[tt * HD + lane * DPL + e] = __bfloat162float(qs[lane * DPL + e]);
+        }
+    }
+    __syncwarp();
+    const float scale = rsqrtf(static_cast<float>(HD));
+    float sa[2], sb[2];  // scores of key lane / lane + 32 for tokens 0 and 1
+#pragma unroll 1
+    for (int h2 = 0; h2 < 2; ++h2) {
+        const int kk = lane + 32 * h2;
+        float acc0 = 0.f, acc1 = 0.f;
+        if (kk < nk) {
+            const uint4* kr = reinterpret_cast<const uint4*>(kp + static_cast<long long>(kk) * HD);
+#pragma unroll
+            for (int hh = 0; hh < HD / 64; ++hh) {  // 128-byte halves of the row: 8 loads in flight
+                uint4 w[8];
+#pragma unroll
+                for (int d8 = 0; d8 < 8; ++d8) w[d8] = kr[hh * 8 + d8];
+#pragma unroll
+                for (int d8 = 0; d8 < 8; ++d8) {
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w[d8]);
+#pragma unroll
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const float2 kf = __bfloat1622float2(b2[e2]);
+                        const int d = (hh * 8 + d8) * 8 + 2 * e2;
+                        acc0 = fmaf(q_s[d], kf.x, acc0);
+                        acc0 = fmaf(q_s[d + 1], kf.y, acc0);
+                        if constexpr (NT > 1) {
+                            acc1 = fmaf(q_s[HD + d], kf.x, acc1);
+                            acc1 = fmaf(q_s[HD + d + 1], kf.y, acc1);
+                        }
+                    }
+                }
+            }
+        }
+        const float s0 = kk < nk0 ? acc0 * scale : -INFINITY, s1 = kk < nk1 ? acc1 * scale : -INFINITY;
+        if (h2 == 0) { sa[0] = s0; sa[1] = s1; } else { sb[0] = s0; sb[1] = s1; }
+    }
+    float mx[2], l[2];
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        const int ntk = tt == 0 ? nk0 : nk1;
+        float m = fmaxf(sa[tt], sb[tt]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        const float e0 = lane < ntk ? __expf(sa[tt] - m) : 0.f, e1 = lane + 32 < ntk ? __expf(sb[tt] - m) : 0.f;
+        p_s[tt * kAttnChunk + lane] = e0;
+        p_s[tt * kAttnChunk + lane + 32] = e1;
+        float s2 = e0 + e1;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+        mx[tt] = m;
+        l[tt] = s2;
+    }
+    __syncwarp();
+    float o0[DPL], o1[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL; ++e) o0[e] = o1[e] = 0.f;
+    const __nv_bfloat16* vl = vp + lane * DPL;
+    using VT = typename std::conditional<DPL == 4, uint2, uint32_t>::type;  // this lane's DPL bf16 of a row
+#pragma unroll 1
+    for (int i0 = 0; i0 < nk; i0 += kVRows) {  // kVRows V rows in flight per round trip
+        VT raw[kVRows];
+#pragma unroll
+        for (int i = 0; i < kVRows; ++i)
+            if (i0 + i < nk) raw[i] = *reinterpret_cast<const VT*>(vl + static_cast<long long>(i0 + i) * HD);
+#pragma unroll
+        for (int i = 0; i < kVRows; ++i) {
+            if (i0 + i >= nk) break;
+            const float p0 = p_s[i0 + i];  // 0 beyond a token's limit
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
+#pragma unroll
+            for (int e2 = 0; e2 < DPL / 2; ++e2) {
+                const float2 vf = __bfloat1622float2(b2[e2]);
+                o0[2 * e2] = fmaf(p0, vf.x, o0[2 * e2]);
+                o0[2 * e2 + 1] = fmaf(p0, vf.y, o0[2 * e2 + 1]);
+                if constexpr (NT > 1) {
+                    const float p1 = p_s[kAttnChunk + i0 + i];
+                    o1[2 * e2] = fmaf(p1, vf.x, o1[2 * e2]);
+                    o1[2 * e2 + 1] = fmaf(p1, vf.y, o1[2 * e2 + 1]);
+                }
+            }
+        }
+    }
+    if (nk0 > 0) attn_token_out<HD>(a, t0, hq, j, pos0 / kAttnChunk + 1, o0, mx[0], l[0], lane);
+    if constexpr (NT > 1)
+        if (nk1 > 0) attn_token_out<HD>(a, t0 + 1, hq, j, (pos0 + 1) / kAttnChunk + 1, o1, mx[1], l[1], lane);
+}
+
 struct BatchSmem {  // a batched forward's row -> lane map (the per-lane pointers stay in the
                    // __grid_constant__ kernel parameter, indexed in place)
     int n;
     int off[kMaxBatch + 1];
     int start[kMaxBatch], lc[kMaxBatch];
+    int poff[kMaxBatch + 1];  // attention token pairs before lane b
 };
 // forward row t -> its lane (return) and position (*pos)
 __device__ __forceinline__ int batch_row(const BatchSmem& B, int t, int* pos) {
@@ -309,15 +347,21 @@ struct FwdSmem {
     float red[128];
     float sval[128];
     int sidx[128];
-    float qv[512];
-    float pv[256];
     TpPeers peers;  // copy of FwdArgs::peers (dynamic indexing of kernel parameters would use local memory)
     BatchSmem bt;   // batched forward only
-    float pre[16 * 128];  // a finisher's presummed split-K partials, parked across the accumulator wait
+    union {
+        float pre[16 * 128];  // GEMM phases: a finisher's presummed split-K partials, parked across the accumulator wait
+        struct {
+            float q[4][2][128];  // ATTN phases: each aux warp's two query rows
+            float p[4][2][64];   //              and their probabilities over the chunk
+        } at;
+    };
 };
 static_assert(sizeof(FwdSmem) <= kFwdMiscBytes, "misc shared state exceeds its budget");
 
-// one attention phase of this warp
+// one attention phase of this warp.  Items = (token, q head, chunk), or — when there are more items
+// than warps — (token pair, q head, chunk): a pair shares the chunk's K/V loads (never spans
+// sequences).  Only the distribution of work changes; each token's arithmetic is the same either way.
 template <int HD, bool kB>
 __device__ __forceinline__ void attn_phase(const FwdArgs& a, const FwdPhase& P, int start, int T, int gw, int GW,
                                         float* q_s, float* p_s, int lane, const BatchSmem& B) {
@@ -328,20 +372,38 @@ __device__ __forceinline__ void attn_phase(const FwdArgs& a, const FwdPhase& P, 
         for (int b = 0; b < B.n; ++b) max_pos = max(max_pos, B.lc[b] - 1);
     }
     const int nch_max = max_pos / kAttnChunk + 1;
-    const int items = T * nh * nch_max;
+    const bool pairs = T * nh * nch_max > GW;
+    int units = T;
+    if (pairs) {
+        if constexpr (kB) units = B.poff[B.n];
+        else units = (T + 1) / 2;
+    }
+    const int items = units * nh * nch_max;
     for (int item = gw; item < items; item += GW) {
         const int j = item % nch_max, rest = item / nch_max;
-        const int hq = rest % nh, t = rest / nh;
+        const int hq = rest % nh, u = rest / nh;
+        int t0 = u, nt = 1, pos0, b = 0;
         if constexpr (kB) {
-            int pos;
-            const int b = batch_row(B, t, &pos);
-            if (j * kAttnChunk > pos) continue;
-            attn_item<HD>(a, t, hq, j, pos, a.batch.page_table[b], P.kc + a.batch.koff[b], P.vc + a.batch.voff[b],
-                          q_s, p_s, lane);
+            if (pairs) {
+                while (b + 1 < B.n && u >= B.poff[b + 1]) ++b;
+                t0 = B.off[b] + 2 * (u - B.poff[b]);
+                nt = min(2, B.off[b + 1] - t0);
+                pos0 = B.start[b] + (t0 - B.off[b]);
+            } else {
+                b = batch_row(B, u, &pos0);
+            }
         } else {
-            if (j * kAttnChunk > start + t) continue;
-            attn_item<HD>(a, t, hq, j, start + t, a.page_table, P.kc, P.vc, q_s, p_s, lane);
+            if (pairs) {
+                t0 = 2 * u;
+                nt = min(2, T - t0);
+            }
+            pos0 = start + t0;
         }
+        if (j * kAttnChunk > pos0 + nt - 1) continue;
+        const int32_t* pt = kB ? a.batch.page_table[b] : a.page_table;
+        const __nv_bfloat16* kc = kB ? P.kc + a.batch.koff[b] : P.kc;
+        const __nv_bfloat16* vc = kB ? P.vc + a.batch.voff[b] : P.vc;
+        attn_item<HD, 2>(a, t0, nt, hq, j, pos0, pt, kc, vc, q_s, p_s, lane);  // one code path (registers)
     }
 }
 
@@ -695,8 +757,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
     float* red = sm.red;   // [4][32]
     float* sval = sm.sval; // [4][32]
     int* sidx = sm.sidx;   // [4][32]
-    float* qv = sm.qv;     // [4][128] attention query per warp
-    float* pv = sm.pv;     // [4][64]  attention probabilities per warp
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x, G = gridDim.x;
@@ -706,16 +766,19 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         if constexpr (kB) {
             BatchSmem& B = sm.bt;
             B.n = a.batch.n;
-            int off = 0;
+            int off = 0, pairs = 0;
             for (int b = 0; b < B.n; ++b) {
                 const LaneState* Ls = a.batch.lane[b];
                 const int st = min(Ls->kv_len, Ls->row0), lc = Ls->L + Ls->c;
                 B.off[b] = off;
                 B.start[b] = st;
                 B.lc[b] = lc;
+                B.poff[b] = pairs;
                 off += lc - st;
+                pairs += (lc - st + 1) / 2;
             }
             B.off[B.n] = off;
+            B.poff[B.n] = pairs;
             sint[0] = 0;
             sint[1] = off;
             sint[2] = 0;
@@ -991,8 +1054,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             } else if (P.kind == kPhAttn) {  // ------------------------- split-KV causal attention
                 acquire(P.dep);
                 stamp(a, p, 3);
-                if (a.hd == 128) attn_phase<128, kB>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane, sm.bt);
-                else attn_phase<64, kB>(a, P, start, T, gw, GW, qv + ew * 128, pv + ew * 64, lane, sm.bt);
+                if (a.hd == 128) attn_phase<128, kB>(a, P, start, T, gw, GW, &sm.at.q[ew][0][0], &sm.at.p[ew][0][0], lane, sm.bt);
+                else attn_phase<64, kB>(a, P, start, T, gw, GW, &sm.at.q[ew][0][0], &sm.at.p[ew][0][0], lane, sm.bt);
                 if (lane == 0) stamp(a, p, 8 + ew);  // each aux warp's last item done
                 signal(p);
             } else {  // kPhArgmax ----------------------------------------- final argmax + cursor
