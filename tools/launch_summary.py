@@ -18,7 +18,8 @@ def main(path, last_forward=True):
     ids = sorted(dur)
     if last_forward:
         fb = [i for i in ids if "forward_begin" in names[i]]
-        ids = [i for i in ids if i >= fb[-1]]
+        if fb:
+            ids = [i for i in ids if i >= fb[-1]]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for i in ids:
         a = agg[names[i]]
