@@ -173,12 +173,27 @@ struct RunResult {  // pipeline.hpp:84-88 (traces as the traces_to_jsonl text)
     std::string jsonl;
 };
 
+namespace detail {
+inline dbl_pipeline_options c_options(const PipelineOptions& o) {
+    return dbl_pipeline_options{o.gamma, o.depth, o.draft_retrieval, o.target_retrieval, 1,
+                                o.t_target, o.t_draft, o.t_lookup, o.t_sync, 1, o.sampler.temperature,
+                                o.sampler.rng_seed};
+}
+inline void flatten(const std::vector<TokenSeq>& seqs, std::vector<int64_t>& off, TokenSeq& flat) {
+    off.assign(1, 0);
+    flat.clear();
+    for (const TokenSeq& s : seqs) {
+        flat.insert(flat.end(), s.begin(), s.end());
+        off.push_back(static_cast<int64_t>(flat.size()));
+    }
+    if (flat.empty()) flat.push_back(0);
+}
+}  // namespace detail
+
 // run (pipeline.cpp:264-323)
 inline RunResult run(const Model& draft, const Model& target, HierarchicalDatastore& store, const TokenSeq& prompt,
                      int max_new_tokens, const PipelineOptions& o) {
-    dbl_pipeline_options c{o.gamma, o.depth, o.draft_retrieval, o.target_retrieval, 1,
-                           o.t_target, o.t_draft, o.t_lookup, o.t_sync, 1, o.sampler.temperature,
-                           o.sampler.rng_seed};
+    const dbl_pipeline_options c = detail::c_options(o);
     RunResult r;
     r.output.resize(static_cast<size_t>(max_new_tokens > 0 ? max_new_tokens : 1));
     int n = 0;
@@ -188,6 +203,66 @@ inline RunResult run(const Model& draft, const Model& target, HierarchicalDatast
     r.output.resize(static_cast<size_t>(n));
     (void)jl;
     return r;
+}
+
+
+// Batched DOUBLE: run() for several sequences, one datastore each, sharing every
+// forward; result b == run(draft, target, *stores[b], prompts[b], ...) alone.
+inline std::vector<RunResult> run_batch(const Model& draft, const Model& target,
+                                        const std::vector<HierarchicalDatastore*>& stores,
+                                        const std::vector<TokenSeq>& prompts, int max_new_tokens,
+                                        const PipelineOptions& o) {
+    const dbl_pipeline_options c = detail::c_options(o);
+    std::vector<int64_t> off;
+    TokenSeq flat;
+    detail::flatten(prompts, off, flat);
+    const int B = static_cast<int>(prompts.size()), n = max_new_tokens > 0 ? max_new_tokens : 1;
+    std::vector<dbl_store_t> hs;
+    for (HierarchicalDatastore* st : stores) hs.push_back(st->handle());
+    TokenSeq out(static_cast<size_t>(B) * n);
+    std::vector<int32_t> out_n(static_cast<size_t>(B > 0 ? B : 1));
+    std::vector<dbl_run_metrics> m(static_cast<size_t>(B > 0 ? B : 1));
+    check(dbl_run_batch(draft.handle(), target.handle(), B, hs.data(), off.data(), flat.data(), max_new_tokens, &c,
+                        out.data(), out_n.data(), m.data(), nullptr, 0, nullptr));
+    std::vector<RunResult> rs(static_cast<size_t>(B));
+    for (int b = 0; b < B; ++b) {
+        rs[b].output.assign(out.begin() + static_cast<long>(b) * n, out.begin() + static_cast<long>(b) * n + out_n[b]);
+        rs[b].metrics = m[b];
+    }
+    return rs;
+}
+
+// Batched serving: run_vanilla_ar for several prompts in lockstep, one forward per step over all
+inline std::vector<TokenSeq> run_vanilla_ar_batch(const Model& target, const std::vector<TokenSeq>& prompts,
+                                                  int max_new_tokens, double* device_ms = nullptr) {
+    std::vector<int64_t> off;
+    TokenSeq flat;
+    detail::flatten(prompts, off, flat);
+    const int B = static_cast<int>(prompts.size()), n = max_new_tokens > 0 ? max_new_tokens : 1;
+    TokenSeq out(static_cast<size_t>(B) * n);
+    std::vector<int32_t> out_n(static_cast<size_t>(B > 0 ? B : 1));
+    double ms = 0.0;
+    int64_t launches = 0;
+    check(dbl_run_ar_batch(target.handle(), B, off.data(), flat.data(), max_new_tokens, out.data(), out_n.data(), &ms,
+                           &launches));
+    if (device_ms) *device_ms = ms;
+    std::vector<TokenSeq> rs(static_cast<size_t>(B));
+    for (int b = 0; b < B; ++b)
+        rs[b].assign(out.begin() + static_cast<long>(b) * n, out.begin() + static_cast<long>(b) * n + out_n[b]);
+    return rs;
+}
+
+// forward_batch (model.cpp:37-53) as ProbVector rows: (|cands|+1) x vocab fp64
+inline std::vector<std::vector<double>> forward_batch(const Model& m, std::span<const TokenId> ctx,
+                                                      std::span<const TokenId> cands) {
+    const int V = m.vocab_size();
+    std::vector<double> flat((cands.size() + 1) * static_cast<size_t>(V));
+    check(dbl_forward_dists(m.handle(), ctx.data(), static_cast<int>(ctx.size()), cands.data(),
+                            static_cast<int>(cands.size()), flat.data()));
+    std::vector<std::vector<double>> rows;
+    for (size_t r = 0; r <= cands.size(); ++r)
+        rows.emplace_back(flat.begin() + static_cast<long>(r * V), flat.begin() + static_cast<long>((r + 1) * V));
+    return rows;
 }
 
 // run_vanilla_ar (harness.cpp:233-258)

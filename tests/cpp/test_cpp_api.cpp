@@ -100,6 +100,25 @@ int main() {
         const RunResult r = run(draft, target, store, prompt, 64, PipelineOptions{});
         const RunResult ar = run_vanilla_ar(target, prompt, 64);
         CHECK(r.output == ar.output);
+        // batched DOUBLE / AR: every sequence equals its own single run
+        HierarchicalDatastore s1(3, 10), s2(3, 10), s3(3, 10);
+        for (HierarchicalDatastore* st : {&s1, &s2, &s3}) build_prior(*st, {{1, 2, 3, 4, 5, 1, 2, 3}, {4, 5, 6, 7, 1, 2}}, 10);
+        const std::vector<TokenSeq> ps{prompt, TokenSeq{7, 7, 1}, TokenSeq{3}};
+        const std::vector<RunResult> rb = run_batch(draft, target, {&s1, &s2, &s3}, ps, 48, PipelineOptions{});
+        const std::vector<TokenSeq> ab = run_vanilla_ar_batch(target, ps, 48);
+        for (size_t b = 0; b < ps.size(); ++b) {
+            HierarchicalDatastore sb(3, 10);
+            build_prior(sb, {{1, 2, 3, 4, 5, 1, 2, 3}, {4, 5, 6, 7, 1, 2}}, 10);
+            CHECK(rb[b].output == run(draft, target, sb, ps[b], 48, PipelineOptions{}).output);
+            CHECK(ab[b] == run_vanilla_ar(target, ps[b], 48).output);
+        }
+        // sampled run (SamplerConfig) is reproducible; forward_batch rows are distributions
+        PipelineOptions so;
+        so.sampler = SamplerConfig{1.0, 42};
+        HierarchicalDatastore t1(3, 10), t2(3, 10);
+        CHECK(run(draft, target, t1, prompt, 32, so).output == run(draft, target, t2, prompt, 32, so).output);
+        const auto rows = forward_batch(target, prompt, TokenSeq{2, 3});
+        CHECK(rows.size() == 3 && rows[0].size() == static_cast<size_t>(V));
         CHECK(throws<std::invalid_argument>([&] { run(draft, target, store, TokenSeq{}, 8, PipelineOptions{}); }));
         PipelineOptions bad;
         bad.gamma = 0;
