@@ -8,7 +8,8 @@
 //   * sums and the inverse-CDF scan follow the reference's sequential order on one thread when the
 //     vocabulary is small (<= kExactVocab, e.g. the table models of config 1), so every decision and
 //     token is bit-identical to the reference; wide vocabularies (transformers, no reference to be
-//     bit-identical to) use a fixed-order chunked reduction / two-level scan — deterministic, same law;
+//     bit-identical to) use coalesced fixed-order reductions, a two-level warp-segment scan and fp32
+//     tempering (pow via exp2/log2) — deterministic, same law, ~1.2 MB rows at block bandwidth;
 //   * every uniform() is drawn by thread 0 from the lane's mt19937_64 state, staged in shared memory
 //     for the kernel's lifetime, in exactly the reference's draw order.
 #include "rng.cuh"
@@ -18,7 +19,7 @@ namespace dbl {
 
 namespace {
 
-constexpr int kNT = 256;
+constexpr int kNT = 1024;
 constexpr int kExactVocab = 4096;
 
 struct Blk {
@@ -45,10 +46,9 @@ __device__ double blk_sum(Blk& sh, const double* w, int n) {
             for (int i = 0; i < n; ++i) a += w[i];
             sh.f = a;
         }
-    } else {
-        const int per = (n + kNT - 1) / kNT, lo = t * per, hi = min(n, lo + per);
+    } else {  // thread t sums the elements t, t + kNT, ... (coalesced), then a fixed tree
         double a = 0.0;
-        for (int i = lo; i < hi; ++i) a += w[i];
+        for (int i = t; i < n; i += kNT) a += w[i];
         sh.red[t] = a;
         __syncthreads();
         for (int s = kNT / 2; s > 0; s >>= 1) {
@@ -80,18 +80,32 @@ __device__ int blk_pick(Blk& sh, const double* w, int n, double u) {
             sh.i0 = r == -2 ? last : r;
         }
     } else {
-        const int per = (n + kNT - 1) / kNT, lo = t * per, hi = min(n, lo + per);
+        // warp v owns the contiguous segment [v*seg, (v+1)*seg); its lanes read it 32 elements at a time
+        constexpr int kW = kNT / 32;
+        const int v = t >> 5, ln = t & 31;
+        const int seg = ((n + kW - 1) / kW + 31) & ~31;
+        const int lo = v * seg, hi = min(n, lo + seg);
         double a = 0.0;
         int last = -1;
-        for (int i = lo; i < hi; ++i)
-            if (w[i] > 0.0) { a += w[i]; last = i; }
-        sh.red[t] = a;
-        sh.last[t] = last;
+        for (int i = lo + ln; i < hi; i += 32)
+            if (w[i] > 0.0) {
+                a += w[i];
+                last = i;
+            }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, off);
+            last = max(last, __shfl_xor_sync(0xffffffffu, last, off));
+        }
+        if (ln == 0) {
+            sh.red[v] = a;
+            sh.last[v] = last;
+        }
         __syncthreads();
         if (t == 0) {
             double acc = 0.0;
             int sel = -1, glast = -1;
-            for (int k = 0; k < kNT; ++k) {
+            for (int k = 0; k < kW; ++k) {
                 if (sh.last[k] < 0) continue;
                 glast = sh.last[k];
                 if (u < acc + sh.red[k]) { sel = k; break; }
@@ -102,15 +116,27 @@ __device__ int blk_pick(Blk& sh, const double* w, int n, double u) {
             sh.i0 = glast;
         }
         __syncthreads();
-        if (sh.i1 == t) {
-            double acc = sh.f;
-            int r = last;
-            for (int i = lo; i < hi; ++i) {
-                if (w[i] <= 0.0) continue;
-                acc += w[i];
-                if (u < acc) { r = i; break; }
+        if (sh.i1 == v) {  // the selected warp scans its segment: inclusive warp prefix per 32-element block
+            double base = sh.f;
+            int r = sh.last[v];
+            for (int i0 = lo; i0 < hi; i0 += 32) {
+                const int i = i0 + ln;
+                const double x = i < hi ? w[i] : 0.0;
+                const double val = x > 0.0 ? x : 0.0;
+                double pre = val;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const double o = __shfl_up_sync(0xffffffffu, pre, off);
+                    if (ln >= off) pre += o;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, val > 0.0 && u < base + pre);
+                if (hit) {
+                    r = i0 + __ffs(hit) - 1;
+                    break;
+                }
+                base += __shfl_sync(0xffffffffu, pre, 31);
             }
-            sh.i0 = r;
+            if (ln == 0) sh.i0 = r;
         }
     }
     __syncthreads();
@@ -127,7 +153,15 @@ __device__ bool blk_tempered(Blk& sh, const double* dist, double* out, int n, do
         return true;
     }
     const double inv = 1.0 / T;
-    for (int i = threadIdx.x; i < n; i += kNT) out[i] = dist[i] > 0.0 ? pow(dist[i], inv) : 0.0;
+    if (n <= kExactVocab) {
+        for (int i = threadIdx.x; i < n; i += kNT) out[i] = dist[i] > 0.0 ? pow(dist[i], inv) : 0.0;
+    } else {  // fp32 pow (exp2 . log2): rows of 1e5+ entries at block rate; no reference to match here
+        const float invf = static_cast<float>(inv);
+        for (int i = threadIdx.x; i < n; i += kNT) {
+            const double x = dist[i];
+            out[i] = x > 0.0 ? static_cast<double>(exp2f(log2f(static_cast<float>(x)) * invf)) : 0.0;
+        }
+    }
     __syncthreads();
     const double sum = blk_sum(sh, out, n);
     if (sum <= 0.0) return false;
@@ -353,8 +387,9 @@ __global__ void __launch_bounds__(kNT) softmax_rows_kernel(const float* __restri
     m = red[0];
     __syncthreads();
     double a = 0.0;
+    const float mf = static_cast<float>(m);
     for (int i = t; i < vocab; i += kNT) {
-        const double e = exp(static_cast<double>(l[i]) - m);
+        const double e = static_cast<double>(__expf(l[i] - mf));
         o[i] = e;
         a += e;
     }
