@@ -360,7 +360,6 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     for (DeviceStore* st : stores)
         if (dm.device() != st->device() || tm.device() != st->device())
             throw_invalid("draft, target and datastore must live on the same device");
-    if (B > 1 && o.temperature != 0.0) throw_invalid("batched run: temperature > 0 is single-sequence only");
     for (int i = 0; i < B; ++i)
         for (int k = i + 1; k < B; ++k)
             if (stores[i] == stores[k]) throw_invalid("batched run: every sequence needs its own datastore");
@@ -441,6 +440,16 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
             for (size_t i = 0; i < ls.size(); ++i) m.forward(*ls[i], bounds[i], s);
         }
     };
+    auto dists_set = [&](Model& m, std::vector<Lane*>& ls, const std::vector<int>& bounds, const std::vector<int>& rows,
+                         const std::vector<double*>& outs, cudaStream_t s) {
+        int total = 0;
+        for (int v : bounds) total += v;
+        if (ls.size() == 1 || (total <= m.max_forward_tokens() && total <= 256)) {
+            m.dists_lanes(ls, total, rows, outs, s);
+        } else {
+            for (size_t i = 0; i < ls.size(); ++i) m.dists(*ls[i], bounds[i], rows[i], outs[i], s);
+        }
+    };
     std::vector<Seq*> act;
     for (;;) {
         act.clear();
@@ -475,12 +484,20 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
                 dls.push_back(q.dl.get());
                 bounds.push_back(j == 0 ? q.L + c_max - std::min(q.dl->kv_len, q.L - 1) : 1 + c_max);
             }
-            if (act.size() == 1 && act[0]->smp) {
-                Seq& q = *act[0];
-                Sampled& sm = *q.smp;
-                dm.dists(*q.dl, bounds[0], c_max + 1, sm.ddist.p, S.draft);
-                launch_draft_accept_sampled(*q.dl, q.rr_dev, j, q.L, sm.ddist.p, sm.chain[sm.cur].p, sm.chain_rows,
-                                            sm.rng.p, sm.T, sm.dscratch.p, S.draft);
+            if (act[0]->smp) {
+                std::vector<int> rows;
+                std::vector<double*> outs;
+                for (Seq* qp : act) {
+                    rows.push_back(c_max + 1);
+                    outs.push_back(qp->smp->ddist.p);
+                }
+                dists_set(dm, dls, bounds, rows, outs, S.draft);
+                for (Seq* qp : act) {
+                    Seq& q = *qp;
+                    Sampled& sm = *q.smp;
+                    launch_draft_accept_sampled(*q.dl, q.rr_dev, j, q.L, sm.ddist.p, sm.chain[sm.cur].p, sm.chain_rows,
+                                                sm.rng.p, sm.T, sm.dscratch.p, S.draft);
+                }
             } else {
                 forward_set(dm, dls, bounds, S.draft);
                 for (Seq* qp : act) launch_draft_accept(*qp->dl, qp->rr_dev, j, S.draft);
@@ -495,14 +512,22 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
             bounds.push_back(q.L + tc_max - std::min(q.tl->kv_len, q.nc - 1));
         }
         CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
-        if (act.size() == 1 && act[0]->smp) {
+        if (act[0]->smp) {
             // verify forward + finish_round's verification (rng_v) + the target's own acceptance (rng_t)
-            Seq& q = *act[0];
-            Sampled& sm = *q.smp;
-            tm.dists(*q.tl, bounds[0], q.ns + tc_max + 1, sm.tdist.p, S.target);
+            std::vector<int> rows;
+            std::vector<double*> outs;
+            for (Seq* qp : act) {
+                rows.push_back(qp->ns + tc_max + 1);
+                outs.push_back(qp->smp->tdist.p);
+            }
+            dists_set(tm, tls, bounds, rows, outs, S.target);
             CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
-            launch_target_accept_sampled(*q.tl, q.nc, q.rr_dev, sm.tdist.p, sm.spec_probs, sm.rng.p + 1,
-                                         sm.rng.p + 2, sm.T, false, sm.tscratch.p, S.target);
+            for (Seq* qp : act) {
+                Seq& q = *qp;
+                Sampled& sm = *q.smp;
+                launch_target_accept_sampled(*q.tl, q.nc, q.rr_dev, sm.tdist.p, sm.spec_probs, sm.rng.p + 1,
+                                             sm.rng.p + 2, sm.T, false, sm.tscratch.p, S.target);
+            }
         } else {
             forward_set(tm, tls, bounds, S.target);
             CUDA_CHECK(cudaEventRecord(S.tf1, S.target));

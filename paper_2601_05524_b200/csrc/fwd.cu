@@ -1115,6 +1115,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         for (int b = 0; b < sm.bt.n; ++b) {
                             a.batch.lane[b]->start = sm.bt.start[b];
                             a.batch.lane[b]->kv_len = sm.bt.lc[b];
+                            if (a.batch.row_base) a.batch.row_base[b] = sm.bt.off[b] - sm.bt.start[b];
                         }
                     } else {
                         a.lane->start = start;

@@ -78,6 +78,7 @@ struct FwdBatch {
     int32_t* argmax[kMaxBatch];
     const int32_t* page_table[kMaxBatch];
     long long koff[kMaxBatch], voff[kMaxBatch];  // element offsets of lane b's K / V cache from lane 0's
+    int* row_base;  // optional out: forward row of lane b's position p = row_base[b] + p (logits consumers)
 };
 
 struct FwdArgs {

@@ -64,6 +64,9 @@ class Model {
     // One forward over several lanes at once (independent sequences sharing one weight stream): lane
     // b's rows [min(kv_len, row0), L+c) as in forward(); max_tokens bounds the rows of all lanes.
     virtual void forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s);
+    // dists() over several lanes in one forward (lane b's rows to outs[b], at most max_rows[b])
+    virtual void dists_lanes(const std::vector<Lane*>& lanes, int max_tokens, const std::vector<int>& max_rows,
+                             const std::vector<double*>& outs, cudaStream_t s);
     // persistent (all-SM, cooperatively launched) grids one forward places on device(): at most two may
     // co-run on a GPU, so the decoder serializes draft and target work when the sum would exceed it
     virtual int persistent_grids() const { return 0; }

@@ -368,12 +368,13 @@ __global__ void __launch_bounds__(kNT) ar_sample_kernel(const double* __restrict
 // logits rows (relative to the forward's first processed position) -> fp64 softmax rows of
 // positions [row0, L+c): p = exp(l - max) / sum, fixed-order block reductions
 __global__ void __launch_bounds__(kNT) softmax_rows_kernel(const float* __restrict__ logits, const LaneState* lane,
-                                                           int vocab, double* __restrict__ out) {
+                                                           int vocab, double* __restrict__ out, const int* row_base) {
     __shared__ double red[kNT];
     const int r = blockIdx.x;
     const int rows = lane->L + lane->c - lane->row0;
     if (r >= rows) return;
-    const float* l = logits + static_cast<size_t>(lane->row0 - lane->start + r) * vocab;
+    const int lrow = row_base ? *row_base + lane->row0 + r : lane->row0 - lane->start + r;
+    const float* l = logits + static_cast<size_t>(lrow) * vocab;
     double* o = out + static_cast<size_t>(r) * vocab;
     const int t = threadIdx.x;
     double m = -INFINITY;
@@ -418,7 +419,17 @@ void Model::dists(Lane& lane, int max_tokens, int max_rows, double* out_dev, cud
     const size_t need = static_cast<size_t>(std::max(max_tokens, 1)) * static_cast<size_t>(vocab());
     if (lane.logit_scratch.n < need) lane.logit_scratch.alloc(need);
     logits(lane, max_tokens, lane.logit_scratch.p, s);
-    softmax_rows_kernel<<<std::max(max_rows, 1), kNT, 0, s>>>(lane.logit_scratch.p, lane.state, vocab(), out_dev);
+    launch_softmax_rows(lane.logit_scratch.p, lane.state, vocab(), out_dev, max_rows, nullptr, s);
+}
+
+void Model::dists_lanes(const std::vector<Lane*>& lanes, int max_tokens, const std::vector<int>& max_rows,
+                        const std::vector<double*>& outs, cudaStream_t s) {
+    for (size_t b = 0; b < lanes.size(); ++b) dists(*lanes[b], max_tokens, max_rows[b], outs[b], s);
+}
+
+void launch_softmax_rows(const float* logits, const LaneState* lane, int vocab, double* out, int max_rows,
+                         const int* row_base, cudaStream_t s) {
+    softmax_rows_kernel<<<std::max(max_rows, 1), kNT, 0, s>>>(logits, lane, vocab, out, row_base);
     CUDA_LAUNCH_CHECK();
 }
 

@@ -12,6 +12,10 @@ namespace dbl {
 enum SampleErr : int { kSampDegenerate = 1, kSampCapacity = 2, kSampInvalid = 3, kSampResidualZero = 4 };
 [[noreturn]] void raise_sample_error(int code);
 
+// fp32 logits rows -> fp64 softmax rows of positions [row0, L+c) of `lane`; logits row of position p is
+// p - start (single-lane forward) or *row_base + p (batched forward)
+void launch_softmax_rows(const float* logits, const LaneState* lane, int vocab, double* out, int max_rows,
+                         const int* row_base, cudaStream_t s);
 // Rng(seed) into g[0]
 void launch_seed_rng(DevRng* g, uint64_t seed, cudaStream_t s);
 // g[lane] = derive_rng(seed, round, lane) for lane in {0, 1, 2} (rng_d, rng_t, rng_v; pipeline.cpp:227-231)

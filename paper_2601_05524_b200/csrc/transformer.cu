@@ -20,6 +20,7 @@
 #include "fwd.cuh"
 #include "gemm.cuh"
 #include "tf_kernels.cuh"
+#include "sampling.cuh"
 #include "transformer.cuh"
 
 namespace dbl {
@@ -63,6 +64,7 @@ struct TfCache final : LaneCache {
     DevBuf<FwdPhase> phases;
     CUtensorMap xmaps[3][5];  // xb, attn, act x boxes of 1, 2, 4, 8, 16 token rows
     DevBuf<unsigned long long> done, epoch, slot_flag;
+    DevBuf<int> row_base;  // batched forwards: per-lane forward-row base (FwdBatch::row_base)
     // tensor parallel: this rank's exchange buffers (written by every rank) and all ranks' addresses
     DevBuf<float> xch;
     DevBuf<unsigned long long> xflag, aflag;
@@ -402,6 +404,8 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
             throw_invalid("batched forward: 1.." + std::to_string(kMaxBatch) + " lanes");
         if (m.world > 1) throw_invalid("batched forward: tensor-parallel models are not supported");
         a.batch.n = static_cast<int>(batch->size());
+        if (!c.row_base.p) c.row_base.alloc(kMaxBatch);
+        a.batch.row_base = c.row_base.p;
         for (int b = 0; b < a.batch.n; ++b) {
             Lane& l = *(*batch)[b];
             TfCache& cb = *static_cast<TfCache*>(l.cache.get());
@@ -435,6 +439,22 @@ void Transformer::forward_lanes(const std::vector<Lane*>& lanes, int max_tokens,
     if (lanes.empty()) return;
     Lane& l0 = *lanes[0];
     run_forward(*impl_, device_, l0.state, l0.buf.p, l0.argmax.p, l0.cache.get(), max_tokens, nullptr, 0, s, &lanes);
+}
+
+void Transformer::dists_lanes(const std::vector<Lane*>& lanes, int max_tokens, const std::vector<int>& max_rows,
+                              const std::vector<double*>& outs, cudaStream_t s) {
+    if (lanes.size() == 1) {
+        dists(*lanes[0], max_tokens, max_rows[0], outs[0], s);
+        return;
+    }
+    Lane& l0 = *lanes[0];
+    const size_t need = static_cast<size_t>(std::max(max_tokens, 1)) * static_cast<size_t>(cfg_.vocab);
+    if (l0.logit_scratch.n < need) l0.logit_scratch.alloc(need);
+    run_forward(*impl_, device_, l0.state, l0.buf.p, l0.argmax.p, l0.cache.get(), max_tokens, l0.logit_scratch.p,
+                cfg_.vocab, s, &lanes);
+    const int* base = static_cast<TfCache*>(l0.cache.get())->row_base.p;
+    for (size_t b = 0; b < lanes.size(); ++b)
+        launch_softmax_rows(l0.logit_scratch.p, lanes[b]->state, cfg_.vocab, outs[b], max_rows[b], base + b, s);
 }
 
 void Transformer::logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) {

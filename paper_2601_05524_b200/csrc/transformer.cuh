@@ -18,6 +18,8 @@ class Transformer final : public Model {
     void forward(Lane& lane, int max_tokens, cudaStream_t s) override;
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
     void forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s) override;
+    void dists_lanes(const std::vector<Lane*>& lanes, int max_tokens, const std::vector<int>& max_rows,
+                     const std::vector<double*>& outs, cudaStream_t s) override;
     int max_forward_tokens() const override;
     std::string kind() const override { return "transformer"; }
     int persistent_grids() const override { return 1; }

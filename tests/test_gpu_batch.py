@@ -96,6 +96,15 @@ def test_batched_double_limits(dbl):
     st = dbl.HierarchicalDatastore(3, 10)
     with pytest.raises(dbl.InvalidArgument):  # one datastore per sequence
         dbl.run_batch(tgt, tgt, [st, st], [[1, 2], [3, 4]], 4)
-    with pytest.raises(dbl.InvalidArgument):  # sampled batches are not supported
-        dbl.run_batch(tgt, tgt, [st, dbl.HierarchicalDatastore(3, 10)], [[1, 2], [3, 4]], 4,
-                      dbl.PipelineOptions(temperature=1.0))
+
+
+@pytest.mark.parametrize("temperature", [1.0, 0.8])
+def test_batched_sampled_double_equals_single_runs(dbl, temperature):
+    """T > 0: every sequence of the batch draws its own derive_rng streams, so each equals its own
+    sampled run (distribution rows from one batched forward + per-lane softmax)."""
+    tgt = dbl.Transformer(dbl.transformer_config("tiny-qwen", seed=21, max_seq=2048, init_std=0.08))
+    drf = dbl.Transformer(dbl.transformer_config("tiny-qwen-draft", seed=22, max_seq=2048, init_std=0.08))
+    prior = _prior(tgt.cfg.vocab, 6)
+    prompts = [prior[0][:20], prior[3][:7], [9, 8, 7, 6]]
+    _check_batch_equals_single(dbl, drf, tgt, prior, prompts, 48,
+                               dbl.PipelineOptions(gamma=2, depth=8, temperature=temperature, rng_seed=77))
