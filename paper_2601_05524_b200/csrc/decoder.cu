@@ -46,6 +46,7 @@ Lane::Lane(Model& m, int cap) : model(m), capacity(cap) {
 }
 Lane::~Lane() {
     if (state) cudaFree(state);
+    if (cache) model.recycle_cache(std::move(cache));
 }
 void Model::forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s) {
     for (Lane* l : lanes) forward(*l, max_tokens, s);  // stateless models: one forward per lane

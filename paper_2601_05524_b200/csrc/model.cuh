@@ -49,6 +49,8 @@ class Model {
     virtual int64_t kv_bytes_per_token() const { return 0; }
     virtual int64_t embed_bytes_per_token() const { return 0; }
     virtual std::unique_ptr<LaneCache> make_cache(int capacity) = 0;
+    // a lane's cache when the lane goes away (models may keep a few for the next make_cache)
+    virtual void recycle_cache(std::unique_ptr<LaneCache>) {}
     // Enqueue one forward on stream s: process positions [min(kv_len,row0), L+c) of the lane, write
     // lane.argmax[p] for those positions and set lane.start / lane.kv_len = L+c.  `max_tokens` is a
     // host-side upper bound of L+c-start (kernel shape bucket); the exact count is read on device.

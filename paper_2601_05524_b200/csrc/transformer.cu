@@ -169,6 +169,7 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
 Transformer::~Transformer() {
     cudaSetDevice(device_);
     cudaDeviceSynchronize();
+    pool_.clear();
     delete impl_;
 }
 
@@ -188,7 +189,24 @@ int64_t Transformer::kv_bytes_per_token() const {
 
 int Transformer::max_forward_tokens() const { return kMaxTp; }
 
+void Transformer::recycle_cache(std::unique_ptr<LaneCache> c) {
+    if (!c || impl_->world != 1) return;  // tensor-parallel shard caches are linked to their peers
+    std::lock_guard<std::mutex> lk(pool_mu_);
+    if (pool_.size() < 4) pool_.push_back(std::move(c));
+}
+
 std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
+    if (impl_->world == 1) {
+        std::lock_guard<std::mutex> lk(pool_mu_);
+        for (auto it = pool_.begin(); it != pool_.end(); ++it) {
+            const int cap = static_cast<TfCache*>(it->get())->capacity;
+            if (cap == capacity) {  // exact: batched forwards need every lane's KV at the same stride
+                std::unique_ptr<LaneCache> c = std::move(*it);
+                pool_.erase(it);
+                return c;
+            }
+        }
+    }
     const Impl& m = *impl_;
     DeviceGuard g(device_);
     auto cp = std::make_unique<TfCache>();

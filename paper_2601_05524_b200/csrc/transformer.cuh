@@ -1,5 +1,7 @@
 // Random-init bf16 decoder-only transformer on sm_100a (configs 2-5): see transformer.cu.
 #pragma once
+#include <mutex>
+
 #include "model.cuh"
 
 namespace dbl {
@@ -15,6 +17,7 @@ class Transformer final : public Model {
     int64_t kv_bytes_per_token() const override;
     int64_t embed_bytes_per_token() const override { return static_cast<int64_t>(cfg_.hidden) * 2; }
     std::unique_ptr<LaneCache> make_cache(int capacity) override;
+    void recycle_cache(std::unique_ptr<LaneCache> c) override;
     void forward(Lane& lane, int max_tokens, cudaStream_t s) override;
     void logits(Lane& lane, int max_tokens, float* out_dev, cudaStream_t s) override;
     void forward_lanes(const std::vector<Lane*>& lanes, int max_tokens, cudaStream_t s) override;
@@ -43,6 +46,10 @@ class Transformer final : public Model {
     dbl_transformer_config cfg_;
     int device_;
     int shards_per_device_ = 1;
+    // lane caches (KV, scratch, phase table: ~100s of MB of allocations) kept for reuse across run()
+    // calls — every public call builds fresh lanes, and re-allocating them dominated its host overhead
+    std::mutex pool_mu_;
+    std::vector<std::unique_ptr<LaneCache>> pool_;
 };
 
 }  // namespace dbl
