@@ -7,5 +7,6 @@ this package is the Python mirror of the reference interface used by tests and b
 from .specpar import *  # noqa: F401,F403
 from .specpar import __all__ as _specpar_all
 from .models import PRESETS, transformer_config  # noqa: F401
+from . import harness  # noqa: F401  (config files -> setup -> methods, harness.cpp)
 
-__all__ = list(_specpar_all) + ["PRESETS", "transformer_config"]
+__all__ = list(_specpar_all) + ["PRESETS", "transformer_config", "harness"]
