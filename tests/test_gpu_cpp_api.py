@@ -1,6 +1,5 @@
 """GPU: the C++ mirror of the reference API (include/double_b200.hpp) — reference datastore and
 pipeline unit cases restated in C++ (tests/cpp/test_cpp_api.cpp) against libdouble_b200.so."""
-import os
 import subprocess
 
 import pytest
