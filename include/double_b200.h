@@ -103,6 +103,13 @@ int dbl_transformer_create(const dbl_transformer_config* cfg, int device, void* 
  * GPUs over NVLink, or repeated devices (shards co-reside) — behind one model handle: forward_batch,
  * run, run_vanilla_ar etc. work unchanged; every shard ends each forward with identical argmax rows. */
 int dbl_tp_transformer_create(const dbl_transformer_config* cfg, const int* devices, int world, dbl_model_t* out);
+/* One process per GPU: a shard made by dbl_transformer_create (cfg->tp_rank of cfg->tp_size) exports its
+ * exchange buffers as 4 CUDA IPC handles (256 bytes into out), the processes all-gather them in rank
+ * order (e.g. torch.distributed), and each imports the world x 256 bytes.  From then on every forward of
+ * the shard exchanges partial tiles / argmax winners with the other processes inside fwd_kernel, and
+ * each process runs the same decode loop (identical decisions on every rank). */
+int dbl_tp_ipc_export(dbl_model_t shard, void* out, int64_t cap);
+int dbl_tp_ipc_import(dbl_model_t shard, const void* all, int world);
 int dbl_model_destroy(dbl_model_t m);
 int dbl_model_vocab(dbl_model_t m, int* vocab);
 /* bytes of weights streamed per forward on this rank (the roofline numerator's static part) */

@@ -85,6 +85,8 @@ PROTOTYPES = {
                    C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
     "dbl_run_ar_sampled": [VP, I32P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, I32P, C.c_int,
                            C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
+    "dbl_tp_ipc_export": [VP, VP, C.c_int64],
+    "dbl_tp_ipc_import": [VP, VP, C.c_int],
     "dbl_run_batch": [VP, VP, C.c_int, C.POINTER(VP), I64P, I32P, C.c_int, C.POINTER(PipelineOptions), I32P, I32P,
                       C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
     "dbl_run_ar_batch": [VP, C.c_int, I64P, I32P, C.c_int, I32P, I32P, F64P, I64P],

@@ -266,6 +266,25 @@ int dbl_transformer_create(const dbl_transformer_config* cfg, int device, void* 
         *out = m.release();
     });
 }
+int dbl_tp_ipc_export(dbl_model_t shard, void* out, int64_t cap) {
+    return guarded([&] {
+        need(shard, "shard");
+        need(out, "out");
+        if (cap < static_cast<int64_t>(4 * sizeof(cudaIpcMemHandle_t))) dbl::throw_invalid("handle buffer too small");
+        auto* t = dynamic_cast<dbl::Transformer*>(shard->impl.get());
+        if (!t) dbl::throw_invalid("not a transformer shard");
+        t->ipc_export(out);
+    });
+}
+int dbl_tp_ipc_import(dbl_model_t shard, const void* all, int world) {
+    return guarded([&] {
+        need(shard, "shard");
+        need(all, "handles");
+        auto* t = dynamic_cast<dbl::Transformer*>(shard->impl.get());
+        if (!t) dbl::throw_invalid("not a transformer shard");
+        t->ipc_import(all, world);
+    });
+}
 int dbl_tp_transformer_create(const dbl_transformer_config* cfg, const int* devices, int world, dbl_model_t* out) {
     return guarded([&] {
         need(cfg, "config");

@@ -340,7 +340,7 @@ __device__ __forceinline__ int batch_row(const BatchSmem& B, int t, int* pos) {
 
 struct FwdSmem {
     uint64_t full[kFwdMaxStages], empty[kFwdMaxStages], tfull[2], tempty[2];
-    unsigned long long ep;
+    unsigned long long ep, tp_ep;
     uint32_t tslot;
     int sint[12];
     float rs[256];
@@ -422,6 +422,7 @@ struct TileCtx {
     float *rs, *red, *sval;
     int* sidx;
     unsigned long long tag;  // slot-flag value of this (forward, phase)
+    unsigned long long xtag; // tensor-parallel exchange flag value of this (forward, phase)
     bool has_pre;            // pre holds the presummed partials of the other contributors (decode)
     float* pre;              // shared memory [16][128] (column-major: thread r reads pre[i*128 + r])
     const TpPeers* peers;    // tensor-parallel exchange buffers (shared-memory copy)
@@ -558,11 +559,11 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         __threadfence_system();
         named_bar_sync(1, 128);
         if (et == 0) {
-            for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(x.peers->xflag[rr] + a.tp_rank * nth + m, x.tag);
+            for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(x.peers->xflag[rr] + a.tp_rank * nth + m, x.xtag);
             for (int src = 0; src < a.tp_world; ++src) {  // every rank's partial of this tile has arrived
                 const unsigned long long* f = x.peers->xflag[a.tp_rank] + src * nth + m;
                 Spin sp;
-                while (ld_acquire_sys_u64(f) != x.tag) sp.tick(a.err, 9, x.p);
+                while (ld_acquire_sys_u64(f) != x.xtag) sp.tick(a.err, 9, x.p);
             }
         }
         named_bar_sync(1, 128);
@@ -790,6 +791,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             sint[2] = Lc;
         }
         *sep = *reinterpret_cast<volatile unsigned long long*>(a.epoch);
+        sm.tp_ep = a.tp_epoch ? *reinterpret_cast<volatile unsigned long long*>(a.tp_epoch) : *sep;
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
@@ -808,6 +810,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
     const uint32_t tmem = *tslot;
     const int start = sint[0], T = sint[1];
     const unsigned long long ep = *sep;
+    const unsigned long long tp_ep = sm.tp_ep;
     if (T < 1 || T > tp) {  // host contract violated: nothing consistent to compute
         if (c == 0 && threadIdx.x == 0) {
             if constexpr (kB) a.batch.lane[0]->error = 2;
@@ -1013,7 +1016,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     const uint32_t taddr = tmem + static_cast<uint32_t>(buf * a.acc_cols) + (static_cast<uint32_t>(q * 32) << 16);
                     const bool finisher = my == 0;
                     TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
-                               q, lane, et, r, rs, red, sval, sidx, tag, false, sm.pre, &sm.peers, &sm.bt};
+                               q, lane, et, r, rs, red, sval, sidx, tag, (tp_ep << 12) | static_cast<unsigned long long>(p + 1),
+                               false, sm.pre, &sm.peers, &sm.bt};
                     const bool early = finisher && n_contrib > 1 && tp == 16;
                     if (early) {  // the other contributors are (nearly always) done: sum them now
                         wait_partials(tc);
@@ -1093,7 +1097,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                 if (c == 0 && et == 0) {  // the forward is complete once every CTA has signalled
                     wait_dep(a, p, ep, 7);
                     if constexpr (kTP) {  // vocab-parallel argmax: (max, lowest global id) over ranks
-                        const unsigned long long tag = (ep << 12) | static_cast<unsigned long long>(p + 1);
+                        const unsigned long long tag = (tp_ep << 12) | static_cast<unsigned long long>(p + 1);
                         __threadfence_system();
                         for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(sm.peers.aflag[rr] + a.tp_rank, tag);
                         for (int src = 0; src < a.tp_world; ++src) {
@@ -1123,6 +1127,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     }
                     __threadfence();
                     *reinterpret_cast<volatile unsigned long long*>(a.epoch) = ep + 1;
+                    if (a.tp_epoch) *reinterpret_cast<volatile unsigned long long*>(a.tp_epoch) = tp_ep + 1;
                 }
             }
         }

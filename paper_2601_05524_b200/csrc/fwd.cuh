@@ -117,6 +117,9 @@ struct FwdArgs {
     unsigned long long* trace;  // optional [n_ph][G][16] %globaltimer stamps
     int tp_world, tp_rank, vocab_off;  // tensor parallel (world 1: none); vocab_off = rank * vocab_l
     TpPeers peers;
+    // optional model-level forward counter for the exchange tags (one process per shard: the exchange
+    // buffers outlive lane caches, so their tags must not restart with a new cache); nullptr = epoch
+    unsigned long long* tp_epoch;
     FwdBatch batch;
 };
 

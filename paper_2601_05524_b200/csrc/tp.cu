@@ -57,6 +57,9 @@ TpTransformer::TpTransformer(const dbl_transformer_config& cfg, const std::vecto
         for (int q = 0; q < world; ++q) same += devices[q] == devices[r];
         shards_.back()->set_shards_per_device(same);
     }
+    std::vector<Transformer*> ptrs;
+    for (auto& s : shards_) ptrs.push_back(s.get());
+    Transformer::link_models(ptrs);  // model-level exchange buffers + exchange-tag counter
 }
 
 TpTransformer::~TpTransformer() = default;
@@ -65,7 +68,6 @@ std::unique_ptr<LaneCache> TpTransformer::make_cache(int capacity) {
     auto tc = std::make_unique<TpCache>();
     tc->capacity = capacity;
     tc->c0 = shards_[0]->make_cache(capacity);
-    std::vector<LaneCache*> all{tc->c0.get()};
     for (int r = 1; r < world(); ++r) {
         auto sl = std::make_unique<ShardLane>();
         sl->device = devices_[r];
@@ -80,10 +82,8 @@ std::unique_ptr<LaneCache> TpTransformer::make_cache(int capacity) {
         CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CUDA_CHECK(cudaStreamCreateWithPriority(&sl->stream, cudaStreamNonBlocking, hi));
         CUDA_CHECK(cudaEventCreateWithFlags(&sl->done, cudaEventDisableTiming));
-        all.push_back(sl->cache.get());
         tc->rest.push_back(std::move(sl));
     }
-    Transformer::link_tp(all);
     {
         DeviceGuard g(devices_[0]);
         CUDA_CHECK(cudaEventCreateWithFlags(&tc->ready, cudaEventDisableTiming));

@@ -49,6 +49,14 @@ struct Transformer::Impl {
     DevBuf<__nv_bfloat16> w_qkv, w_o, w_gu, w_down;
     CUtensorMap t_qkv, t_o, t_gu, t_down, t_lm;
     GemmProfiler* prof = nullptr;
+    // one process per shard (IPC): this rank's exchange buffers (model-level, exported once), every
+    // rank's addresses (peers' opened from their IPC handles) and the model-level exchange-tag counter
+    DevBuf<float> ipc_xch;
+    DevBuf<unsigned long long> ipc_xflag, ipc_aflag, ipc_epoch;
+    DevBuf<float2> ipc_axch;
+    TpPeers ipc_peers{};
+    bool ipc_linked = false;
+    std::vector<void*> ipc_opened;
 };
 
 void Transformer::set_profiler(GemmProfiler* p) { impl_->prof = p; }
@@ -170,6 +178,7 @@ Transformer::~Transformer() {
     cudaSetDevice(device_);
     cudaDeviceSynchronize();
     pool_.clear();
+    for (void* p : impl_->ipc_opened) cudaIpcCloseMemHandle(p);
     delete impl_;
 }
 
@@ -337,7 +346,9 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     if (ph.size() >= 4095) throw_invalid("stream forward: too many phases for the slot-flag tag");
     c.slot_flag.alloc(2 * static_cast<size_t>(sms) + 2);
     c.slot_flag.zero();
-    if (m.world > 1) {
+    if (m.world > 1 && m.ipc_linked) {
+        c.peers = m.ipc_peers;  // one process per shard: the model-level buffers, linked once
+    } else if (m.world > 1) {
         const size_t nth = static_cast<size_t>(m.h / 128);
         c.xch.alloc(kMaxTpRanks * nth * kMaxTp * 128);
         c.xflag.alloc(kMaxTpRanks * nth);
@@ -417,6 +428,7 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
     a.tp_rank = m.rank;
     a.vocab_off = m.rank * m.vocab_l;
     a.peers = c.peers;
+    a.tp_epoch = m.ipc_linked ? m.ipc_epoch.p : nullptr;
     if (batch) {  // several lanes in one forward; lane 0's cache holds the shared scratch and phase table
         if (batch->empty() || static_cast<int>(batch->size()) > kMaxBatch)
             throw_invalid("batched forward: 1.." + std::to_string(kMaxBatch) + " lanes");
@@ -485,6 +497,85 @@ void Transformer::forward_raw(LaneState* state, const int32_t* buf, int32_t* arg
                               int max_tokens, float* logits_dev, cudaStream_t s) {
     DeviceGuard g(device_);
     run_forward(*impl_, device_, state, buf, argmax, cache, max_tokens, logits_dev, logits_dev ? cfg_.vocab : 0, s);
+}
+
+void Transformer::ensure_xbuf() {
+    Impl& m = *impl_;
+    if (m.world < 2) throw_invalid("tensor-parallel exchange: not a shard (tp_size < 2)");
+    DeviceGuard g(device_);
+    if (!m.ipc_xch.p) {
+        const size_t nth = static_cast<size_t>(m.h / 128);
+        m.ipc_xch.alloc(kMaxTpRanks * nth * kMaxTp * 128);
+        m.ipc_xflag.alloc(kMaxTpRanks * nth);
+        m.ipc_xflag.zero();
+        m.ipc_axch.alloc(static_cast<size_t>(kMaxTpRanks) * kMaxTp);
+        m.ipc_aflag.alloc(kMaxTpRanks);
+        m.ipc_aflag.zero();
+        m.ipc_epoch.alloc(1);
+        m.ipc_epoch.zero();
+        CUDA_CHECK(cudaDeviceSynchronize());
+    }
+}
+
+void Transformer::link_models(const std::vector<Transformer*>& shards) {
+    // in-process group: every shard addresses the others' model-level buffers directly (same device or
+    // a peer device over NVLink) — the same exchange state the IPC path links across processes
+    TpPeers p{};
+    for (size_t r = 0; r < shards.size(); ++r) {
+        shards[r]->ensure_xbuf();
+        Impl& m = *shards[r]->impl_;
+        if (m.rank != static_cast<int>(r) || m.world != static_cast<int>(shards.size()))
+            throw_invalid("link_models: shards must be ranks 0..world-1 in order");
+        p.xch[r] = m.ipc_xch.p;
+        p.xflag[r] = m.ipc_xflag.p;
+        p.axch[r] = m.ipc_axch.p;
+        p.aflag[r] = m.ipc_aflag.p;
+    }
+    for (Transformer* t : shards) {
+        t->impl_->ipc_peers = p;
+        t->impl_->ipc_linked = true;
+    }
+}
+
+void Transformer::ipc_export(void* out) {
+    Impl& m = *impl_;
+    ensure_xbuf();
+    DeviceGuard g(device_);
+    cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(out);
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[0], m.ipc_xch.p));
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[1], m.ipc_xflag.p));
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[2], m.ipc_axch.p));
+    CUDA_CHECK(cudaIpcGetMemHandle(&h[3], m.ipc_aflag.p));
+}
+
+void Transformer::ipc_import(const void* all, int world) {
+    Impl& m = *impl_;
+    if (world != m.world) throw_invalid("ipc_import: handle count does not match tp_size");
+    if (!m.ipc_xch.p) throw_logic("ipc_import: call ipc_export first");
+    if (m.ipc_linked) throw_logic("ipc_import: already linked");
+    DeviceGuard g(device_);
+    const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all);
+    TpPeers p{};
+    for (int r = 0; r < world; ++r) {
+        if (r == m.rank) {
+            p.xch[r] = m.ipc_xch.p;
+            p.xflag[r] = m.ipc_xflag.p;
+            p.axch[r] = m.ipc_axch.p;
+            p.aflag[r] = m.ipc_aflag.p;
+            continue;
+        }
+        void* ptr[4];
+        for (int k = 0; k < 4; ++k) {
+            CUDA_CHECK(cudaIpcOpenMemHandle(&ptr[k], h[4 * r + k], cudaIpcMemLazyEnablePeerAccess));
+            m.ipc_opened.push_back(ptr[k]);
+        }
+        p.xch[r] = static_cast<float*>(ptr[0]);
+        p.xflag[r] = static_cast<unsigned long long*>(ptr[1]);
+        p.axch[r] = static_cast<float2*>(ptr[2]);
+        p.aflag[r] = static_cast<unsigned long long*>(ptr[3]);
+    }
+    m.ipc_peers = p;
+    m.ipc_linked = true;
 }
 
 void Transformer::link_tp(const std::vector<LaneCache*>& caches) {

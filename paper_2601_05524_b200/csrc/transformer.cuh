@@ -35,11 +35,19 @@ class Transformer final : public Model {
                      float* logits_dev, cudaStream_t s);
     // tensor parallel: make every rank's lane cache address all ranks' exchange buffers (rank order)
     static void link_tp(const std::vector<LaneCache*>& caches);
+    // tensor parallel with one process per shard: export this shard's exchange buffers as 4 CUDA IPC
+    // handles (out: 4 x cudaIpcMemHandle_t), then import every rank's (rank order, world x 4) — after
+    // which every lane cache of this shard exchanges with the other processes inside fwd_kernel
+    void ipc_export(void* out);
+    void ipc_import(const void* all, int world);
+    // the same model-level exchange state for shards of ONE process (TpTransformer)
+    static void link_models(const std::vector<Transformer*>& shards);
     // tensor-parallel shards sharing one GPU: each forward takes 1/k of the SMs (set before make_cache)
     void set_shards_per_device(int k) { shards_per_device_ = k; }
 
     struct Impl;
     static int64_t weight_bytes_of(const Impl& m);
+    void ensure_xbuf();  // this shard's model-level exchange buffers (allocated once)
 
   private:
     Impl* impl_ = nullptr;

@@ -33,7 +33,7 @@ PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
 __all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
-           "run_vanilla_ar", "run_vanilla_ar_batch", "run_batch",
+           "run_vanilla_ar", "run_vanilla_ar_batch", "run_batch", "link_tp_processes",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
            "parse_model_v1", "parse_dstore_v1", "serialize_model", "serialize_index", "save_model",
            "load_model", "save_index", "load_index"]
@@ -515,6 +515,23 @@ def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float 
                                   float(temperature), C.c_uint64(int(rng_seed)), _p32(out), cap, C.byref(n),
                                   C.byref(m), js, len(js) if js is not None else 0, C.byref(jl))
     return _finish(rc, out, n, m, js, jl, want_jsonl)
+
+
+def link_tp_processes(shard: "Transformer", group=None):
+    """One process per GPU: link this process's tensor-parallel shard (tp_rank = this
+    rank of `group`) with the other ranks' shards — CUDA IPC handles of the exchange buffers,
+    all-gathered with torch.distributed (any backend; gloo is enough).  Afterwards every rank runs the
+    same decode loop; the forwards exchange partial tiles inside fwd_kernel."""
+    import torch.distributed as dist
+    buf = (C.c_uint8 * 256)()
+    check(lib().dbl_tp_ipc_export(shard._h, buf, 256))
+    world = dist.get_world_size(group)
+    if shard.cfg.tp_size != world or shard.cfg.tp_rank != dist.get_rank(group):
+        raise InvalidArgument("link_tp_processes: the shard's tp_rank / tp_size must be this rank / world size")
+    allh = [None] * world
+    dist.all_gather_object(allh, bytes(buf), group=group)
+    flat = b"".join(allh)
+    check(lib().dbl_tp_ipc_import(shard._h, flat, world))
 
 
 def run_batch(draft: _Model, target: _Model, stores, prompts, max_new_tokens: int,
