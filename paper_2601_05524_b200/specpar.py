@@ -523,15 +523,23 @@ def link_tp_processes(shard: "Transformer", group=None):
     all-gathered with torch.distributed (any backend; gloo is enough).  Afterwards every rank runs the
     same decode loop; the forwards exchange partial tiles inside fwd_kernel."""
     import torch.distributed as dist
-    buf = (C.c_uint8 * 256)()
-    check(lib().dbl_tp_ipc_export(shard._h, buf, 256))
     world = dist.get_world_size(group)
     if shard.cfg.tp_size != world or shard.cfg.tp_rank != dist.get_rank(group):
         raise InvalidArgument("link_tp_processes: the shard's tp_rank / tp_size must be this rank / world size")
-    allh = [None] * world
-    dist.all_gather_object(allh, bytes(buf), group=group)
-    flat = b"".join(allh)
+    buf = (C.c_uint8 * 256)()
+    check(lib().dbl_tp_ipc_export(shard._h, buf, 256))
+    flat = gather_tp_handles(bytes(buf), group)
     check(lib().dbl_tp_ipc_import(shard._h, flat, world))
+
+
+def gather_tp_handles(mine: bytes, group=None) -> bytes:
+    """Every rank's exchange-buffer handles (256 bytes each), concatenated in rank order."""
+    import torch.distributed as dist
+    if len(mine) != 256:
+        raise InvalidArgument("gather_tp_handles: 4 CUDA IPC handles (256 bytes) per rank")
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    return b"".join(allh)
 
 
 def run_batch(draft: _Model, target: _Model, stores, prompts, max_new_tokens: int,
