@@ -200,16 +200,40 @@ __device__ __forceinline__ void attn_token_out(const FwdArgs& a, int t, int hq, 
     __syncwarp();  // lane 0's acquire orders the other lanes' reads of the partials
     // combine this position's chunks in chunk order
     const long long base = (static_cast<long long>(t) * nh + hq) * a.max_chunks;
+    // lane jj holds chunk jj's (max, sum) (32 chunks per pass); outputs 4 chunks per round trip, in
+    // chunk order
+    const float2* ml = reinterpret_cast<const float2*>(a.part_ml) + base;
     float M = -INFINITY;
-    for (int jj = 0; jj < nch; ++jj) M = fmaxf(M, __ldcg(a.part_ml + 2 * (base + jj)));
+    for (int jb = 0; jb < nch; jb += 32)
+        if (jb + lane < nch) M = fmaxf(M, __ldcg(ml + jb + lane).x);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
     float den = 0.f, acc[DPL];
 #pragma unroll
     for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
-    for (int jj = 0; jj < nch; ++jj) {
-        const float wgt = __expf(__ldcg(a.part_ml + 2 * (base + jj)) - M);
-        den = fmaf(__ldcg(a.part_ml + 2 * (base + jj) + 1), wgt, den);
+    for (int jb = 0; jb < nch; jb += 32) {
+        const bool mine = jb + lane < nch;
+        const float2 mv = mine ? __ldcg(ml + jb + lane) : make_float2(M, 0.f);
+        const float wl = mine ? __expf(mv.x - M) : 0.f;
+        const int n32 = min(32, nch - jb);
+        for (int i0 = 0; i0 < n32; i0 += 4) {
+            float v[4][DPL];
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[e] = fmaf(__ldcg(a.part_o + (base + jj) * HD + lane * DPL + e), wgt, acc[e]);
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int e = 0; e < DPL; ++e)
+                    v[i][e] = i0 + i < n32 ? __ldcg(a.part_o + (base + jb + i0 + i) * HD + lane * DPL + e) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float wi = __shfl_sync(0xffffffffu, wl, (i0 + i) & 31);
+                const float li = __shfl_sync(0xffffffffu, mv.y, (i0 + i) & 31);
+                if (i0 + i < n32) {
+                    den = fmaf(li, wi, den);
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) acc[e] = fmaf(v[i][e], wi, acc[e]);
+                }
+            }
+        }
     }
     const float inv = 1.0f / den;
 #pragma unroll
