@@ -302,7 +302,7 @@ def main():
                    "--max-new", str(a.max_new), "--seed", str(a.seed)]
             line, err = None, ""
             try:
-                r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1500)
+                r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
                 outs = [x for x in r.stdout.splitlines() if x.startswith("{")]
                 if r.returncode == 0 and outs:
                     line = outs[-1]
