@@ -513,13 +513,13 @@ __device__ __forceinline__ int slot_of(const TileCtx& x, int j) {  // partial sl
     const int cj = x.first + j;
     return 2 * cj + (range_begin(cj, x.U, x.A) >= x.tile_u0 ? 0 : 1);
 }
-__device__ __forceinline__ void wait_partials(const TileCtx& x) {  // et == 0 polls, then the epilogue barrier
-    if (x.et == 0) {
-        for (int j = 1; j < x.n_contrib; ++j) {
-            const unsigned long long* f = x.a->slot_flag + slot_of(x, j);
-            Spin sp;
-            while (ld_relaxed_u64(f) != x.tag) sp.tick(x.a->err, 8, x.p);
-        }
+// one poller per contributor flag (all polls in flight together: a tile split over k CTAs costs one
+// round trip, not k - 1), each acquiring its flag, then the epilogue barrier
+__device__ __forceinline__ void wait_partials(const TileCtx& x) {
+    for (int j = 1 + x.et; j < x.n_contrib; j += 128) {
+        const unsigned long long* f = x.a->slot_flag + slot_of(x, j);
+        Spin sp;
+        while (ld_relaxed_u64(f) != x.tag) sp.tick(x.a->err, 8, x.p);
         fence_acq_rel_gpu();
     }
     named_bar_sync(1, 128);
@@ -582,13 +582,13 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         }
         __threadfence_system();
         named_bar_sync(1, 128);
-        if (et == 0) {
-            for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(x.peers->xflag[rr] + a.tp_rank * nth + m, x.xtag);
-            for (int src = 0; src < a.tp_world; ++src) {  // every rank's partial of this tile has arrived
-                const unsigned long long* f = x.peers->xflag[a.tp_rank] + src * nth + m;
-                Spin sp;
-                while (ld_acquire_sys_u64(f) != x.xtag) sp.tick(a.err, 9, x.p);
-            }
+        // thread rr releases this rank's flag at rank rr and then waits for rank rr's flag here: all the
+        // ranks' flags are polled in parallel (one round trip, not world - 1)
+        if (et < a.tp_world) {
+            st_release_sys_u64(x.peers->xflag[et] + a.tp_rank * nth + m, x.xtag);
+            const unsigned long long* f = x.peers->xflag[a.tp_rank] + et * nth + m;
+            Spin sp;
+            while (ld_acquire_sys_u64(f) != x.xtag) sp.tick(a.err, 9, x.p);
         }
         named_bar_sync(1, 128);
     }
