@@ -401,9 +401,9 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
         ar_ms += ar.metrics["device_ms"]
         ar_tok += len(ar.output)
     lossless = all(r.output == ar.output for r in results)
-    gamma_c_line = None
-    if gamma_c != gamma:  # the reference's own gamma rule, same workload, same timing
-        oc = dbl.PipelineOptions(gamma=gamma_c, depth=DEPTH)
+    def gamma_line(g):  # the same workload and timing at another gamma (ceil(C), 4, 8)
+        nonlocal lossless
+        oc = dbl.PipelineOptions(gamma=g, depth=DEPTH)
         dbl.run(drf, tgt, store(), prompt, max_new, oc, want_jsonl=False)
         gms, gtok, gm = 0.0, 0, None
         for _ in range(a.steps):
@@ -413,7 +413,10 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
             lossless &= rg.output == ar.output
             gm = rg.metrics
         gv = all_sum(gtok, world) / (all_max(gms, world) / 1e3)
-        gamma_c_line = {"gamma": gamma_c, "value": round(gv, 3), "mean_accepted_len": round(gm["m"], 4)}
+        return {"gamma": g, "value": round(gv, 3), "mean_accepted_len": round(gm["m"], 4)}
+
+    gamma_c_line = gamma_line(gamma_c) if gamma_c != gamma else None
+    gamma_8_line = gamma_line(8) if 8 not in (gamma, gamma_c) else None
 
     t_dev = all_max(dev_ms, world)
     t_e2e = all_max(e2e_ms, world)
@@ -449,6 +452,7 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
         "rounds_per_step": m0["rounds"], "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 3),
         "lossless_vs_ar": lossless,
         "gamma_C": dict(gamma_c_line, speedup_vs_ar=round(gamma_c_line["value"] / ar_value, 4)) if gamma_c_line else None,
+        "gamma_8": dict(gamma_8_line, speedup_vs_ar=round(gamma_8_line["value"] / ar_value, 4)) if gamma_8_line else None,
         "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s",
                 "h2d_bytes_per_step": 4 * (len(prompt) + sum(len(s) for s in prior)),
                 "d2h_bytes_per_step": 4 * max_new},
