@@ -60,3 +60,17 @@ def test_acceptance_criteria_5_to_7_on_device(hz):
         assert all(ms[i] >= ms[i - 1] - 1e-9 for i in range(1, len(ms))), (seed, ms)
     sat = hz.sweep_depth(dataclasses.replace(sw, rho=0.7, t_draft=0.25, gamma=4, seed=11), [10, 20])
     assert (sat[1].m - sat[0].m) / sat[0].m < 0.05
+
+
+def test_cli_run_writes_the_reference_trace(tmp_path):
+    import subprocess
+    import sys
+    from conftest import ROOT
+    cfg = tmp_path / "ceiling_break.cfg"
+    cfg.write_text(CFG1["config"])
+    tr = tmp_path / "trace.jsonl"
+    r = subprocess.run([sys.executable, "-m", "paper_2601_05524_b200", "run", "--config", str(cfg), "--trace", str(tr)],
+                       env=dict(os.environ, PYTHONPATH=ROOT), capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert hashlib.sha256(tr.read_text().encode()).hexdigest() == CFG1["methods"]["double"]["jsonl_sha256"]
+    assert "double" in r.stdout and "speedup" in r.stdout
