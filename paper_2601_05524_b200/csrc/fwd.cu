@@ -607,13 +607,22 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         } else {
             tmem_ld<CH>(x.taddr + ch, v);
         }
-        if (x.n_contrib > 1 && !tp_resid) {  // own + (p_1 + p_2 + ...): fixed contributor order (per shape)
+        // own + (p_1 + p_2 + ...): fixed contributor order (per shape); a split residual tile adds the
+        // residual to the presum (own + (presum + resid)) so the early finisher can do it before its
+        // accumulator is ready — every path (row count, early or not) uses this one order
+        const bool fold = !kTP && P.epi == kFeResid && x.n_contrib > 1;
+        if (x.n_contrib > 1 && !tp_resid) {
             float pre[16];
             if (x.has_pre) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) pre[i] = x.pre[i * kBM + r];
             } else {
                 presum(x, ch, pre);
+                if (fold) {
+                    const float* o = a.resid + static_cast<long long>(ch) * h + n;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pre[i] += i < nc ? __ldcg(o + static_cast<long long>(i) * h) : 0.f;
+                }
             }
 #pragma unroll
             for (int i = 0; i < CH; ++i) v[i] += pre[i];
@@ -623,10 +632,10 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
             float* o = a.resid + static_cast<long long>(ch) * h + n;
             float sq[CH];
 #pragma unroll
-            for (int i = 0; i < CH; ++i) sq[i] = i < nc ? __ldcg(o + static_cast<long long>(i) * h) : 0.f;
+            for (int i = 0; i < CH; ++i) sq[i] = (i < nc && !fold) ? __ldcg(o + static_cast<long long>(i) * h) : 0.f;
 #pragma unroll
             for (int i = 0; i < CH; ++i) {
-                const float nv = sq[i] + v[i];
+                const float nv = fold ? v[i] : sq[i] + v[i];
                 if (i < nc) {
                     o[static_cast<long long>(i) * h] = nv;
                     a.xb[static_cast<long long>(ch + i) * h + n] = __float2bfloat16_rn(nv);
@@ -1047,6 +1056,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         wait_partials(tc);
                         float pre[16];
                         presum(tc, 0, pre);
+                        if (!kTP && P.epi == kFeResid) {  // fold the residual in too (off the tail's chain)
+                            const float* o = a.resid + m * kBM + r;
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) pre[i] += __ldcg(o + static_cast<long long>(i) * a.h);
+                        }
 #pragma unroll
                         for (int i = 0; i < 16; ++i) sm.pre[i * kBM + r] = pre[i];  // own thread's row only
                         tc.has_pre = true;
