@@ -882,7 +882,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         stamped = w.p;
                     }
                     mbar_arrive_expect_tx(&full[wr.st], stage_tx);
-                    tma_load_2d(sA + wr.st * kABytes, &a.wmaps[w.wmap], &full[wr.st], w.kb * kBK, w.wrow + w.m * kBM,
+                    // tiled weight image: tile (row block, kb) is rows [(blk * KB + kb) * 128, +128) of 128 B
+                    tma_load_2d(sA + wr.st * kABytes, &a.wmaps[w.wmap], &full[wr.st], 0,
+                                ((w.wrow / kBM + w.m) * w.KB + w.kb) * kBM,
                                 kEvictFirst);
                     wr.next(S);
                     ++pending;

@@ -406,6 +406,19 @@ void gemm_prepare() {
     set_smem_attr<static_cast<int>(Epi::StoreF32)>();
 }
 
+CUtensorMap make_tmap_bf16_tiled(const void* ptr, uint64_t tiles) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(kBlockK), tiles * 128};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(kBlockK) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBlockK), 128};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(DBL_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {cols, rows};

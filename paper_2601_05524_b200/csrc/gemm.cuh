@@ -60,6 +60,9 @@ struct GemmWorkspace {  // per decode lane (a lane's GEMMs are stream-ordered)
 int num_sms(int device);
 void gemm_prepare();  // set kernel attributes (call before stream capture)
 CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t rows, uint64_t cols, int box_rows);
+// a tiled weight image (launch_tile_weights) of `tiles` 128 x 64 tiles as [tiles * 128][64] rows of
+// 128 B: box (64, 128) at row tile * 128 is one contiguous 16 KiB tile
+CUtensorMap make_tmap_bf16_tiled(const void* ptr, uint64_t tiles);
 CUtensorMap make_tmap_bf16_kblocks(const void* ptr, uint64_t rows, uint64_t cols, int box_rows, int box_kb);
 
 // Launch one GEMM.  tmW: weights (box 128 x 64), tmX: activations (box 16 x 64).

@@ -426,6 +426,38 @@ void launch_init_qkv(__nv_bfloat16* dst, int q_dim, int kv_dim, int hd, int hidd
     CUDA_LAUNCH_CHECK();
 }
 
+__global__ void tile_weights_kernel(__nv_bfloat16* __restrict__ dst, const __nv_bfloat16* __restrict__ src, int rows,
+                                    int K, int rows_p, bool untile) {
+    const long long n8 = static_cast<long long>(rows_p) * K / 8;  // 16-byte groups of the tiled image
+    const int KB = K / kWTileK;
+    for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < n8;
+         g += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long e = g * 8;
+        const long long tile = e / (kWTileRows * kWTileK);
+        const int in = static_cast<int>(e % (kWTileRows * kWTileK));
+        const int r = static_cast<int>(tile / KB) * kWTileRows + in / kWTileK;
+        const long long k = (tile % KB) * kWTileK + in % kWTileK;
+        if (!untile) {
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (r < rows) v = *reinterpret_cast<const uint4*>(src + static_cast<long long>(r) * K + k);
+            *reinterpret_cast<uint4*>(dst + e) = v;
+        } else if (r < rows) {
+            *reinterpret_cast<uint4*>(dst + static_cast<long long>(r) * K + k) = *reinterpret_cast<const uint4*>(src + e);
+        }
+    }
+}
+
+void launch_tile_weights(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, cudaStream_t s) {
+    if (K % kWTileK) throw_invalid("tiled weights: K must be a multiple of 64");
+    tile_weights_kernel<<<1184, 256, 0, s>>>(dst, src, rows, K, static_cast<int>(tiled_rows(rows)), false);
+    CUDA_CHECK(cudaGetLastError());
+}
+void launch_untile_weights(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, cudaStream_t s) {
+    if (K % kWTileK) throw_invalid("tiled weights: K must be a multiple of 64");
+    tile_weights_kernel<<<1184, 256, 0, s>>>(dst, src, rows, K, static_cast<int>(tiled_rows(rows)), true);
+    CUDA_CHECK(cudaGetLastError());
+}
+
 void launch_fill(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t s) {
     fill_kernel<<<blocks_for(n, 256), 256, 0, s>>>(dst, n, v);
     CUDA_LAUNCH_CHECK();

@@ -49,6 +49,13 @@ inline int qkv_perm_dim(int pr, int hd) {
     return l < 16 ? 16 * w + l : hd / 2 + 16 * w + l - 16;
 }
 void launch_fill(__nv_bfloat16* dst, int64_t n, float v, cudaStream_t s);
+// row-major [rows][K] -> the stream forward's tiled weight image: 128 x 64 tiles, each one contiguous
+// 16 KiB block, tile (m, kb) at ((m * K/64) + kb) * 8192 elements; rows padded to a multiple of 128
+// with zeros.  (K % 64 == 0.)  Inverse: launch_untile_weights.
+constexpr int kWTileRows = 128, kWTileK = 64;
+inline int64_t tiled_rows(int64_t rows) { return (rows + kWTileRows - 1) / kWTileRows * kWTileRows; }
+void launch_tile_weights(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, cudaStream_t s);
+void launch_untile_weights(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, cudaStream_t s);
 void launch_forward_begin(LaneState* lane, cudaStream_t s);  // lane.start = min(kv_len, row0)
 void launch_forward_end(LaneState* lane, cudaStream_t s);    // lane.kv_len = L + c
 

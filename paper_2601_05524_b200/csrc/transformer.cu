@@ -121,12 +121,17 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
     const float sd = c.init_std;
     const int h = m.h;
     m.layers.resize(c.n_layers);
-    const size_t n_qkv = static_cast<size_t>(m.qkv_rows) * h, n_o = static_cast<size_t>(h) * m.q_dim;
-    const size_t n_gu = static_cast<size_t>(2) * m.ffn_l * h, n_down = static_cast<size_t>(h) * m.ffn_l;
+    // weights live in HBM as tiled images (launch_tile_weights: every 128 x 64 tile one contiguous
+    // 16 KiB block, so a CTA's stream-K range is one sequential read); each is generated row-major
+    // into `scratch` first
+    const size_t n_qkv = static_cast<size_t>(tiled_rows(m.qkv_rows)) * h, n_o = static_cast<size_t>(tiled_rows(h)) * m.q_dim;
+    const size_t n_gu = static_cast<size_t>(tiled_rows(2LL * m.ffn_l)) * h, n_down = static_cast<size_t>(tiled_rows(h)) * m.ffn_l;
     m.w_qkv.alloc(n_qkv * c.n_layers);
     m.w_o.alloc(n_o * c.n_layers);
     m.w_gu.alloc(n_gu * c.n_layers);
     m.w_down.alloc(n_down * c.n_layers);
+    DevBuf<__nv_bfloat16> scratch;
+    scratch.alloc(std::max({n_qkv, n_o, n_gu, n_down, static_cast<size_t>(tiled_rows(m.vocab_l) * h)}));
     for (int l = 0; l < c.n_layers; ++l) {
         LayerW& w = m.layers[l];
         // RMSNorm weights are 1 in this random-init family; the stream forward folds them (fwd.cuh)
@@ -141,37 +146,44 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
             launch_fill(w.k_norm.p, m.hd, 1.0f, s);
         }
         w.qkv = m.w_qkv.p + n_qkv * l;
-        launch_init_qkv(w.qkv, m.q_dim, m.kv_dim, m.hd, h, seed, layer_id(l, kQ), layer_id(l, kK), layer_id(l, kV),
+        launch_init_qkv(scratch.p, m.q_dim, m.kv_dim, m.hd, h, seed, layer_id(l, kQ), layer_id(l, kK), layer_id(l, kV),
                         static_cast<int64_t>(m.rank) * m.q_dim, static_cast<int64_t>(m.rank) * m.kv_dim, sd, s);
+        launch_tile_weights(w.qkv, scratch.p, m.qkv_rows, h, s);
         w.o = m.w_o.p + n_o * l;
-        launch_init_normal(w.o, h, m.q_dim, m.q_dim, seed, layer_id(l, kO), 0,
+        launch_init_normal(scratch.p, h, m.q_dim, m.q_dim, seed, layer_id(l, kO), 0,
                            static_cast<int64_t>(m.rank) * m.q_dim, static_cast<int64_t>(c.n_heads) * m.hd, sd, s);
+        launch_tile_weights(w.o, scratch.p, h, m.q_dim, s);
         w.gateup = m.w_gu.p + n_gu * l;
-        launch_init_gateup(w.gateup, m.ffn_l, h, seed, layer_id(l, kGate), layer_id(l, kUp),
+        launch_init_gateup(scratch.p, m.ffn_l, h, seed, layer_id(l, kGate), layer_id(l, kUp),
                            static_cast<int64_t>(m.rank) * m.ffn_l, sd, s);
+        launch_tile_weights(w.gateup, scratch.p, 2 * m.ffn_l, h, s);
         w.down = m.w_down.p + n_down * l;
-        launch_init_normal(w.down, h, m.ffn_l, m.ffn_l, seed, layer_id(l, kDown), 0,
+        launch_init_normal(scratch.p, h, m.ffn_l, m.ffn_l, seed, layer_id(l, kDown), 0,
                            static_cast<int64_t>(m.rank) * m.ffn_l, c.ffn, sd, s);
+        launch_tile_weights(w.down, scratch.p, h, m.ffn_l, s);
     }
     const uint64_t nl = static_cast<uint64_t>(c.n_layers);
-    m.t_qkv = make_tmap_bf16_2d(m.w_qkv.p, nl * m.qkv_rows, h, 128);
-    m.t_o = make_tmap_bf16_2d(m.w_o.p, nl * h, m.q_dim, 128);
-    m.t_gu = make_tmap_bf16_2d(m.w_gu.p, nl * 2 * m.ffn_l, h, 128);
-    m.t_down = make_tmap_bf16_2d(m.w_down.p, nl * h, m.ffn_l, 128);
+    m.t_qkv = make_tmap_bf16_tiled(m.w_qkv.p, nl * n_qkv / (128 * 64));
+    m.t_o = make_tmap_bf16_tiled(m.w_o.p, nl * n_o / (128 * 64));
+    m.t_gu = make_tmap_bf16_tiled(m.w_gu.p, nl * n_gu / (128 * 64));
+    m.t_down = make_tmap_bf16_tiled(m.w_down.p, nl * n_down / (128 * 64));
     m.final_norm.alloc(h);
     launch_fill(m.final_norm.p, h, 1.0f, s);
     m.embed.alloc(static_cast<size_t>(c.vocab) * h);
     launch_init_normal(m.embed.p, c.vocab, h, h, seed, kEmbed, 0, 0, h, sd, s);
+    // the LM head is streamed, so it is tiled too; a tied model keeps the row-major table for the
+    // embedding gather and a tiled copy of its vocab shard for the head
+    m.lm_head_own.alloc(tiled_rows(m.vocab_l) * h);
     if (c.tied_embeddings) {
-        m.lm_head = m.embed.p + static_cast<size_t>(m.rank) * m.vocab_l * h;
+        launch_tile_weights(m.lm_head_own.p, m.embed.p + static_cast<size_t>(m.rank) * m.vocab_l * h, m.vocab_l, h, s);
     } else {
-        m.lm_head_own.alloc(static_cast<size_t>(m.vocab_l) * h);
-        launch_init_normal(m.lm_head_own.p, m.vocab_l, h, h, seed, kLmHead, static_cast<int64_t>(m.rank) * m.vocab_l, 0,
+        launch_init_normal(scratch.p, m.vocab_l, h, h, seed, kLmHead, static_cast<int64_t>(m.rank) * m.vocab_l, 0,
                            h, sd, s);
-        m.lm_head = m.lm_head_own.p;
+        launch_tile_weights(m.lm_head_own.p, scratch.p, m.vocab_l, h, s);
     }
-    m.t_lm = make_tmap_bf16_2d(m.lm_head, m.vocab_l, h, 128);
-    CUDA_CHECK(cudaDeviceSynchronize());
+    m.lm_head = m.lm_head_own.p;
+    m.t_lm = make_tmap_bf16_tiled(m.lm_head, tiled_rows(m.vocab_l) / 128 * (h / 64));
+    CUDA_CHECK(cudaDeviceSynchronize());  // before `scratch` is freed
 }
 
 Transformer::~Transformer() {
@@ -298,7 +310,7 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
         p.kind = kPhGemm;
         p.epi = epi;
         p.wmap = wmap;
-        p.w_row0 = layer >= 0 ? layer * n_out : 0;
+        p.w_row0 = layer >= 0 ? layer * static_cast<int>(tiled_rows(n_out)) : 0;  // tiled images: padded rows
         p.xmap = xmap;
         p.n_out = n_out;
         p.K = K;
@@ -602,13 +614,20 @@ void Transformer::get_weight(const std::string& name, int layer, uint16_t* out, 
         dst.resize(n);
         CUDA_CHECK(cudaMemcpy(dst.data(), src, n * 2, cudaMemcpyDeviceToHost));
     };
+    auto fetch_tiled = [&](const __nv_bfloat16* src, int rows, int K, std::vector<uint16_t>& dst) {  // row-major
+        DevBuf<__nv_bfloat16> tmp;
+        tmp.alloc(static_cast<size_t>(rows) * K);
+        launch_untile_weights(tmp.p, src, rows, K, 0);
+        CUDA_CHECK(cudaDeviceSynchronize());
+        fetch(tmp.p, static_cast<int64_t>(rows) * K, dst);
+    };
     std::vector<uint16_t> v;
     auto need_layer = [&]() -> LayerW& {
         if (layer < 0 || layer >= cfg_.n_layers) throw_invalid("get_weight: layer out of range");
         return m.layers[layer];
     };
     if (name == "embed") fetch(m.embed.p, static_cast<int64_t>(cfg_.vocab) * h, v);
-    else if (name == "lm_head") fetch(m.lm_head, static_cast<int64_t>(m.vocab_l) * h, v);
+    else if (name == "lm_head") fetch_tiled(m.lm_head, m.vocab_l, h, v);
     else if (name == "final_norm") fetch(m.final_norm.p, h, v);
     else if (name == "attn_norm") fetch(need_layer().attn_norm.p, h, v);
     else if (name == "mlp_norm") fetch(need_layer().mlp_norm.p, h, v);
@@ -619,19 +638,20 @@ void Transformer::get_weight(const std::string& name, int layer, uint16_t* out, 
         const int region = name == "q_proj" ? 0 : name == "k_proj" ? 1 : 2;
         const int rows = region == 0 ? m.q_dim : m.kv_dim;
         const size_t off = region == 0 ? 0 : region == 1 ? m.q_dim : m.q_dim + m.kv_dim;
-        std::vector<uint16_t> phys;
-        fetch(need_layer().qkv + off * h, static_cast<int64_t>(rows) * h, phys);
-        v.resize(phys.size());
+        std::vector<uint16_t> all;
+        fetch_tiled(need_layer().qkv, m.qkv_rows, h, all);
+        const uint16_t* phys = all.data() + off * h;
+        v.resize(static_cast<size_t>(rows) * h);
         for (int p = 0; p < rows; ++p) {
             const int logical = (p / m.hd) * m.hd + qkv_perm_dim(p % m.hd, m.hd);
-            std::memcpy(v.data() + static_cast<size_t>(logical) * h, phys.data() + static_cast<size_t>(p) * h, h * 2);
+            std::memcpy(v.data() + static_cast<size_t>(logical) * h, phys + static_cast<size_t>(p) * h, h * 2);
         }
     }
-    else if (name == "o_proj") fetch(need_layer().o, static_cast<int64_t>(h) * m.q_dim, v);
-    else if (name == "down_proj") fetch(need_layer().down, static_cast<int64_t>(h) * m.ffn_l, v);
+    else if (name == "o_proj") fetch_tiled(need_layer().o, h, m.q_dim, v);
+    else if (name == "down_proj") fetch_tiled(need_layer().down, h, m.ffn_l, v);
     else if (name == "gate_proj" || name == "up_proj") {
         std::vector<uint16_t> gu;
-        fetch(need_layer().gateup, static_cast<int64_t>(2) * m.ffn_l * h, gu);
+        fetch_tiled(need_layer().gateup, 2 * m.ffn_l, h, gu);
         const int half = name == "up_proj";
         v.resize(static_cast<size_t>(m.ffn_l) * h);
         for (int64_t p = 0; p < 2LL * m.ffn_l; ++p) {
