@@ -24,8 +24,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUtensorMap map, const uint8_t* w, int U,
-                                                    int KB, int S, int tiles_per_copy) {
+__global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUtensorMap map,
+                                                    const __grid_constant__ CUtensorMap xmap, const uint8_t* w, int U,
+                                                    int KB, int S, int tiles_per_copy, int busy) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint64_t full[32], empty[32];
     const int ci = blockIdx.x, A = gridDim.x;
@@ -40,15 +41,21 @@ __global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUte
     }
     __syncthreads();
     const int step = MODE == 1 ? tiles_per_copy : 1;
+    const int xb = MODE == 3 ? 16 * 64 * 2 : 0;  // MODE 3: tiled weights + a 16-row activation box per stage
     if (threadIdx.x == 0) {  // producer
         int st = 0, ph = 0;
         for (int u = b0; u < b1; u += step) {
             mbar_wait(&empty[st], ph ^ 1);
+            if (busy) {  // emulate per-stage producer bookkeeping
+                const long long t0 = clock64();
+                while (clock64() - t0 < busy) {}
+            }
             const int n = min(step, b1 - u);
-            mbar_arrive_expect_tx(&full[st], n * kTile);
-            uint8_t* dst = smem + static_cast<size_t>(st) * step * kTile;
+            mbar_arrive_expect_tx(&full[st], n * kTile + xb);
+            uint8_t* dst = smem + static_cast<size_t>(st) * step * (kTile + xb);
+            if (MODE == 3) tma_load_2d(dst + kTile, &xmap, &full[st], (u % KB) * 64, 0, kEvictLast);
             if (MODE == 0) tma_load_2d(dst, &map, &full[st], (u % KB) * 64, (u / KB) * 128, kEvictFirst);
-            else if (MODE == 2) tma_load_2d(dst, &map, &full[st], 0, u * 128, kEvictFirst);  // tiled [U*128][64] view
+            else if (MODE >= 2) tma_load_2d(dst, &map, &full[st], 0, u * 128, kEvictFirst);  // tiled [U*128][64] view
             else bulk_g2s(dst, w + static_cast<size_t>(u) * kTile, n * kTile, &full[st], kEvictFirst);
             if (++st == S) { st = 0; ph ^= 1; }
         }
@@ -89,28 +96,42 @@ int main() {
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
+    CUtensorMap xm;
+    uint8_t* x;
+    cudaMalloc(&x, 16 * K * 2);
+    cudaMemset(x, 0, 16 * K * 2);
+    {
+        const cuuint64_t d2[2] = {static_cast<cuuint64_t>(K), 16};
+        const cuuint64_t s2[1] = {static_cast<cuuint64_t>(K * 2)};
+        const cuuint32_t b2[2] = {64, 16};
+        reinterpret_cast<EncodeFn>(p)(&xm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, d2, s2, b2, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     const int KB = static_cast<int>(K / 64), U = static_cast<int>(N / 128) * KB;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaFuncSetAttribute(stream_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    struct Cfg { int mode, per_sm, S, tpc; };
-    const Cfg cfgs[] = {{0, 2, 5, 1}, {1, 2, 5, 1}, {2, 2, 5, 1}, {0, 2, 5, 1}, {1, 2, 5, 1}, {2, 2, 5, 1},
-                        {0, 1, 10, 1}, {1, 1, 10, 1}, {2, 1, 10, 1}, {0, 2, 3, 1}, {1, 2, 3, 1}, {2, 2, 3, 1}};
+    struct Cfg { int mode, per_sm, S, tpc, busy; };
+    const Cfg cfgs[] = {{3, 1, 5, 1, 0},   {3, 1, 5, 1, 200},  {3, 1, 5, 1, 400}, {3, 1, 5, 1, 600},
+                        {3, 1, 5, 1, 800}, {3, 1, 5, 1, 1000}, {3, 2, 5, 1, 400}, {3, 2, 5, 1, 800}};
     for (const Cfg& c : cfgs) {
         const int grid = sms * c.per_sm;
-        const size_t sm_bytes = static_cast<size_t>(c.S) * c.tpc * kTile;
+        const size_t sm_bytes = static_cast<size_t>(c.S) * c.tpc * (kTile + (c.mode == 3 ? 2048 : 0));
         float best = 1e30f, sum = 0.f;
         const int reps = 20;
         for (int r = 0; r < reps + 2; ++r) {
             cudaEventRecord(e0);
-            if (c.mode == 0) stream_kernel<0><<<grid, 64, sm_bytes>>>(map, w, U, KB, c.S, c.tpc);
-            else if (c.mode == 1) stream_kernel<1><<<grid, 64, sm_bytes>>>(map, w, U, KB, c.S, c.tpc);
-            else stream_kernel<2><<<grid, 64, sm_bytes>>>(tmap, w, U, KB, c.S, c.tpc);
+            if (c.mode == 0) stream_kernel<0><<<grid, 64, sm_bytes>>>(map, xm, w, U, KB, c.S, c.tpc, c.busy);
+            else if (c.mode == 1) stream_kernel<1><<<grid, 64, sm_bytes>>>(map, xm, w, U, KB, c.S, c.tpc, c.busy);
+            else if (c.mode == 2) stream_kernel<2><<<grid, 64, sm_bytes>>>(tmap, xm, w, U, KB, c.S, c.tpc, c.busy);
+            else stream_kernel<3><<<grid, 64, sm_bytes>>>(tmap, xm, w, U, KB, c.S, c.tpc, c.busy);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms = 0.f;
@@ -118,8 +139,8 @@ int main() {
             if (r >= 2) { best = ms < best ? ms : best; sum += ms; }
         }
         const cudaError_t err = cudaGetLastError();
-        printf("mode=%s ctas/sm=%d stages=%d tiles/copy=%d smem=%zuKB: best %.1f GB/s mean %.1f GB/s %s\n",
-               c.mode == 0 ? "tma2d" : c.mode == 1 ? "bulk1d" : "tma2d-tiled", c.per_sm, c.S, c.tpc, sm_bytes / 1024, bytes / best / 1e6,
+        printf("busy=%d mode=%s ctas/sm=%d stages=%d tiles/copy=%d smem=%zuKB: best %.1f GB/s mean %.1f GB/s %s\n",
+               c.busy, c.mode == 0 ? "tma2d" : c.mode == 1 ? "bulk1d" : c.mode == 2 ? "tma2d-tiled" : "tiled+x", c.per_sm, c.S, c.tpc, sm_bytes / 1024, bytes / best / 1e6,
                bytes / (sum / reps) / 1e6, err == cudaSuccess ? "" : cudaGetErrorString(err));
     }
     return 0;
