@@ -122,6 +122,9 @@ struct FwdArgs {
     unsigned long long* tp_epoch;
     FwdBatch batch;
 };
+// the kernel takes FwdArgs by value: past 4 KiB of parameters the launch takes a slower parameter
+// path (measured in r1h: +9-13 % on the whole forward)
+static_assert(sizeof(FwdArgs) <= 4096, "FwdArgs must stay within 4 KiB of kernel parameters");
 
 constexpr int kFwdThreads = 192;  // warp 0 TMA producer, warp 1 MMA, warps 2..5 epilogue / aux work
 constexpr int kFwdMiscBytes = 16 * 1024;     // static shared state (barriers, reductions, attention)
