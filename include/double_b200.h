@@ -161,6 +161,9 @@ int dbl_run(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int3
  * ext_emitted[ext_matched+1].  Used to replay the reference's own host loop with the forward
  * excluded (bench.py cpu_baseline / --impl reference).  len receives the full length. */
 int dbl_last_run_log(int32_t* buf, int64_t cap, int64_t* len);
+/* traces_to_jsonl (pipeline.cpp:373-400) of this thread's last single-sequence run / run_ar /
+ * run_serial_sd: also the recovery path when the caller's jsonl buffer was too small (*len = bytes) */
+int dbl_last_run_jsonl(char* buf, int64_t cap, int64_t* len);
 /* run_vanilla_ar (harness.cpp:233-258), greedy: target-only, one forward per token */
 int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,

@@ -94,6 +94,7 @@ PROTOTYPES = {
                           I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p,
                           C.c_int64, I64P],
     "dbl_last_run_log": [I32P, C.c_int64, I64P],
+    "dbl_last_run_jsonl": [C.c_char_p, C.c_int64, I64P],
     "dbl_profile_forward": [VP, C.c_int, C.c_int, C.c_int, F64P],
     "dbl_debug_gemm_trace": [C.POINTER(C.c_uint64), C.c_int64, I32P, I64P, C.POINTER(C.c_int)],
     "dbl_debug_fwd_trace": [C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)],

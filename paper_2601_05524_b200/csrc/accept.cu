@@ -47,6 +47,12 @@ __global__ void target_accept_kernel(const int32_t* __restrict__ argmax, const i
     if (threadIdx.x != 0) return;
     const int L = lane->L, c = lane->c;
     const int n_spec = L - n_committed;
+    if (c + 1 > kMaxRoundTokens) {  // host-validated (depth < kMaxRoundTokens); never write past the record
+        lane->error = 2;
+        rr->target_error = 2;
+        rr->ext_c = 0;
+        return;
+    }
     int rej = -1;
     for (int k = 0; k < n_spec; ++k) {
         if (buf[n_committed + k] != argmax[n_committed - 1 + k]) { rej = k; break; }

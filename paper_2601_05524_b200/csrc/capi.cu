@@ -28,6 +28,7 @@ struct dbl_model_s {
 namespace {
 thread_local std::string g_last_error;
 thread_local std::vector<int32_t> g_last_log;
+thread_local std::string g_last_jsonl;  // traces_to_jsonl of this thread's last single-sequence run
 
 template <class F>
 int guarded(F&& f) {
@@ -58,10 +59,15 @@ int copy_run(const dbl::RunOutput& r, int32_t* out, int cap, int* n_out, dbl_run
     if (n_out) *n_out = static_cast<int>(r.output.size());
     if (metrics) *metrics = r.metrics;
     if (jsonl || jsonl_len) {
-        const std::string js = dbl::traces_to_jsonl(r.traces);
+        // tokens and metrics are already out; the text stays readable through dbl_last_run_jsonl, so a
+        // short buffer costs a second copy, never the (already mutated-store) run
+        g_last_jsonl = dbl::traces_to_jsonl(r.traces);
+        const std::string& js = g_last_jsonl;
         if (jsonl_len) *jsonl_len = static_cast<int64_t>(js.size());
         if (jsonl) {
-            if (static_cast<int64_t>(js.size()) + 1 > jsonl_cap) dbl::throw_invalid("jsonl buffer too small");
+            if (static_cast<int64_t>(js.size()) + 1 > jsonl_cap)
+                dbl::throw_invalid("jsonl buffer too small (need " + std::to_string(js.size() + 1) +
+                                   " bytes; tokens and metrics were written, the text is in dbl_last_run_jsonl)");
             std::memcpy(jsonl, js.c_str(), js.size() + 1);
         }
     }
@@ -360,6 +366,15 @@ int dbl_last_run_log(int32_t* buf, int64_t cap, int64_t* len) {
         if (buf) {
             if (cap < static_cast<int64_t>(g_last_log.size())) dbl::throw_invalid("log buffer too small");
             std::memcpy(buf, g_last_log.data(), g_last_log.size() * 4);
+        }
+    });
+}
+int dbl_last_run_jsonl(char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        if (len) *len = static_cast<int64_t>(g_last_jsonl.size());
+        if (buf) {
+            if (cap < static_cast<int64_t>(g_last_jsonl.size()) + 1) dbl::throw_invalid("jsonl buffer too small");
+            std::memcpy(buf, g_last_jsonl.c_str(), g_last_jsonl.size() + 1);
         }
     });
 }

@@ -96,6 +96,25 @@ void catch_up(Lane& lane, int upto, cudaStream_t s) {
     }
 }
 
+// forward_batch has no row cap (model.cpp:37-53), one device forward carries <= 256 token columns.  A
+// longer forward (a verify over a gamma >= ~23 speculative tail, or a draft segment after a long
+// commit) is split: positions [first, e) — KV and argmax rows — are processed first in <= 256-row
+// chunks, so the forward issued next covers [e, L + c_max) only.  Batch invariance makes every row
+// bitwise the row of the unsplit forward.  Must run before the lane's lookup (set_state resets it).
+// Returns the first position the next forward processes (its row bound is L + c_max - that).
+int split_long_forward(Lane& lane, int L, int row0, int c_max, bool sampled, cudaStream_t s) {
+    const int first = std::min(lane.kv_len, row0);
+    if (!lane.model.has_kv()) return first;
+    const int cap = std::min(kPrefillChunk, lane.model.max_forward_tokens());
+    if (L + c_max - first <= cap) return first;
+    if (sampled) throw_runtime("sampled forward exceeds 256 consumed rows (gamma * (depth + 1) too large)");
+    const int e = L + c_max - cap;
+    lane.kv_len = first;  // [first, kv_len) is recomputed with its rows (identical KV rewritten)
+    catch_up(lane, e, s);
+    lane.set_state(L, 0, e, e, s);
+    return e;
+}
+
 struct Timer {
     cudaEvent_t a = nullptr, b = nullptr;
     Timer() {
@@ -161,7 +180,8 @@ const char* source_name(int s) {  // to_string(LookupSource), datastore.cpp:33-4
 void validate_opts(const dbl_pipeline_options& o) {  // pipeline.cpp:267-272, pipeline.hpp:24-28
     if (o.gamma < 1) throw_invalid("gamma must be >= 1");
     if (o.depth < 1) throw_invalid("depth must be >= 1");
-    if (o.depth > 65535) throw_invalid("depth must be <= 65535");
+    // the round record holds <= kMaxRoundTokens target candidates + the continuation (RoundResult)
+    if (o.depth > kMaxRoundTokens - 1) throw_invalid("depth must be <= " + std::to_string(kMaxRoundTokens - 1));
     if (o.gamma > kMaxSegs) throw_invalid("gamma exceeds the device chain record");
     if (o.t_target < 0.0 || o.t_draft <= 0.0 || o.t_lookup < 0.0 || o.t_sync < 0.0)
         throw_invalid("latency values out of range");
@@ -481,9 +501,10 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
             bounds.clear();
             for (Seq* qp : act) {
                 Seq& q = *qp;
+                const int first = j == 0 ? split_long_forward(*q.dl, q.L, q.L - 1, c_max, q.smp != nullptr, S.draft) : 0;
                 if (o.draft_retrieval) q.st->lookup_lane(q.dl->buf.p, q.dl->state, d, S.draft);
                 dls.push_back(q.dl.get());
-                bounds.push_back(j == 0 ? q.L + c_max - std::min(q.dl->kv_len, q.L - 1) : 1 + c_max);
+                bounds.push_back(j == 0 ? q.L + c_max - first : 1 + c_max);
             }
             if (act[0]->smp) {
                 std::vector<int> rows;
@@ -508,9 +529,10 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
         bounds.clear();
         for (Seq* qp : act) {
             Seq& q = *qp;
+            const int first = split_long_forward(*q.tl, q.L, q.nc - 1, tc_max, q.smp != nullptr, S.target);
             if (o.target_retrieval) q.st->lookup_lane(q.tl->buf.p, q.tl->state, d, S.target);
             tls.push_back(q.tl.get());
-            bounds.push_back(q.L + tc_max - std::min(q.tl->kv_len, q.nc - 1));
+            bounds.push_back(q.L + tc_max - first);
         }
         CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
         if (act[0]->smp) {
@@ -964,9 +986,10 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
         // rng_d / rng_v = derive_rng(seed, round, 0 / 2) (harness.cpp:281-282)
         if (smp) launch_derive_rngs(smp->rng.p, smp->seed, static_cast<uint64_t>(round), S.main);
         for (int j = 0; j < gamma; ++j) {
-            if (use_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.main);
             const int c_max = use_retrieval ? d : 0;
-            const int bound = j == 0 ? nc + c_max - std::min(dl.kv_len, nc - 1) : 1 + c_max;
+            const int first = j == 0 ? split_long_forward(dl, nc, nc - 1, c_max, smp != nullptr, S.main) : 0;
+            if (use_retrieval) st.lookup_lane(dl.buf.p, dl.state, d, S.main);
+            const int bound = j == 0 ? nc + c_max - first : 1 + c_max;
             if (smp) {
                 dm.dists(dl, bound, c_max + 1, smp->ddist.p, S.main);
                 launch_draft_accept_sampled(dl, rr_dev, j, nc, smp->ddist.p, smp->chain[0].p, smp->chain_rows,
@@ -986,7 +1009,7 @@ RunOutput run_serial_sd(Model& dm, Model& tm, DeviceStore& st, const int32_t* pr
         const int lcp = tio.sync_tokens(X, S.main);
         tl.kv_len = std::min(tl.kv_len, lcp);
         tl.set_state(nc + n_chain, 0, tl.kv_len, nc - 1, S.main);
-        const int tbound = nc + n_chain - std::min(tl.kv_len, nc - 1);
+        const int tbound = nc + n_chain - split_long_forward(tl, nc + n_chain, nc - 1, 0, smp != nullptr, S.main);
         if (smp) {
             tm.dists(tl, tbound, n_chain + 1, smp->tdist.p, S.main);
             launch_target_accept_sampled(tl, nc, rr_dev, smp->tdist.p, smp->chain[0].p, smp->rng.p + 1,
@@ -1080,17 +1103,24 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     X.insert(X.end(), cands, cands + c);
     io.sync_tokens(X, S.main);
     catch_up(lane, L - 1, S.main);
-    lane.set_state(L, c, lane.kv_len, L - 1, S.main);
     DevBuf<float> lg;
     DevBuf<double> dd;
-    if (out_dists) {  // the rows the sampled loop consumes (Model::dists)
-        dd.alloc(static_cast<size_t>(c + 1) * m.vocab());
-        m.dists(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), c + 1, dd.p, S.main);
-    } else if (out_logits) {
-        lg.alloc(static_cast<size_t>(c + 1) * m.vocab());
-        m.logits(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), lg.p, S.main);
-    } else {
-        m.forward(lane, c + 1 + (L - 1 - std::min(lane.kv_len, L - 1)), S.main);
+    if (out_dists) dd.alloc(static_cast<size_t>(c + 1) * m.vocab());
+    else if (out_logits) lg.alloc(static_cast<size_t>(c + 1) * m.vocab());
+    // rows [L-1, L+c): one forward, or (forward_batch has no row cap, model.cpp:37-53) consecutive
+    // <= 256-row forwards — batch invariance makes each row bitwise the one-forward row
+    const int cap = m.has_kv() ? std::min(kPrefillChunk, m.max_forward_tokens()) : c + 1;
+    for (int p0 = L - 1; p0 < L + c;) {
+        const int p1 = std::min(L + c, p0 + cap);
+        const int first = std::min(lane.kv_len, p0);
+        if (p1 == L + c) lane.set_state(L, c, lane.kv_len, p0, S.main);  // the last piece: L + c = p1
+        else lane.set_state(p1, 0, lane.kv_len, p0, S.main);
+        const size_t at = static_cast<size_t>(p0 - (L - 1)) * m.vocab();
+        if (out_dists) m.dists(lane, p1 - first, p1 - p0, dd.p + at, S.main);
+        else if (out_logits) m.logits(lane, p1 - first, lg.p + at, S.main);
+        else m.forward(lane, p1 - first, S.main);
+        lane.kv_len = std::max(lane.kv_len, p1);
+        p0 = p1;
     }
     DevBuf<int32_t> rows(c + 1);
     gather_rows_kernel<<<1, 256, 0, S.main>>>(lane.argmax.p, L - 1, c + 1, rows.p);

@@ -146,6 +146,11 @@ __device__ __forceinline__ void l2_warm(const void* base, long long bytes, int p
     }
 }
 
+// the embedding gather's range check (the table covers the unsharded vocab: vocab_l per rank)
+__device__ __forceinline__ bool valid_token(int tok, const FwdArgs& a) {
+    return static_cast<unsigned>(tok) < static_cast<unsigned>(a.vocab_l * a.tp_world);
+}
+
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 // 32 columns x 32 lanes -> lane l holds the sum over the warp's lanes of column l (fixed tree)
@@ -979,7 +984,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         };
         if constexpr (!kB) {  // warm L2: this forward's embedding rows and RoPE rows (tiny, cold, on the critical path)
             const int gt = c * 128 + et, GT = G * 128;
-            for (int t = gt; t < T; t += GT) l2_warm(a.embed + static_cast<long long>(a.buf[start + t]) * h, h * 2, 0, 1);
+            for (int t = gt; t < T; t += GT) {
+                const int tok = a.buf[start + t];
+                l2_warm(a.embed + static_cast<long long>(valid_token(tok, a) ? tok : 0) * h, h * 2, 0, 1);
+            }
             if (gt == GT - 1) l2_warm(a.rope + static_cast<long long>(start) * (a.hd / 2), T * (a.hd / 2) * 8LL, 0, 1);
         }
         for (int p = 0; p < a.n_ph; ++p) {
@@ -1008,6 +1016,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                             tok = a.buf[start + t];
                         }
                     }
+                    if (!valid_token(tok, a)) tok = 0;  // ids outside the vocab (a draft's or a datastore's) are
+                                                        // never accepted; their rows only need to be safe
                     const int col = mt * kBM + lane * 4;
                     const uint2 raw = *reinterpret_cast<const uint2*>(a.embed + static_cast<long long>(tok) * h + col);
                     const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);

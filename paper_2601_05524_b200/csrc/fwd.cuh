@@ -61,8 +61,8 @@ struct FwdPhase {
 // NVLink, or an IPC mapping).  Written remotely, read locally.
 constexpr int kMaxTpRanks = 8;
 struct TpPeers {
-    float* xch[kMaxTpRanks];                 // [src rank][h/128 tiles][256 cols][128 rows] fp32 partial tiles
-    unsigned long long* xflag[kMaxTpRanks];  // [src rank][h/128 tiles] tags
+    float* xch[kMaxTpRanks];                 // [parity][src rank][h/128 tiles][256 cols][128 rows] fp32 partials
+    unsigned long long* xflag[kMaxTpRanks];  // [parity][src rank][h/128 tiles] tags (parity: O 0, down 1)
     float2* axch[kMaxTpRanks];               // [src rank][256] (max logit, global id) per token
     unsigned long long* aflag[kMaxTpRanks];  // [src rank] tags
 };

@@ -328,6 +328,12 @@ __global__ void __launch_bounds__(kNT) target_accept_sampled_kernel(
     rng_store(rng_t, gt);
     rng_store(rng_v, gv);
     if (threadIdx.x != 0) return;
+    if (c + 1 > kMaxRoundTokens) {  // host-validated; never write past the round record
+        lane->error = kSampCapacity;
+        rr->target_error = kSampCapacity;
+        rr->ext_c = 0;
+        return;
+    }
     rr->tgt_rej = rej;
     rr->tgt_correction = corr;
     for (int i = 0; i < s; ++i) rr->ext_emitted[i] = buf[L + i];

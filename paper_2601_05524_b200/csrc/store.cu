@@ -252,8 +252,7 @@ DeviceStore::DeviceStore(int max_order, int depth, int device)
     DeviceGuard g(device);
     CUDA_CHECK(cudaMalloc(&desc_dev_, sizeof(StoreDesc)));
     CUDA_CHECK(cudaMemset(desc_dev_, 0, sizeof(StoreDesc)));
-    staging_.alloc(1 << 16);  // grown on demand (insert)
-    CUDA_CHECK(cudaEventCreateWithFlags(&staging_done_, cudaEventDisableTiming));
+    for (Staging& r : staging_) r.buf.alloc(1 << 16);  // grown on demand (insert)
     for (int l = 0; l < 3; ++l) {
         layers_[l].max_order = max_order;
         grow(l, 1024, 64, 0);
@@ -267,7 +266,26 @@ DeviceStore::~DeviceStore() {
     cudaSetDevice(device_);
     cudaDeviceSynchronize();
     if (desc_dev_) cudaFree(desc_dev_);
-    if (staging_done_) cudaEventDestroy(staging_done_);
+    for (Staging& r : staging_)
+        for (auto& e : r.pend) cudaEventDestroy(e.second);
+}
+
+// Insert payloads go through two mapped pinned rings used alternately.  Switching to a ring waits (on
+// the host, per stream that appended from it) only for that ring's own earlier append kernels — not
+// for the device: a wrap never stalls the decode loop's other streams.
+void DeviceStore::Staging::drain() {
+    for (auto& e : pend) CUDA_CHECK(cudaEventSynchronize(e.second));
+}
+void DeviceStore::Staging::mark(cudaStream_t s) {
+    for (auto& e : pend)
+        if (e.first == s) {
+            CUDA_CHECK(cudaEventRecord(e.second, s));
+            return;
+        }
+    cudaEvent_t ev;
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventRecord(ev, s));
+    pend.emplace_back(s, ev);
 }
 
 void DeviceStore::push_desc(cudaStream_t) {}
@@ -339,20 +357,21 @@ void DeviceStore::insert(int l, const int32_t* tokens, int n, long step, cudaStr
         throw_runtime("datastore layer exceeds 2^24 tokens/sequences");
     DeviceGuard g(device_);
     grow(l, h.n_tokens + n, h.n_seqs + 1, s);
-    if (static_cast<size_t>(n) > staging_.n || staging_at_ + n > staging_.n) {
-        // ring wrap / growth: every payload in flight (any stream) must have been consumed first
-        CUDA_CHECK(cudaDeviceSynchronize());
-        if (static_cast<size_t>(n) > staging_.n) {
-            size_t cap = staging_.n;
-            while (cap < static_cast<size_t>(n)) cap *= 2;
-            staging_.alloc(cap);
-        }
+    if (staging_at_ + n > staging_[staging_cur_].buf.n) {
+        // ring full: continue in the other ring once its own earlier payloads have been consumed
+        Staging& nx = staging_[staging_cur_ ^ 1];
+        nx.drain();
+        size_t cap = std::max(nx.buf.n, staging_[staging_cur_].buf.n);
+        while (cap < static_cast<size_t>(n)) cap *= 2;
+        if (cap > nx.buf.n) nx.buf.alloc(cap);  // nothing of nx is in flight any more
+        staging_cur_ ^= 1;
         staging_at_ = 0;
     }
-    int32_t* host = staging_.p + staging_at_;
-    std::memcpy(host, tokens, static_cast<size_t>(n) * 4);
-    append_kernel<<<1, 256, 0, s>>>(desc_dev_, l, staging_.dev() + staging_at_, n, step);
+    Staging& rg = staging_[staging_cur_];
+    std::memcpy(rg.buf.p + staging_at_, tokens, static_cast<size_t>(n) * 4);
+    append_kernel<<<1, 256, 0, s>>>(desc_dev_, l, rg.buf.dev() + staging_at_, n, step);
     CUDA_LAUNCH_CHECK();
+    rg.mark(s);
     staging_at_ += static_cast<size_t>(n);
     h.n_tokens += n;
     h.n_seqs += 1;

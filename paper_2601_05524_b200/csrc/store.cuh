@@ -13,6 +13,7 @@
 // over the context.  Inserts are O(len) appends — no index maintenance — which is what makes the
 // per-round datastore update (pipeline.cpp:146-184) a single tiny kernel.
 #pragma once
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -87,9 +88,15 @@ class DeviceStore {
     bool rejected_enabled_ = true;
     HostLayer layers_[3];
     StoreDesc* desc_dev_ = nullptr;
-    PinBuf<int32_t> staging_;  // mapped pinned ring for insert payloads
+    struct Staging {  // mapped pinned ring for insert payloads + the last append per stream using it
+        PinBuf<int32_t> buf;
+        std::vector<std::pair<cudaStream_t, cudaEvent_t>> pend;
+        void drain();
+        void mark(cudaStream_t s);
+    };
+    Staging staging_[2];
+    int staging_cur_ = 0;
     size_t staging_at_ = 0;
-    cudaEvent_t staging_done_ = nullptr;
 };
 
 }  // namespace dbl

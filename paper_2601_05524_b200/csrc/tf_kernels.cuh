@@ -1,6 +1,5 @@
-// Non-GEMM kernels of the verify forward (embedding, RMSNorm, QK-norm + RoPE + paged-KV append,
-// split-KV attention + ordered combine, weight init).  Every reduction has a fixed order that depends
-// only on the row/position, never on how many tokens the forward carries (batch invariance).
+// Transformer set-up kernels: seeded random init of every weight tensor and the tiled weight images the
+// stream forward (fwd.cu) reads; plus the KV page / attention chunk constants it shares.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -12,26 +11,6 @@ namespace dbl {
 constexpr int kPage = 64;       // KV page (tokens)
 constexpr int kAttnChunk = 64;  // keys per split-KV chunk = one page (fixed => batch invariant)
 
-struct KVView {  // one layer of a lane's paged KV cache
-    __nv_bfloat16* k;  // [n_pages][n_kv][kPage][hd]
-    __nv_bfloat16* v;
-    const int32_t* page_table;  // logical page -> physical page
-    int n_kv, hd;
-};
-
-// resid[t][:] = float(E[buf[start+t]]) for t < tp (token 0 past the valid rows)
-void launch_embed(const __nv_bfloat16* E, int hidden, const int32_t* buf, const LaneState* lane, int tp,
-                  float* resid, cudaStream_t s);
-// out[t][:] = bf16(x[t] * rsqrt(mean(x^2) + eps) * w), t < tp
-void launch_rmsnorm(const float* x, const __nv_bfloat16* w, int hidden, float eps, int tp, __nv_bfloat16* out,
-                    cudaStream_t s);
-// per valid token: q/k per-head RMSNorm (optional), RoPE (rotate-half), q -> qbuf, k/v -> KV cache
-void launch_qkv_post(const __nv_bfloat16* qkv, int n_heads, int n_kv, int hd, const __nv_bfloat16* qn,
-                     const __nv_bfloat16* kn, float eps, float theta, const LaneState* lane, KVView kv,
-                     __nv_bfloat16* qbuf, int tp, cudaStream_t s);
-// causal attention of the valid tokens over KV positions [0, pos]; partials per 256-key chunk
-void launch_attention(const __nv_bfloat16* qbuf, int n_heads, int n_kv, int hd, KVView kv, const LaneState* lane,
-                      int tp, int max_chunks, float* part_o, float* part_ml, __nv_bfloat16* out, cudaStream_t s);
 // weights ~ N(0, std) from (seed, tensor, logical index); rows [r0, r0+rows) x cols [c0, c0+cols) of a
 // logical [R, C] tensor written to dst (row stride ld)
 void launch_init_normal(__nv_bfloat16* dst, int rows, int cols, int ld, uint64_t seed, uint64_t tensor,
@@ -56,7 +35,5 @@ constexpr int kWTileRows = 128, kWTileK = 64;
 inline int64_t tiled_rows(int64_t rows) { return (rows + kWTileRows - 1) / kWTileRows * kWTileRows; }
 void launch_tile_weights(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, cudaStream_t s);
 void launch_untile_weights(__nv_bfloat16* dst, const __nv_bfloat16* src, int rows, int K, cudaStream_t s);
-void launch_forward_begin(LaneState* lane, cudaStream_t s);  // lane.start = min(kv_len, row0)
-void launch_forward_end(LaneState* lane, cudaStream_t s);    // lane.kv_len = L + c
 
 }  // namespace dbl

@@ -367,36 +367,3 @@ def run_pipelined(cfg: ExperimentConfig, setup: ExperimentSetup, draft_retrieval
                            t_lookup=cfg.t_lookup, t_sync=cfg.t_sync, temperature=cfg.temperature,
                            rng_seed=cfg.seed, engine=cfg.engine)
     return run(setup.draft.device(device), setup.target.device(device), st, setup.prompt, cfg.max_new_tokens, opts)
-
-
-def ablate(cfg: ExperimentConfig, device: int = 0):  # harness.cpp:436-458
-    s = build_setup(cfg)
-    rows = [_row("double", run_pipelined(cfg, s, True, True, cfg.rejected_cache, device)),
-            _row("wo_draft_retrieval", run_pipelined(cfg, s, False, True, cfg.rejected_cache, device)),
-            _row("wo_target_retrieval", run_pipelined(cfg, s, True, False, cfg.rejected_cache, device)),
-            _row("wo_rejected_cache", run_pipelined(cfg, s, True, True, False, device))]
-    import dataclasses
-    c = dataclasses.replace(cfg, prior_rounds=0)
-    rows.append(_row("wo_prior", run_pipelined(c, s, True, True, cfg.rejected_cache, device)))
-    return rows
-
-
-def sweep_depth(cfg: ExperimentConfig, depths, device: int = 0):  # harness.cpp:460-472
-    import dataclasses
-    s = build_setup(cfg)
-    return [_row(f"d={d}", run_pipelined(dataclasses.replace(cfg, depth=d), s, True, True, cfg.rejected_cache, device))
-            for d in depths]
-
-
-def emit_report(rows, fmt: str = "text") -> str:  # harness.cpp:474-500
-    if fmt == "csv":
-        out = ["method,m,amt,speedup,hit_rate,tokens,clock\n"]
-        out += ["%s,%.6g,%.6g,%.6g,%.6g,%d,%.6g\n" % (r.label, r.m, r.amt, r.speedup, r.hit_rate, r.tokens, r.clock)
-                for r in rows]
-        return "".join(out)
-    if fmt == "text":
-        out = ["%-22s %10s %8s %9s %9s %8s %10s\n" % ("method", "M", "AMT", "speedup", "hit_rate", "tokens", "clock")]
-        out += ["%-22s %10.4f %8.4f %9.4f %9.4f %8d %10.2f\n" % (r.label, r.m, r.amt, r.speedup, r.hit_rate, r.tokens,
-                                                               r.clock) for r in rows]
-        return "".join(out)
-    raise InvalidArgument("format must be csv|text")

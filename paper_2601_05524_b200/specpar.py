@@ -463,8 +463,12 @@ class RunResult:  # pipeline.hpp:84-88
 
 
 def _finish(rc, out, n, m, js, jl, want_jsonl) -> RunResult:
-    check(rc)
     import json
+    if rc != 0 and want_jsonl and lib().dbl_last_error().decode().startswith("jsonl buffer too small"):
+        # tokens and metrics were written; the traces outgrew the guess: fetch them at their size
+        js = C.create_string_buffer(int(jl.value) + 1)
+        rc = lib().dbl_last_run_jsonl(js, len(js), C.byref(jl))
+    check(rc)
     text = js.value.decode() if want_jsonl else ""
     return RunResult(out[:n.value].tolist(), m.as_dict(), text,
                      [json.loads(x) for x in text.splitlines()] if want_jsonl else [])

@@ -3,6 +3,12 @@
 It mirrors the kernels' definition: bf16 weights, fp32 accumulation, bf16 rounding at the same
 points (normed activations, qkv, roped q/k, attention output, SiLU*up), fp32 residual stream and
 logits.  Weights are read back from the device model through dbl_transformer_get_weight.
+
+fold=True (default) mirrors the kernel's folded RMSNorm exactly: the norm weights of this random-init
+family are 1, so RMSNorm(x) @ W^T == rstd(x) * (x @ W^T); the kernel feeds bf16(x) (the residual's
+bf16 copy) to the tensor cores and scales the fp32 GEMM output column by rstd (fwd.cuh), where an
+HF-style reference rounds bf16(x * rstd).  fold=False is that HF-style rounding point; the two differ
+by bf16 re-rounding noise only (~1 % of max|logit| on 2-layer Qwen3-14B shapes).
 """
 from __future__ import annotations
 
@@ -16,11 +22,13 @@ def _bf(x: torch.Tensor) -> torch.Tensor:
 
 
 class RefTransformer:
-    def __init__(self, model, preset_cfg):
+    def __init__(self, model, preset_cfg, device: str = "cpu", fold: bool = True):
         c = preset_cfg
         self.c = c
+        self.dev = device
+        self.fold = fold
         L, h, f, nh, nkv, hd, V = (c.n_layers, c.hidden, c.ffn, c.n_heads, c.n_kv_heads, c.head_dim, c.vocab)
-        t = lambda a: torch.from_numpy(a.copy())  # noqa: E731
+        t = lambda a: torch.from_numpy(a.copy()).to(device)  # noqa: E731
         self.embed = t(model.weight("embed", -1, (V, h)))
         self.lm = t(model.weight("lm_head", -1, (V, h)))
         self.final_norm = t(model.weight("final_norm", -1, (h,)))
@@ -42,6 +50,13 @@ class RefTransformer:
                 d["kn"] = t(model.weight("k_norm", l, (hd,)))
             self.layers.append(d)
 
+    def _norm_mm(self, x, w, W, eps):
+        """fp32 RMSNorm(x; w) @ W^T at the kernel's (fold) or the HF-style rounding point."""
+        if self.fold:
+            assert bool((w == 1).all()), "fold mode needs unit norm weights (the kernel folds them)"
+            return (_bf(x) @ W.T) * torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
+        return self._rms(x, w, eps) @ W.T
+
     def _rms(self, x, w, eps):
         r = torch.rsqrt((x * x).mean(-1, keepdim=True) + eps)
         return _bf(x * r * w)
@@ -49,27 +64,29 @@ class RefTransformer:
     def _rope(self, x, pos):  # x [T, H, hd]
         hd = x.shape[-1]
         half = hd // 2
-        i = torch.arange(half, dtype=torch.float32)
-        inv = torch.pow(torch.tensor(self.c.rope_theta, dtype=torch.float32), -2.0 * i / hd)
-        ang = pos[:, None].to(torch.float32) * inv[None, :]
-        cs, sn = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+        # the device RoPE table is computed in fp64 and rounded to fp32 (transformer.cu make_cache)
+        i = torch.arange(half, dtype=torch.float64, device=x.device)
+        inv = torch.pow(torch.tensor(self.c.rope_theta, dtype=torch.float64, device=x.device), -2.0 * i / hd)
+        ang = pos[:, None].to(torch.float64) * inv[None, :]
+        cs, sn = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
         a, b = x[..., :half], x[..., half:]
         return _bf(torch.cat([a * cs - b * sn, b * cs + a * sn], dim=-1))
 
     @torch.no_grad()
-    def logits(self, tokens) -> torch.Tensor:
-        """fp32 logits for every position of `tokens` (full causal recompute)."""
+    def logits(self, tokens, first_row: int = 0) -> torch.Tensor:
+        """fp32 logits for positions [first_row, len(tokens)) of `tokens` (full causal recompute)."""
         c = self.c
         T = len(tokens)
         nh, nkv, hd, eps = c.n_heads, c.n_kv_heads, c.head_dim, c.rms_eps
-        x = self.embed[torch.tensor(tokens)].clone()
-        pos = torch.arange(T)
-        mask = torch.tril(torch.ones(T, T, dtype=torch.bool))
+        dev = self.dev
+        x = self.embed[torch.tensor(tokens, device=dev)].clone()
+        pos = torch.arange(T, device=dev)
+        mask = torch.tril(torch.ones(T, T, dtype=torch.bool, device=dev))
         for d in self.layers:
-            xn = self._rms(x, d["attn_norm"], eps)
-            q = _bf(xn @ d["q"].T).view(T, nh, hd)
-            k = _bf(xn @ d["k"].T).view(T, nkv, hd)
-            v = _bf(xn @ d["v"].T).view(T, nkv, hd)
+            an = d["attn_norm"]
+            q = _bf(self._norm_mm(x, an, d["q"], eps)).view(T, nh, hd)
+            k = _bf(self._norm_mm(x, an, d["k"], eps)).view(T, nkv, hd)
+            v = _bf(self._norm_mm(x, an, d["v"], eps)).view(T, nkv, hd)
             if c.qk_norm:
                 q = self._rms(q, d["qn"], eps)
                 k = self._rms(k, d["kn"], eps)
@@ -82,9 +99,8 @@ class RefTransformer:
             p = torch.softmax(s, dim=-1)
             a = _bf(torch.einsum("hts,shd->thd", p, v)).reshape(T, nh * hd)
             x = x + a @ d["o"].T
-            xn = self._rms(x, d["mlp_norm"], eps)
-            gg, uu = xn @ d["g"].T, xn @ d["u"].T
+            mn = d["mlp_norm"]
+            gg, uu = self._norm_mm(x, mn, d["g"], eps), self._norm_mm(x, mn, d["u"], eps)
             act = _bf(gg / (1 + torch.exp(-gg)) * uu)
             x = x + act @ d["d"].T
-        xn = self._rms(x, self.final_norm, eps)
-        return xn @ self.lm.T
+        return self._norm_mm(x[first_row:], self.final_norm, self.lm, eps).cpu()

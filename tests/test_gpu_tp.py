@@ -78,3 +78,23 @@ def test_double_with_tp_target_equals_tp_ar(dbl):
         r = dbl.run(drf, tgt, st, prompt, 96, dbl.PipelineOptions(gamma=gamma, depth=10))
         ar = dbl.run_vanilla_ar(tgt, prompt, 96)
         assert r.output == ar.output
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_double_transformer_draft_with_tp_target(dbl, world):
+    """A transformer draft beside a TP=2/4/8 target whose shards share this GPU: more than two
+    persistent forwards cannot co-run, so the decoder runs both workers on one stream (same round
+    results by construction, pipeline.cpp:239-261) — DOUBLE == target-only AR with the TP target."""
+    tcfg = dbl.transformer_config("tiny-qwen", seed=13, max_seq=2048, n_kv_heads=8, n_heads=8)
+    tgt = dbl.TpTransformer(tcfg, devices=[0] * world)
+    drf = dbl.Transformer(dbl.transformer_config("tiny-qwen-draft", seed=14, max_seq=2048))
+    rng = random.Random(world)
+    base = [rng.randrange(1, tcfg.vocab - 1) for _ in range(40)]
+    prior = [(base * 3)[i:i + 64] for i in range(0, 30, 3)]
+    prompt = prior[0][:24]
+    ar = dbl.run_vanilla_ar(tgt, prompt, 64)
+    for gamma in (1, 3):
+        st = dbl.HierarchicalDatastore(3, 10)
+        dbl.build_prior(st, prior, 10)
+        r = dbl.run(drf, tgt, st, prompt, 64, dbl.PipelineOptions(gamma=gamma, depth=10))
+        assert r.output == ar.output, (world, gamma)

@@ -130,3 +130,37 @@ def test_long_prompt_prefill_chunks(dbl):
     st = dbl.HierarchicalDatastore(3, 10)
     r = dbl.run(m, m, st, ctx, 20, dbl.PipelineOptions(gamma=2))
     assert r.output == ar.output
+
+
+def test_forward_batch_above_256_rows(dbl):
+    """forward_batch has no row cap (model.cpp:37-53): 300 candidates = 301 rows run as <= 256-row
+    forwards, each row bitwise the single-row forward's (batch invariance)."""
+    m, cfg = make(dbl, "tiny-qwen", 5)
+    rng = random.Random(3)
+    ctx = [rng.randrange(cfg.vocab) for _ in range(50)]
+    cands = [rng.randrange(cfg.vocab) for _ in range(300)]
+    got = dbl.forward_logits(m, ctx, cands)
+    assert got.shape[0] == 301
+    assert dbl.forward_batch(m, ctx, cands) == got.argmax(axis=1).tolist()
+    for k in (0, 100, 255, 256, 257, 300):
+        assert np.array_equal(dbl.forward_logits(m, ctx + cands[:k], [])[0], got[k]), k
+
+
+def test_verify_forward_above_256_rows_is_split(dbl):
+    """With gamma = 24-64, d = 10-40 and a self-draft whose prior holds its own greedy stream, draft
+    segments retrieve long runs of correct candidates and the kept speculative tail passes one
+    forward's 256 token columns: the decoder splits the verify (decoder.cu split_long_forward) and the
+    output is still target-only greedy AR."""
+    tgt, tcfg = make(dbl, "tiny-qwen", 21)
+    prompt = list(range(1, 30))
+    ar = dbl.run_vanilla_ar(tgt, prompt, 900)
+    stream = prompt + ar.output
+    prior = [stream[i:i + 64] for i in range(0, len(stream) - 64, 8)]
+    longest = 0
+    for gamma, depth in ((24, 10), (24, 40), (64, 40)):
+        st = dbl.HierarchicalDatastore(3, depth)
+        dbl.build_prior(st, prior, len(prior))
+        r = dbl.run(tgt, tgt, st, prompt, 900, dbl.PipelineOptions(gamma=gamma, depth=depth))
+        assert r.output == ar.output, (gamma, depth)
+        longest = max(longest, max(t["pending"] + depth + 1 for t in r.traces))
+    assert longest > 256, f"workload never needed a split forward ({longest} rows)"
