@@ -217,6 +217,103 @@ int dbl_guided_output(const int32_t* draft, int n_draft, const double* draft_pro
                       const int64_t* guide_off, int n_guide_rows, int first_reject, double temperature, dbl_rng_t r,
                       int32_t* committed, int cap, int* n_committed, int* accepted_len, int* kind);
 
+/* ===================================================================== model-level helpers
+ * tempered / argmax_token / sample (model.hpp:40-48, model.cpp:55-97) over explicit fp64 rows.
+ * argmax is a block reduction (warp shuffles, ties -> lowest id, RuntimeError when the max <= 0);
+ * tempered/sample keep the reference's summation order (single-thread fp64: bit-identical draws). */
+int dbl_tempered(const double* dist, int n, double temperature, int device, double* out);    /* model.cpp:55-68 */
+int dbl_argmax_token(const double* dist, int n, int device, int32_t* out);                    /* model.cpp:70-81 */
+/* argmax_token of n_rows ragged rows (row r = probs[off[r] .. off[r+1])), one CTA per row, one launch */
+int dbl_argmax_rows(const double* probs, const int64_t* off, int n_rows, int device, int32_t* out);
+int dbl_sample(const double* dist, int n, double temperature, dbl_rng_t r, int device, int32_t* out); /* model.cpp:83-97 */
+
+/* ===================================================================== drafter
+ * Replaces accept_with_model / retrieval_forward / iterative_draft / measure_amt (speculation.hpp:34-59,
+ * speculation.cpp:7-94).  RetrievalResult: emitted[matched_len + 1] tokens, probs = the model's effective
+ * row at every emitted position (greedy: the rows themselves; T > 0: tempered), source. */
+typedef struct {
+    int matched_len;
+    int n_emitted;
+    int source;   /* dbl_source (DBL_SRC_MISS when retrieval is off) */
+    int n_probs;  /* rows written to probs */
+} dbl_retrieval_result;
+/* rows: n_dists (= c + 1) ragged fp64 rows; probs (may be NULL) receives rows 0..n_probs of the same
+ * lengths, flattened; r may be NULL at temperature 0 (no draw is consumed) */
+int dbl_accept_with_model(const double* dists, const int64_t* dist_off, int n_dists, const int32_t* cands, int c,
+                          double temperature, dbl_rng_t r, int device, int32_t* emitted, int emitted_cap,
+                          double* probs, int64_t probs_cap, dbl_retrieval_result* res);
+/* lookup (if use_retrieval) -> one forward_batch of model m over ctx ⊕ candidates -> accept_with_model;
+ * probs rows are vocab long.  st may be NULL when use_retrieval is 0. */
+int dbl_retrieval_forward(dbl_model_t m, dbl_store_t st, const int32_t* ctx, int L, int depth, double temperature,
+                          dbl_rng_t r, int use_retrieval, int32_t* emitted, int emitted_cap, double* probs,
+                          int64_t probs_cap, dbl_retrieval_result* res);
+/* gamma chained retrieval forwards over the growing context: segs[gamma], tokens = the flattened
+ * emissions (DraftChain::tokens), probs (may be NULL) = one vocab row per token */
+int dbl_iterative_draft(dbl_model_t m, dbl_store_t st, const int32_t* ctx, int L, int gamma, int depth,
+                        double temperature, dbl_rng_t r, int use_retrieval, dbl_retrieval_result* segs,
+                        int32_t* tokens, int tokens_cap, int* n_tokens, double* probs, int64_t probs_cap);
+int dbl_measure_amt(const int32_t* matched_lens, int n, double* out);                          /* speculation.cpp:88-94 */
+
+/* ===================================================================== decoder state machine
+ * PipelineState / RoundTrace / rollback / run_round / compute_metrics / traces_to_jsonl / write_traces
+ * (pipeline.hpp:46-115, pipeline.cpp:15-400). */
+typedef enum { DBL_MODE_PRE_VERIFY = 0, DBL_MODE_POST_VERIFY = 1, DBL_MODE_AR = 2, DBL_MODE_SERIAL = 3 } dbl_trace_mode;
+typedef enum {
+    DBL_KIND_PENDING_REJECT = 0, DBL_KIND_EXTEND_KEEP_DRAFT = 1, DBL_KIND_EXTEND_DRAFT_SUBSUMED = 2,
+    DBL_KIND_EXTEND_DROP_DRAFT = 3, DBL_KIND_AR_STEP = 4, DBL_KIND_REJECT = 5, DBL_KIND_ALL_ACCEPTED = 6
+} dbl_trace_kind;
+#define DBL_MAX_SEGS 64
+typedef struct { /* RoundTrace (pipeline.hpp:57-71); mode / kind / target_source as enums */
+    int64_t round;
+    int mode;                          /* dbl_trace_mode */
+    int pending, draft_len;
+    int n_draft_matched;
+    int32_t draft_matched[DBL_MAX_SEGS];
+    int target_matched;                /* -1 when target retrieval is off */
+    int target_source;                 /* dbl_source */
+    int accepted_pending;
+    int pending_reject, rejected;
+    int committed_count;
+    int kind;                          /* dbl_trace_kind */
+    double clock_delta;
+} dbl_round_trace;
+typedef struct { /* PipelineState (pipeline.hpp:46-55) over caller-owned host arrays */
+    int32_t* committed;    int64_t n_committed;   int64_t committed_cap;
+    int32_t* speculative;  int64_t n_speculative; int64_t speculative_cap;
+    int64_t n_spec_probs;  /* |spec_probs| (rows); check_state requires == n_speculative */
+    double* spec_probs;    /* T > 0: n_spec_probs x vocab rows, capacity spec_probs_cap rows.  NULL on input =
+                              the session's own device rows from its previous round (greedy never reads them) */
+    int64_t spec_probs_cap;
+    int mode;              /* Mode: 0 PreVerify, 1 PostVerify */
+    int prev_tokens;
+    int64_t round;
+    double clock;          /* SimClock::now */
+    int64_t last_committed_len;
+} dbl_pipeline_state;
+/* rollback (pipeline.cpp:15-30): InvalidArgument beyond the context, LogicError below the boundary */
+int dbl_rollback(dbl_pipeline_state* st, int64_t keep_len);
+/* run_round needs the draft/target lanes (token buffers + KV) to persist between rounds: a session
+ * holds them and re-synchronises them with the state it is given (longest common prefix), so a fresh,
+ * rolled-back or copied state runs exactly as the reference's and an unchanged one costs nothing. */
+typedef struct dbl_session_s* dbl_session_t;
+int dbl_session_create(dbl_model_t draft, dbl_model_t target, dbl_session_t* out);
+int dbl_session_destroy(dbl_session_t s);
+/* run_round (pipeline.cpp:223-262): one round; st advanced in place.  Capacities are checked before any
+ * work: committed_cap >= n_committed + n_speculative + depth + 1, speculative_cap >= gamma * (depth + 1)
+ * (and spec_probs_cap rows, when spec_probs is non-NULL at T > 0). */
+int dbl_run_round(dbl_session_t s, dbl_store_t store, const dbl_pipeline_options* opts, dbl_pipeline_state* st,
+                  dbl_round_trace* trace);
+int dbl_compute_metrics(const dbl_round_trace* traces, int n, double t_target, dbl_run_metrics* out); /* pipeline.cpp:325-371 */
+int dbl_traces_to_jsonl(const dbl_round_trace* traces, int n, char* buf, int64_t cap, int64_t* len);  /* pipeline.cpp:373-394 */
+int dbl_write_traces(const dbl_round_trace* traces, int n, const char* path);                        /* pipeline.cpp:396-400 */
+/* RunResult::traces of this thread's last dbl_run / dbl_run_ar(_sampled) / dbl_run_serial_sd */
+int dbl_last_run_traces(dbl_round_trace* out, int64_t cap, int64_t* n);
+/* HierarchicalDatastore copy (the reference's store is a value type: test_pipeline.cpp:170-187) */
+int dbl_store_clone(dbl_store_t src, dbl_store_t* out);
+/* build_prior (datastore.cpp:149-159): the store's prior layer := the first `rounds` of n_seqs sequences
+ * (seq_off[n_seqs + 1] into tokens), step = index, n-gram order max_order — one bulk upload */
+int dbl_build_prior(dbl_store_t s, const int64_t* seq_off, const int32_t* tokens, int n_seqs, int max_order, int rounds);
+
 /* ===================================================================== kernel-level checks
  * Debug entry points used by the parity tests to exercise one kernel against a host reference.
  * dbl_debug_gemm: W [n_out x K] bf16 bits, X [T x K] bf16 bits, padded to tp token columns.

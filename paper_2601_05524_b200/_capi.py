@@ -48,6 +48,28 @@ class RunMetrics(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class RetrievalResult(C.Structure):
+    _fields_ = [("matched_len", C.c_int), ("n_emitted", C.c_int), ("source", C.c_int), ("n_probs", C.c_int)]
+
+
+MAX_SEGS = 64
+
+
+class RoundTrace(C.Structure):
+    _fields_ = [("round", C.c_int64), ("mode", C.c_int), ("pending", C.c_int), ("draft_len", C.c_int),
+                ("n_draft_matched", C.c_int), ("draft_matched", C.c_int32 * MAX_SEGS), ("target_matched", C.c_int),
+                ("target_source", C.c_int), ("accepted_pending", C.c_int), ("pending_reject", C.c_int),
+                ("rejected", C.c_int), ("committed_count", C.c_int), ("kind", C.c_int), ("clock_delta", C.c_double)]
+
+
+class PipelineStateC(C.Structure):
+    _fields_ = [("committed", I32P), ("n_committed", C.c_int64), ("committed_cap", C.c_int64),
+                ("speculative", I32P), ("n_speculative", C.c_int64), ("speculative_cap", C.c_int64),
+                ("n_spec_probs", C.c_int64), ("spec_probs", F64P), ("spec_probs_cap", C.c_int64),
+                ("mode", C.c_int), ("prev_tokens", C.c_int), ("round", C.c_int64), ("clock", C.c_double),
+                ("last_committed_len", C.c_int64)]
+
+
 # name -> argtypes (all return int status unless listed in _RESTYPE)
 PROTOTYPES = {
     "dbl_last_error": [],
@@ -111,6 +133,27 @@ PROTOTYPES = {
     "dbl_guided_output": [I32P, C.c_int, F64P, I64P, C.c_int, I32P, C.c_int, F64P, I64P, C.c_int, C.c_int,
                           C.c_double, VP, I32P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                           C.POINTER(C.c_int)],
+    "dbl_tempered": [F64P, C.c_int, C.c_double, C.c_int, F64P],
+    "dbl_argmax_token": [F64P, C.c_int, C.c_int, I32P],
+    "dbl_argmax_rows": [F64P, I64P, C.c_int, C.c_int, I32P],
+    "dbl_sample": [F64P, C.c_int, C.c_double, VP, C.c_int, I32P],
+    "dbl_accept_with_model": [F64P, I64P, C.c_int, I32P, C.c_int, C.c_double, VP, C.c_int, I32P, C.c_int, F64P,
+                              C.c_int64, C.POINTER(RetrievalResult)],
+    "dbl_retrieval_forward": [VP, VP, I32P, C.c_int, C.c_int, C.c_double, VP, C.c_int, I32P, C.c_int, F64P,
+                              C.c_int64, C.POINTER(RetrievalResult)],
+    "dbl_iterative_draft": [VP, VP, I32P, C.c_int, C.c_int, C.c_int, C.c_double, VP, C.c_int,
+                            C.POINTER(RetrievalResult), I32P, C.c_int, C.POINTER(C.c_int), F64P, C.c_int64],
+    "dbl_measure_amt": [I32P, C.c_int, F64P],
+    "dbl_rollback": [C.POINTER(PipelineStateC), C.c_int64],
+    "dbl_session_create": [VP, VP, C.POINTER(VP)],
+    "dbl_session_destroy": [VP],
+    "dbl_run_round": [VP, VP, C.POINTER(PipelineOptions), C.POINTER(PipelineStateC), C.POINTER(RoundTrace)],
+    "dbl_compute_metrics": [C.POINTER(RoundTrace), C.c_int, C.c_double, C.POINTER(RunMetrics)],
+    "dbl_traces_to_jsonl": [C.POINTER(RoundTrace), C.c_int, C.c_char_p, C.c_int64, I64P],
+    "dbl_write_traces": [C.POINTER(RoundTrace), C.c_int, C.c_char_p],
+    "dbl_last_run_traces": [C.POINTER(RoundTrace), C.c_int64, I64P],
+    "dbl_store_clone": [VP, C.POINTER(VP)],
+    "dbl_build_prior": [VP, I64P, I32P, C.c_int, C.c_int, C.c_int],
     "dbl_debug_gemm": [C.c_int, U16P, C.c_int, C.c_int, U16P, C.c_int, C.c_int, C.c_int, F32P,
                        I32P],
 }

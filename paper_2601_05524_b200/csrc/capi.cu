@@ -24,11 +24,15 @@ struct dbl_store_s {
 struct dbl_model_s {
     std::unique_ptr<dbl::Model> impl;
 };
+struct dbl_rng_s {
+    std::unique_ptr<dbl::DeviceRng> impl;
+};
 
 namespace {
 thread_local std::string g_last_error;
 thread_local std::vector<int32_t> g_last_log;
 thread_local std::string g_last_jsonl;  // traces_to_jsonl of this thread's last single-sequence run
+thread_local std::vector<dbl::Trace> g_last_traces;  // RunResult::traces of that run
 
 template <class F>
 int guarded(F&& f) {
@@ -58,6 +62,7 @@ int copy_run(const dbl::RunOutput& r, int32_t* out, int cap, int* n_out, dbl_run
     if (out && !r.output.empty()) std::memcpy(out, r.output.data(), r.output.size() * 4);
     if (n_out) *n_out = static_cast<int>(r.output.size());
     if (metrics) *metrics = r.metrics;
+    g_last_traces = r.traces;
     if (jsonl || jsonl_len) {
         // tokens and metrics are already out; the text stays readable through dbl_last_run_jsonl, so a
         // short buffer costs a second copy, never the (already mutated-store) run
@@ -344,6 +349,321 @@ int dbl_transformer_get_weight(dbl_model_t m, const char* name, int layer, uint1
     });
 }
 
+// ------------------------------------------------------------------------ model-level helpers
+int dbl_tempered(const double* dist, int n, double temperature, int device, double* out) {
+    return guarded([&] { dbl::tempered(dist, n, temperature, out, device); });
+}
+int dbl_argmax_token(const double* dist, int n, int device, int32_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        if (n <= 0) dbl::throw_runtime("degenerate distribution");  // model.cpp:79 (empty row)
+        need(dist, "dist");
+        const int64_t off[2] = {0, n};
+        dbl::argmax_rows(dist, off, 1, out, device);
+    });
+}
+int dbl_argmax_rows(const double* probs, const int64_t* off, int n_rows, int device, int32_t* out) {
+    return guarded([&] {
+        if (n_rows < 0) dbl::throw_invalid("negative row count");
+        if (n_rows == 0) return;
+        need(off, "offsets");
+        need(out, "out");
+        for (int r = 0; r < n_rows; ++r)
+            if (off[r + 1] <= off[r]) dbl::throw_runtime("degenerate distribution");
+        dbl::argmax_rows(probs, off, n_rows, out, device);
+    });
+}
+int dbl_sample(const double* dist, int n, double temperature, dbl_rng_t r, int device, int32_t* out) {
+    return guarded([&] {
+        need(out, "out");
+        *out = dbl::sample(dist, n, temperature, r ? r->impl.get() : nullptr, r ? r->impl->device() : device);
+    });
+}
+
+// ------------------------------------------------------------------------------------ drafter
+namespace {
+void copy_retrieval(const std::vector<int32_t>& emitted, int matched, int source, int n_probs,
+                    const std::vector<double>& probs, int32_t* out, int cap, double* pout, int64_t pcap,
+                    dbl_retrieval_result* res) {
+    if (static_cast<int>(emitted.size()) > cap) dbl::throw_invalid("emitted buffer too small");
+    if (!emitted.empty()) std::memcpy(out, emitted.data(), emitted.size() * 4);
+    if (pout) {
+        if (static_cast<int64_t>(probs.size()) > pcap) dbl::throw_invalid("probs buffer too small");
+        if (!probs.empty()) std::memcpy(pout, probs.data(), probs.size() * sizeof(double));
+    }
+    if (res) *res = dbl_retrieval_result{matched, static_cast<int>(emitted.size()), source, n_probs};
+}
+}  // namespace
+
+int dbl_accept_with_model(const double* dists, const int64_t* dist_off, int n_dists, const int32_t* cands, int c,
+                          double temperature, dbl_rng_t r, int device, int32_t* emitted, int emitted_cap,
+                          double* probs, int64_t probs_cap, dbl_retrieval_result* res) {
+    return guarded([&] {
+        need(emitted, "emitted");
+        if (n_dists > 0) {
+            need(dists, "dists");
+            need(dist_off, "dist offsets");
+        }
+        const dbl::AcceptOut a = dbl::accept_with_model(dists, dist_off, n_dists, cands, c, temperature,
+                                                        r ? r->impl.get() : nullptr, device, probs != nullptr);
+        copy_retrieval(a.emitted, a.matched_len, DBL_SRC_MISS, a.n_probs, a.probs, emitted, emitted_cap, probs,
+                       probs_cap, res);
+    });
+}
+int dbl_retrieval_forward(dbl_model_t m, dbl_store_t st, const int32_t* ctx, int L, int depth, double temperature,
+                          dbl_rng_t r, int use_retrieval, int32_t* emitted, int emitted_cap, double* probs,
+                          int64_t probs_cap, dbl_retrieval_result* res) {
+    return guarded([&] {
+        need(m, "model");
+        need(emitted, "emitted");
+        if (L > 0) need(ctx, "ctx");
+        if (use_retrieval) need(st, "store");
+        const dbl::RetrievalOut o =
+            dbl::retrieval_forward(*m->impl, st ? st->impl.get() : nullptr, ctx, L, depth, temperature,
+                                   r ? r->impl.get() : nullptr, use_retrieval != 0, probs != nullptr);
+        copy_retrieval(o.emitted, o.matched_len, o.source, o.n_probs, o.probs, emitted, emitted_cap, probs, probs_cap,
+                       res);
+    });
+}
+int dbl_iterative_draft(dbl_model_t m, dbl_store_t st, const int32_t* ctx, int L, int gamma, int depth,
+                        double temperature, dbl_rng_t r, int use_retrieval, dbl_retrieval_result* segs,
+                        int32_t* tokens, int tokens_cap, int* n_tokens, double* probs, int64_t probs_cap) {
+    return guarded([&] {  // speculation.cpp:68-86
+        need(m, "model");
+        if (gamma < 1) dbl::throw_invalid("iterative_draft: gamma must be >= 1");
+        need(tokens, "tokens");
+        if (L > 0) need(ctx, "ctx");
+        if (use_retrieval) need(st, "store");
+        std::vector<int32_t> grown(ctx, ctx + std::max(L, 0)), flat;
+        std::vector<double> rows;
+        std::vector<dbl_retrieval_result> rs;
+        for (int j = 0; j < gamma; ++j) {
+            const dbl::RetrievalOut o = dbl::retrieval_forward(
+                *m->impl, st ? st->impl.get() : nullptr, grown.data(), static_cast<int>(grown.size()), depth,
+                temperature, r ? r->impl.get() : nullptr, use_retrieval != 0, probs != nullptr);
+            grown.insert(grown.end(), o.emitted.begin(), o.emitted.end());
+            flat.insert(flat.end(), o.emitted.begin(), o.emitted.end());
+            rows.insert(rows.end(), o.probs.begin(), o.probs.end());
+            rs.push_back(dbl_retrieval_result{o.matched_len, static_cast<int>(o.emitted.size()), o.source, o.n_probs});
+        }
+        if (static_cast<int>(flat.size()) > tokens_cap) dbl::throw_invalid("token buffer too small");
+        if (probs && static_cast<int64_t>(rows.size()) > probs_cap) dbl::throw_invalid("probs buffer too small");
+        std::memcpy(tokens, flat.data(), flat.size() * 4);
+        if (probs && !rows.empty()) std::memcpy(probs, rows.data(), rows.size() * sizeof(double));
+        if (segs) std::memcpy(segs, rs.data(), rs.size() * sizeof(dbl_retrieval_result));
+        if (n_tokens) *n_tokens = static_cast<int>(flat.size());
+    });
+}
+int dbl_measure_amt(const int32_t* matched_lens, int n, double* out) {
+    return guarded([&] {  // speculation.cpp:88-94
+        need(out, "out");
+        if (n <= 0) dbl::throw_invalid("measure_amt: empty trace");
+        need(matched_lens, "matched lengths");
+        double sum = 0.0;
+        for (int i = 0; i < n; ++i) sum += matched_lens[i];
+        *out = sum / static_cast<double>(n);
+    });
+}
+
+// --------------------------------------------------------------------- decoder state machine
+struct dbl_session_s {
+    std::unique_ptr<dbl::RoundSession> impl;
+    int device;
+};
+
+namespace {
+const char* const kModeNames[] = {"pre_verify", "post_verify", "ar", "serial"};
+const char* const kKindNames[] = {"pending_reject", "extend_keep_draft", "extend_draft_subsumed",
+                                  "extend_drop_draft", "ar_step", "reject", "all_accepted"};
+const char* const kSourceNames[] = {"prior", "dynamic", "rejected", "context", "miss"};
+int name_index(const char* const* names, int n, const std::string& s) {
+    for (int i = 0; i < n; ++i)
+        if (s == names[i]) return i;
+    dbl::throw_invalid("unknown trace label '" + s + "'");
+}
+dbl_round_trace to_c(const dbl::Trace& t) {
+    dbl_round_trace c{};
+    c.round = t.round;
+    c.mode = name_index(kModeNames, 4, t.mode);
+    c.pending = t.pending;
+    c.draft_len = t.draft_len;
+    if (t.draft_matched.size() > DBL_MAX_SEGS) dbl::throw_invalid("trace has more than DBL_MAX_SEGS segments");
+    c.n_draft_matched = static_cast<int>(t.draft_matched.size());
+    for (size_t k = 0; k < t.draft_matched.size(); ++k) c.draft_matched[k] = t.draft_matched[k];
+    c.target_matched = t.target_matched;
+    c.target_source = t.target_source.empty() ? DBL_SRC_MISS : name_index(kSourceNames, 5, t.target_source);
+    c.accepted_pending = t.accepted_pending;
+    c.pending_reject = t.pending_reject;
+    c.rejected = t.rejected;
+    c.committed_count = t.committed_count;
+    c.kind = name_index(kKindNames, 7, t.kind);
+    c.clock_delta = t.clock_delta;
+    return c;
+}
+std::vector<dbl::Trace> from_c(const dbl_round_trace* ts, int n) {
+    std::vector<dbl::Trace> out;
+    for (int i = 0; i < n; ++i) {
+        const dbl_round_trace& c = ts[i];
+        if (c.mode < 0 || c.mode > 3 || c.kind < 0 || c.kind > 6 || c.target_source < 0 || c.target_source > 4 ||
+            c.n_draft_matched < 0 || c.n_draft_matched > DBL_MAX_SEGS)
+            dbl::throw_invalid("trace field out of range");
+        dbl::Trace t;
+        t.round = c.round;
+        t.mode = kModeNames[c.mode];
+        t.pending = c.pending;
+        t.draft_len = c.draft_len;
+        t.draft_matched.assign(c.draft_matched, c.draft_matched + c.n_draft_matched);
+        t.target_matched = c.target_matched;
+        t.target_source = kSourceNames[c.target_source];
+        t.accepted_pending = c.accepted_pending;
+        t.pending_reject = c.pending_reject != 0;
+        t.rejected = c.rejected != 0;
+        t.committed_count = c.committed_count;
+        t.kind = kKindNames[c.kind];
+        t.clock_delta = c.clock_delta;
+        out.push_back(std::move(t));
+    }
+    return out;
+}
+}  // namespace
+
+int dbl_rollback(dbl_pipeline_state* st, int64_t keep_len) {
+    return guarded([&] {  // pipeline.cpp:15-30
+        need(st, "state");
+        const int64_t ctx_len = st->n_committed + st->n_speculative;
+        if (keep_len > ctx_len) dbl::throw_invalid("rollback: keep_len beyond context");
+        if (keep_len < st->last_committed_len) dbl::throw_logic("rollback: keep_len below committed boundary");
+        if (keep_len < st->n_committed) st->n_committed = keep_len;
+        st->n_speculative = 0;
+        st->n_spec_probs = 0;
+        st->mode = 0;
+    });
+}
+int dbl_session_create(dbl_model_t draft, dbl_model_t target, dbl_session_t* out) {
+    return guarded([&] {
+        need(draft, "draft");
+        need(target, "target");
+        need(out, "out");
+        *out = new dbl_session_s{std::make_unique<dbl::RoundSession>(*draft->impl, *target->impl),
+                                 target->impl->device()};
+    });
+}
+int dbl_session_destroy(dbl_session_t s) {
+    return guarded([&] { delete s; });
+}
+int dbl_run_round(dbl_session_t s, dbl_store_t store, const dbl_pipeline_options* opts, dbl_pipeline_state* st,
+                  dbl_round_trace* trace) {
+    return guarded([&] {
+        need(s, "session");
+        need(store, "store");
+        need(opts, "options");
+        need(st, "state");
+        if (st->n_committed < 0 || st->n_speculative < 0 || st->n_committed > st->committed_cap ||
+            st->n_speculative > st->speculative_cap)
+            dbl::throw_invalid("state lengths out of range");
+        if (st->n_committed > 0) need(st->committed, "committed");
+        if (st->n_speculative > 0) need(st->speculative, "speculative");
+        // capacities first: the round mutates the datastore, so it must never fail after it ran
+        const int64_t grow = st->n_speculative + opts->depth + 1;
+        if (st->committed_cap < st->n_committed + grow)
+            dbl::throw_invalid("committed buffer too small (need n_committed + n_speculative + depth + 1)");
+        if (st->speculative_cap < static_cast<int64_t>(opts->gamma) * (opts->depth + 1))
+            dbl::throw_invalid("speculative buffer too small (need gamma * (depth + 1))");
+        if (opts->temperature != 0.0 && st->spec_probs &&
+            st->spec_probs_cap < static_cast<int64_t>(opts->gamma) * (opts->depth + 1))
+            dbl::throw_invalid("spec_probs buffer too small (need gamma * (depth + 1) rows)");
+        dbl::HostPipelineState h;
+        h.committed.assign(st->committed, st->committed + st->n_committed);
+        h.speculative.assign(st->speculative, st->speculative + st->n_speculative);
+        h.n_spec_probs = static_cast<long>(st->n_spec_probs);
+        h.spec_probs_in = opts->temperature != 0.0 ? st->spec_probs : nullptr;
+        h.mode = st->mode;
+        h.prev_tokens = st->prev_tokens;
+        h.round = static_cast<long>(st->round);
+        h.clock = st->clock;
+        h.last_committed_len = static_cast<long>(st->last_committed_len);
+        std::vector<double> rows;
+        const dbl::Trace t = s->impl->run_round(h, *store->impl, *opts,
+                                                opts->temperature != 0.0 && st->spec_probs ? &rows : nullptr);
+        std::memcpy(st->committed, h.committed.data(), h.committed.size() * 4);
+        st->n_committed = static_cast<int64_t>(h.committed.size());
+        if (!h.speculative.empty()) std::memcpy(st->speculative, h.speculative.data(), h.speculative.size() * 4);
+        st->n_speculative = static_cast<int64_t>(h.speculative.size());
+        st->n_spec_probs = h.n_spec_probs;
+        if (!rows.empty()) std::memcpy(st->spec_probs, rows.data(), rows.size() * sizeof(double));
+        st->mode = h.mode;
+        st->prev_tokens = h.prev_tokens;
+        st->round = h.round;
+        st->clock = h.clock;
+        st->last_committed_len = h.last_committed_len;
+        if (trace) *trace = to_c(t);
+    });
+}
+int dbl_compute_metrics(const dbl_round_trace* traces, int n, double t_target, dbl_run_metrics* out) {
+    return guarded([&] {
+        need(out, "out");
+        if (n <= 0) dbl::throw_invalid("compute_metrics: no traces");  // pipeline.cpp:327
+        need(traces, "traces");
+        *out = dbl_run_metrics{};
+        dbl::compute_metrics(from_c(traces, n), t_target, out);
+    });
+}
+int dbl_traces_to_jsonl(const dbl_round_trace* traces, int n, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        if (n < 0) dbl::throw_invalid("negative trace count");
+        if (n > 0) need(traces, "traces");
+        const std::string js = dbl::traces_to_jsonl(from_c(traces, n));
+        if (len) *len = static_cast<int64_t>(js.size());
+        if (buf) {
+            if (cap < static_cast<int64_t>(js.size()) + 1) dbl::throw_invalid("jsonl buffer too small");
+            std::memcpy(buf, js.c_str(), js.size() + 1);
+        }
+    });
+}
+int dbl_write_traces(const dbl_round_trace* traces, int n, const char* path) {
+    return guarded([&] {
+        need(path, "path");
+        if (n < 0) dbl::throw_invalid("negative trace count");
+        if (n > 0) need(traces, "traces");
+        const std::string js = dbl::traces_to_jsonl(from_c(traces, n));
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) dbl::throw_runtime(std::string("cannot write ") + path);  // pipeline.cpp:398
+        const bool ok = std::fwrite(js.data(), 1, js.size(), f) == js.size();
+        std::fclose(f);
+        if (!ok) dbl::throw_runtime(std::string("cannot write ") + path);
+    });
+}
+int dbl_last_run_traces(dbl_round_trace* out, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        if (n) *n = static_cast<int64_t>(g_last_traces.size());
+        if (out) {
+            if (cap < static_cast<int64_t>(g_last_traces.size())) dbl::throw_invalid("trace buffer too small");
+            for (size_t i = 0; i < g_last_traces.size(); ++i) out[i] = to_c(g_last_traces[i]);
+        }
+    });
+}
+int dbl_store_clone(dbl_store_t src, dbl_store_t* out) {
+    return guarded([&] {
+        need(src, "store");
+        need(out, "out");
+        *out = new dbl_store_s{src->impl->clone()};
+    });
+}
+int dbl_build_prior(dbl_store_t s, const int64_t* seq_off, const int32_t* tokens, int n_seqs, int max_order,
+                    int rounds) {
+    return guarded([&] {  // datastore.cpp:149-159
+        need(s, "store");
+        if (rounds < 0) dbl::throw_invalid("build_prior: rounds must be >= 0");
+        if (n_seqs < 0) dbl::throw_invalid("negative sequence count");
+        const int take = std::min(n_seqs, rounds);
+        if (take > 0) {
+            need(seq_off, "sequence offsets");
+            need(tokens, "tokens");
+        }
+        s->impl->load_layer(DBL_LAYER_PRIOR, max_order, seq_off, tokens, take, 0);
+    });
+}
+
 // ------------------------------------------------------------------------------ decode loop
 int dbl_run(dbl_model_t draft, dbl_model_t target, dbl_store_t store, const int32_t* prompt, int n_prompt,
             int max_new, const dbl_pipeline_options* opts, int32_t* out, int cap, int* n_out,
@@ -556,9 +876,6 @@ int dbl_debug_gemm_trace(uint64_t* stamps, int64_t cap, int32_t* grids, int64_t*
 
 // --------------------------------------------------------------------------- kernel checks
 // ------------------------------------------------------------------------ verifier + RNG
-struct dbl_rng_s {
-    std::unique_ptr<dbl::DeviceRng> impl;
-};
 
 int dbl_rng_create(uint64_t seed, int device, dbl_rng_t* out) {
     return guarded([&] {

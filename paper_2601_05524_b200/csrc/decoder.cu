@@ -341,9 +341,9 @@ std::string traces_to_jsonl(const std::vector<Trace>& traces) {  // pipeline.cpp
 
 // ------------------------------------------------------------------------------- run (DOUBLE)
 namespace {
-// One sequence of a (possibly batched) DOUBLE run: PipelineState (pipeline.hpp:46-55), its lanes, its
-// datastore and its round record.
-struct Seq {
+// One sequence of a (possibly batched) DOUBLE decode: PipelineState (pipeline.hpp:46-55), its lanes,
+// its datastore and its round record.
+struct DoubleSeq {
     DeviceStore* st = nullptr;
     std::unique_ptr<Lane> dl, tl;
     std::unique_ptr<LaneIO> dio, tio;
@@ -360,6 +360,294 @@ struct Seq {
     int L = 0, nc = 0, ns = 0;  // this round
     int64_t trows = 0;
     RunOutput res;
+};
+
+// The round engine shared by run() (pipeline.cpp:264-323) and the run_round session (pipeline.cpp:
+// 223-262): the draft worker (iterative_draft) and the target worker (lookup + one verify forward)
+// on two streams over the frozen datastore snapshot, then finish_round (pipeline.cpp:91-206) on the
+// host with the datastore appends and the lanes' KV commit enqueued for the next round.
+struct DoubleEngine {
+    Model& dm;
+    Model& tm;
+    Streams S;
+    double tfwd_ms = 0.0;
+    int64_t tfwd_n = 0;
+
+    DoubleEngine(Model& d, Model& t) : dm(d), tm(t) {
+        // draft and target run concurrently unless that would put more than two persistent forwards on
+        // this GPU (tensor-parallel shards sharing it): then both workers share one stream — the round's
+        // results are identical either way (frozen snapshot, pipeline.cpp:239-261)
+        if (dm.persistent_grids() + tm.persistent_grids() > 2) S.target = S.draft;
+    }
+
+    // lanes (capacity `cap` tokens), round record and sampled-loop buffers of one sequence
+    void init_seq(DoubleSeq& q, DeviceStore* st, int cap, const dbl_pipeline_options& o) const {
+        q.st = st;
+        q.dl = std::make_unique<Lane>(dm, cap);
+        q.tl = std::make_unique<Lane>(tm, cap);
+        q.dio = std::make_unique<LaneIO>(q.dl.get());
+        q.tio = std::make_unique<LaneIO>(q.tl.get());
+        q.rr_buf.alloc(1);
+        q.rr = q.rr_buf.p;
+        q.rr_dev = q.rr_buf.dev();
+        q.smp.reset();
+        if (o.temperature != 0.0) {
+            if (dm.vocab() != tm.vocab()) throw_invalid("draft and target vocabularies differ");
+            const int d = o.depth, gamma = o.gamma;
+            q.smp = std::make_unique<Sampled>(o.temperature, o.rng_seed, tm.vocab(), d + 1, gamma * (d + 1),
+                                              gamma * (d + 1) + d + 2);
+        }
+    }
+
+    // one forward over the given lanes: the lane's own forward for a single lane, else batched when the
+    // rows fit one forward (<= 256), else one forward per lane
+    void forward_set(Model& m, std::vector<Lane*>& ls, const std::vector<int>& bounds, cudaStream_t s) {
+        if (ls.size() == 1) {
+            m.forward(*ls[0], bounds[0], s);
+            return;
+        }
+        int total = 0;
+        for (int v : bounds) total += v;
+        if (total <= m.max_forward_tokens() && total <= 256) {
+            m.forward_lanes(ls, total, s);
+        } else {
+            for (size_t i = 0; i < ls.size(); ++i) m.forward(*ls[i], bounds[i], s);
+        }
+    }
+    void dists_set(Model& m, std::vector<Lane*>& ls, const std::vector<int>& bounds, const std::vector<int>& rows,
+                   const std::vector<double*>& outs, cudaStream_t s) {
+        int total = 0;
+        for (int v : bounds) total += v;
+        if (ls.size() == 1 || (total <= m.max_forward_tokens() && total <= 256)) {
+            m.dists_lanes(ls, total, rows, outs, s);
+        } else {
+            for (size_t i = 0; i < ls.size(); ++i) m.dists(*ls[i], bounds[i], rows[i], outs[i], s);
+        }
+    }
+
+    // run_round (pipeline.cpp:223-262) for every sequence in `act`: each gets one Trace appended to
+    // q.res.traces and its PipelineState advanced; lanes are left holding committed ⊕ speculative.
+    void round(const std::vector<DoubleSeq*>& act, const dbl_pipeline_options& o) {
+        const int d = o.depth, gamma = o.gamma;
+        const int c_max = o.draft_retrieval ? d : 0, tc_max = o.target_retrieval ? d : 0;
+        for (DoubleSeq* qp : act) {
+            DoubleSeq& q = *qp;
+            // check_state, pipeline.cpp:208-219
+            if (q.mode == 0 && !q.spec.empty()) throw_logic("pre-verify mode with a speculative tail");
+            if (q.mode == 1 && q.prev_tokens != static_cast<int>(q.spec.size()))
+                throw_logic("prev_tokens out of sync with speculative tail");
+            q.nc = static_cast<int>(q.committed.size());
+            q.ns = static_cast<int>(q.spec.size());
+            q.L = q.nc + q.ns;
+            q.rr->draft_L0 = q.L;
+            q.rr->draft_L = q.L;
+            q.rr->n_segs = 0;
+            q.rr->draft_error = q.rr->target_error = 0;
+            if (q.smp) launch_derive_rngs(q.smp->rng.p, q.smp->seed, static_cast<uint64_t>(q.round), S.main);
+        }
+        S.fork();
+        // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
+        std::vector<Lane*> dls, tls;
+        std::vector<int> bounds;
+        for (int j = 0; j < gamma; ++j) {
+            dls.clear();
+            bounds.clear();
+            for (DoubleSeq* qp : act) {
+                DoubleSeq& q = *qp;
+                const int first = j == 0 ? split_long_forward(*q.dl, q.L, q.L - 1, c_max, q.smp != nullptr, S.draft) : 0;
+                if (o.draft_retrieval) q.st->lookup_lane(q.dl->buf.p, q.dl->state, d, S.draft);
+                dls.push_back(q.dl.get());
+                bounds.push_back(j == 0 ? q.L + c_max - first : 1 + c_max);
+            }
+            if (act[0]->smp) {
+                std::vector<int> rows;
+                std::vector<double*> outs;
+                for (DoubleSeq* qp : act) {
+                    rows.push_back(c_max + 1);
+                    outs.push_back(qp->smp->ddist.p);
+                }
+                dists_set(dm, dls, bounds, rows, outs, S.draft);
+                for (DoubleSeq* qp : act) {
+                    DoubleSeq& q = *qp;
+                    Sampled& sm = *q.smp;
+                    launch_draft_accept_sampled(*q.dl, q.rr_dev, j, q.L, sm.ddist.p, sm.chain[sm.cur].p, sm.chain_rows,
+                                                sm.rng.p, sm.T, sm.dscratch.p, S.draft);
+                }
+            } else {
+                forward_set(dm, dls, bounds, S.draft);
+                for (DoubleSeq* qp : act) launch_draft_accept(*qp->dl, qp->rr_dev, j, S.draft);
+            }
+        }
+        // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
+        bounds.clear();
+        for (DoubleSeq* qp : act) {
+            DoubleSeq& q = *qp;
+            const int first = split_long_forward(*q.tl, q.L, q.nc - 1, tc_max, q.smp != nullptr, S.target);
+            if (o.target_retrieval) q.st->lookup_lane(q.tl->buf.p, q.tl->state, d, S.target);
+            tls.push_back(q.tl.get());
+            bounds.push_back(q.L + tc_max - first);
+        }
+        CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
+        if (act[0]->smp) {
+            // verify forward + finish_round's verification (rng_v) + the target's own acceptance (rng_t)
+            std::vector<int> rows;
+            std::vector<double*> outs;
+            for (DoubleSeq* qp : act) {
+                rows.push_back(qp->ns + tc_max + 1);
+                outs.push_back(qp->smp->tdist.p);
+            }
+            dists_set(tm, tls, bounds, rows, outs, S.target);
+            CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
+            for (DoubleSeq* qp : act) {
+                DoubleSeq& q = *qp;
+                Sampled& sm = *q.smp;
+                launch_target_accept_sampled(*q.tl, q.nc, q.rr_dev, sm.tdist.p, sm.spec_probs, sm.rng.p + 1,
+                                             sm.rng.p + 2, sm.T, false, sm.tscratch.p, S.target);
+            }
+        } else {
+            forward_set(tm, tls, bounds, S.target);
+            CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
+            for (DoubleSeq* qp : act) launch_target_accept(*qp->tl, qp->nc, qp->rr_dev, S.target);
+        }
+        CUDA_CHECK(cudaStreamSynchronize(S.draft));
+        CUDA_CHECK(cudaStreamSynchronize(S.target));
+        {
+            float ms = 0.f;
+            CUDA_CHECK(cudaEventElapsedTime(&ms, S.tf0, S.tf1));
+            tfwd_ms += ms;
+            ++tfwd_n;
+        }
+        for (DoubleSeq* qp : act) finish(*qp, o);
+    }
+
+    // finish_round (pipeline.cpp:91-206) + rollback(state, |committed|) (pipeline.cpp:15-30) + the KV
+    // commit of both lanes (kv_len := LCP of what the device processed and committed' ⊕ spec')
+    void finish(DoubleSeq& q, const dbl_pipeline_options& o) {
+        const int gamma = o.gamma;
+        RoundResult* rr = q.rr;
+        DeviceStore& st = *q.st;
+        Lane& dl = *q.dl;
+        Lane& tl = *q.tl;
+        Sampled* smp = q.smp.get();
+        const int L = q.L, nc = q.nc, ns = q.ns;
+        if ((rr->draft_error || rr->target_error) && std::getenv("DBL_DEBUG_ROUND"))
+            std::fprintf(stderr, "dbl round %ld: draft_error %d target_error %d L %d nc %d ns %d n_segs %d draft_L %d ext_c %d\n",
+                         q.round, rr->draft_error, rr->target_error, L, nc, ns, rr->n_segs, rr->draft_L, rr->ext_c);
+        check_round_errors(rr);
+        const int c_t = rr->ext_c;
+        q.trows += L + c_t - (nc - 1);
+
+        const int n_chain = rr->draft_L - rr->draft_L0;
+        const int32_t* chain = rr->draft_tokens;
+        const int ne = rr->ext_matched + 1;
+        const int32_t* ext = rr->ext_emitted;
+        Trace tr;
+        tr.round = q.round;
+        tr.mode = q.mode ? "post_verify" : "pre_verify";
+        tr.pending = ns;
+        tr.draft_len = n_chain;
+        if (o.draft_retrieval)
+            for (int j = 0; j < rr->n_segs; ++j) tr.draft_matched.push_back(rr->segs[j].matched);
+        tr.target_matched = o.target_retrieval ? rr->ext_matched : -1;
+        tr.target_source = source_name(rr->ext_source);
+
+        const std::vector<int32_t> committed_before = q.committed;
+        std::vector<int32_t> add, new_spec;
+        const std::vector<int32_t>& spec = q.spec;
+        if (smp) smp->spec_probs = nullptr;
+        if (rr->tgt_rej >= 0) {
+            const int k = rr->tgt_rej;
+            tr.accepted_pending = k;
+            tr.pending_reject = tr.rejected = true;
+            tr.kind = "pending_reject";
+            add.assign(spec.begin(), spec.begin() + k);
+            add.push_back(rr->tgt_correction);
+            std::vector<int32_t> pre_k = committed_before;
+            pre_k.insert(pre_k.end(), spec.begin(), spec.begin() + k);
+            record_run(st, 2, pre_k, spec.data() + k, spec.size() - k, S.main);
+            std::vector<int32_t> pre_d = committed_before;
+            pre_d.insert(pre_d.end(), spec.begin(), spec.end());
+            record_run(st, 2, pre_d, chain, n_chain, S.main);
+        } else {
+            tr.accepted_pending = ns;
+            add = spec;
+            add.insert(add.end(), ext, ext + ne);
+            const int cmp = std::min(n_chain, ne);
+            int j = 0;
+            while (j < cmp && chain[j] == ext[j]) ++j;
+            if (j == ne && n_chain > ne) {
+                tr.kind = "extend_keep_draft";
+                new_spec.assign(chain + ne, chain + n_chain);
+                if (smp) {  // new_spec_probs = chain.probs[ne:] (pipeline.cpp:168-169)
+                    smp->spec_probs = smp->chain[smp->cur].p + static_cast<size_t>(ne) * smp->V;
+                    smp->cur ^= 1;
+                }
+            } else if (j == cmp) {
+                tr.kind = "extend_draft_subsumed";
+            } else {
+                tr.kind = "extend_drop_draft";
+                tr.rejected = true;
+                std::vector<int32_t> pre_j = committed_before;
+                pre_j.insert(pre_j.end(), spec.begin(), spec.end());
+                pre_j.insert(pre_j.end(), chain, chain + j);
+                record_run(st, 2, pre_j, chain + j, n_chain - j, S.main);
+            }
+        }
+        tr.committed_count = static_cast<int>(add.size());
+        record_run(st, 1, committed_before, add.data(), add.size(), S.main);
+        q.committed.insert(q.committed.end(), add.begin(), add.end());
+        // rollback(state, |committed|) (pipeline.cpp:15-30)
+        if (static_cast<long>(q.committed.size()) < q.last_committed_len)
+            throw_logic("rollback: keep_len below committed boundary");
+        q.spec = std::move(new_spec);
+        q.mode = q.spec.empty() ? 0 : 1;
+        q.prev_tokens = q.spec.empty() ? gamma : static_cast<int>(q.spec.size());
+        q.last_committed_len = static_cast<long>(q.committed.size());
+        ++q.round;
+        const double draft_time = gamma * (o.t_draft + (o.draft_retrieval ? o.t_lookup : 0.0));
+        const double target_time = o.t_target + (o.target_retrieval ? o.t_lookup : 0.0);
+        tr.clock_delta = std::max(draft_time, target_time) + o.t_sync;
+        q.res.traces.push_back(std::move(tr));
+        {  // decision log (see RunOutput::log)
+            auto& lg = q.res.log;
+            lg.push_back(rr->n_segs);
+            int at = 0;
+            for (int j = 0; j < rr->n_segs; ++j) {
+                lg.push_back(rr->segs[j].matched);
+                lg.insert(lg.end(), chain + at, chain + at + rr->segs[j].n_emit);
+                at += rr->segs[j].n_emit;
+            }
+            lg.push_back(ns);
+            lg.push_back(rr->tgt_rej);
+            lg.push_back(rr->tgt_correction);
+            lg.push_back(rr->ext_matched);
+            lg.insert(lg.end(), ext, ext + ne);
+        }
+
+        // ---- lane cursors for the next round (KV commit by length)
+        // the draft lane holds committed_before ⊕ spec ⊕ chain; KV valid below its last token
+        dl.mirror.resize(L);
+        dl.mirror.insert(dl.mirror.end(), chain, chain + n_chain);
+        dl.kv_len = L + n_chain - 1;  // sync() takes the LCP with committed' ⊕ spec'
+        tl.mirror.resize(L);
+        tl.mirror.insert(tl.mirror.end(), rr->ext_cands, rr->ext_cands + c_t);
+        tl.kv_len = L + c_t;
+        sync(q);
+    }
+
+    // make both lanes hold committed ⊕ speculative with KV valid for the longest common prefix of what
+    // they processed (the "rollback-free" commit: nothing moves, only kv_len)
+    void sync(DoubleSeq& q) {
+        std::vector<int32_t> X = q.committed;
+        X.insert(X.end(), q.spec.begin(), q.spec.end());
+        const int n = static_cast<int>(X.size()), nc = static_cast<int>(q.committed.size());
+        Lane& dl = *q.dl;
+        Lane& tl = *q.tl;
+        dl.kv_len = std::min(dl.kv_len, q.dio->sync_tokens(X, S.main));
+        dl.set_state(n, 0, dl.kv_len, n - 1, S.main);
+        tl.kv_len = std::min(tl.kv_len, q.tio->sync_tokens(X, S.main));
+        tl.set_state(n, 0, tl.kv_len, nc - 1, S.main);
+    }
 };
 }  // namespace
 
@@ -389,28 +677,13 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     size_t longest = 0;
     for (const auto& p : prompts) longest = std::max(longest, p.size());
     const int cap = static_cast<int>(longest) + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
-    Streams S;
-    // draft and target run concurrently unless that would put more than two persistent forwards on
-    // this GPU (tensor-parallel shards sharing it): then both workers share one stream — the round's
-    // results are identical either way (frozen snapshot, pipeline.cpp:239-261)
-    if (dm.persistent_grids() + tm.persistent_grids() > 2) S.target = S.draft;
+    DoubleEngine E(dm, tm);
+    Streams& S = E.S;
 
-    std::vector<Seq> seqs(B);
+    std::vector<DoubleSeq> seqs(B);
     for (int b = 0; b < B; ++b) {
-        Seq& q = seqs[b];
-        q.st = stores[b];
-        q.dl = std::make_unique<Lane>(dm, cap);
-        q.tl = std::make_unique<Lane>(tm, cap);
-        q.dio = std::make_unique<LaneIO>(q.dl.get());
-        q.tio = std::make_unique<LaneIO>(q.tl.get());
-        q.rr_buf.alloc(1);
-        q.rr = q.rr_buf.p;
-        q.rr_dev = q.rr_buf.dev();
-        if (o.temperature != 0.0) {
-            if (dm.vocab() != tm.vocab()) throw_invalid("draft and target vocabularies differ");
-            q.smp = std::make_unique<Sampled>(o.temperature, o.rng_seed, tm.vocab(), d + 1, gamma * (d + 1),
-                                              gamma * (d + 1) + d + 2);
-        }
+        DoubleSeq& q = seqs[b];
+        E.init_seq(q, stores[b], cap, o);
         device_counts(*q.st, S.main, &q.base_lookups, &q.base_hits);
         q.n_prompt = static_cast<int>(prompts[b].size());
         q.committed = prompts[b];
@@ -425,7 +698,7 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     Timer pre;
     CUDA_CHECK(cudaEventRecord(pre.a, S.main));
     S.fork();
-    for (Seq& q : seqs) {
+    for (DoubleSeq& q : seqs) {
         catch_up(*q.dl, q.n_prompt - 1, S.draft);
         catch_up(*q.tl, q.n_prompt - 1, S.target);
     }
@@ -434,7 +707,7 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     CUDA_CHECK(cudaEventRecord(S.ready, S.target));
     CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
     CUDA_CHECK(cudaEventRecord(pre.b, S.main));
-    for (Seq& q : seqs) {
+    for (DoubleSeq& q : seqs) {
         q.dl->set_state(q.n_prompt, 0, q.dl->kv_len, q.n_prompt - 1, S.main);
         q.tl->set_state(q.n_prompt, 0, q.tl->kv_len, q.n_prompt - 1, S.main);
     }
@@ -442,255 +715,16 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     Timer loop;
     CUDA_CHECK(cudaEventRecord(loop.a, S.main));
     const long long launches0 = launch_counter();
-    double tfwd_ms = 0.0;
-    int64_t tfwd_n = 0;
     const int32_t eos = tm.vocab() - 1;
-    const int c_max = o.draft_retrieval ? d : 0, tc_max = o.target_retrieval ? d : 0;
-    // one forward over the given lanes: the lane's own forward for a single lane, else batched when the
-    // rows fit one forward (<= 256), else one forward per lane
-    auto forward_set = [&](Model& m, std::vector<Lane*>& ls, const std::vector<int>& bounds, cudaStream_t s) {
-        if (ls.size() == 1) {
-            m.forward(*ls[0], bounds[0], s);
-            return;
-        }
-        int total = 0;
-        for (int v : bounds) total += v;
-        if (total <= m.max_forward_tokens() && total <= 256) {
-            m.forward_lanes(ls, total, s);
-        } else {
-            for (size_t i = 0; i < ls.size(); ++i) m.forward(*ls[i], bounds[i], s);
-        }
-    };
-    auto dists_set = [&](Model& m, std::vector<Lane*>& ls, const std::vector<int>& bounds, const std::vector<int>& rows,
-                         const std::vector<double*>& outs, cudaStream_t s) {
-        int total = 0;
-        for (int v : bounds) total += v;
-        if (ls.size() == 1 || (total <= m.max_forward_tokens() && total <= 256)) {
-            m.dists_lanes(ls, total, rows, outs, s);
-        } else {
-            for (size_t i = 0; i < ls.size(); ++i) m.dists(*ls[i], bounds[i], rows[i], outs[i], s);
-        }
-    };
-    std::vector<Seq*> act;
+    std::vector<DoubleSeq*> act;
     for (;;) {
         act.clear();
-        for (Seq& q : seqs)
+        for (DoubleSeq& q : seqs)
             if (!q.done) act.push_back(&q);
         if (act.empty()) break;
-        for (Seq* qp : act) {
-            Seq& q = *qp;
-            // check_state, pipeline.cpp:208-219
-            if (q.mode == 0 && !q.spec.empty()) throw_logic("pre-verify mode with a speculative tail");
-            if (q.mode == 1 && q.prev_tokens != static_cast<int>(q.spec.size()))
-                throw_logic("prev_tokens out of sync with speculative tail");
-            q.nc = static_cast<int>(q.committed.size());
-            q.ns = static_cast<int>(q.spec.size());
-            q.L = q.nc + q.ns;
-            q.rr->draft_L0 = q.L;
-            q.rr->draft_L = q.L;
-            q.rr->n_segs = 0;
-            q.rr->draft_error = q.rr->target_error = 0;
-            if (q.smp) launch_derive_rngs(q.smp->rng.p, q.smp->seed, static_cast<uint64_t>(q.round), S.main);
-        }
-        S.fork();
-        // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
-        std::vector<Lane*> dls, tls;
-        std::vector<int> bounds;
-        for (int j = 0; j < gamma; ++j) {
-            dls.clear();
-            bounds.clear();
-            for (Seq* qp : act) {
-                Seq& q = *qp;
-                const int first = j == 0 ? split_long_forward(*q.dl, q.L, q.L - 1, c_max, q.smp != nullptr, S.draft) : 0;
-                if (o.draft_retrieval) q.st->lookup_lane(q.dl->buf.p, q.dl->state, d, S.draft);
-                dls.push_back(q.dl.get());
-                bounds.push_back(j == 0 ? q.L + c_max - first : 1 + c_max);
-            }
-            if (act[0]->smp) {
-                std::vector<int> rows;
-                std::vector<double*> outs;
-                for (Seq* qp : act) {
-                    rows.push_back(c_max + 1);
-                    outs.push_back(qp->smp->ddist.p);
-                }
-                dists_set(dm, dls, bounds, rows, outs, S.draft);
-                for (Seq* qp : act) {
-                    Seq& q = *qp;
-                    Sampled& sm = *q.smp;
-                    launch_draft_accept_sampled(*q.dl, q.rr_dev, j, q.L, sm.ddist.p, sm.chain[sm.cur].p, sm.chain_rows,
-                                                sm.rng.p, sm.T, sm.dscratch.p, S.draft);
-                }
-            } else {
-                forward_set(dm, dls, bounds, S.draft);
-                for (Seq* qp : act) launch_draft_accept(*qp->dl, qp->rr_dev, j, S.draft);
-            }
-        }
-        // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
-        bounds.clear();
-        for (Seq* qp : act) {
-            Seq& q = *qp;
-            const int first = split_long_forward(*q.tl, q.L, q.nc - 1, tc_max, q.smp != nullptr, S.target);
-            if (o.target_retrieval) q.st->lookup_lane(q.tl->buf.p, q.tl->state, d, S.target);
-            tls.push_back(q.tl.get());
-            bounds.push_back(q.L + tc_max - first);
-        }
-        CUDA_CHECK(cudaEventRecord(S.tf0, S.target));
-        if (act[0]->smp) {
-            // verify forward + finish_round's verification (rng_v) + the target's own acceptance (rng_t)
-            std::vector<int> rows;
-            std::vector<double*> outs;
-            for (Seq* qp : act) {
-                rows.push_back(qp->ns + tc_max + 1);
-                outs.push_back(qp->smp->tdist.p);
-            }
-            dists_set(tm, tls, bounds, rows, outs, S.target);
-            CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
-            for (Seq* qp : act) {
-                Seq& q = *qp;
-                Sampled& sm = *q.smp;
-                launch_target_accept_sampled(*q.tl, q.nc, q.rr_dev, sm.tdist.p, sm.spec_probs, sm.rng.p + 1,
-                                             sm.rng.p + 2, sm.T, false, sm.tscratch.p, S.target);
-            }
-        } else {
-            forward_set(tm, tls, bounds, S.target);
-            CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
-            for (Seq* qp : act) launch_target_accept(*qp->tl, qp->nc, qp->rr_dev, S.target);
-        }
-        CUDA_CHECK(cudaStreamSynchronize(S.draft));
-        CUDA_CHECK(cudaStreamSynchronize(S.target));
-        {
-            float ms = 0.f;
-            CUDA_CHECK(cudaEventElapsedTime(&ms, S.tf0, S.tf1));
-            tfwd_ms += ms;
-            ++tfwd_n;
-        }
-
-        for (Seq* qp : act) {
-            Seq& q = *qp;
-            RoundResult* rr = q.rr;
-            DeviceStore& st = *q.st;
-            Lane& dl = *q.dl;
-            Lane& tl = *q.tl;
-            Sampled* smp = q.smp.get();
-            const int L = q.L, nc = q.nc, ns = q.ns;
-            if ((rr->draft_error || rr->target_error) && std::getenv("DBL_DEBUG_ROUND"))
-                std::fprintf(stderr, "dbl round %ld: draft_error %d target_error %d L %d nc %d ns %d n_segs %d draft_L %d ext_c %d\n",
-                             q.round, rr->draft_error, rr->target_error, L, nc, ns, rr->n_segs, rr->draft_L, rr->ext_c);
-            check_round_errors(rr);
-            const int c_t = rr->ext_c;
-            q.trows += L + c_t - (nc - 1);
-
-            // ---- finish_round (pipeline.cpp:91-206)
-            const int n_chain = rr->draft_L - rr->draft_L0;
-            const int32_t* chain = rr->draft_tokens;
-            const int ne = rr->ext_matched + 1;
-            const int32_t* ext = rr->ext_emitted;
-            Trace tr;
-            tr.round = q.round;
-            tr.mode = q.mode ? "post_verify" : "pre_verify";
-            tr.pending = ns;
-            tr.draft_len = n_chain;
-            if (o.draft_retrieval)
-                for (int j = 0; j < rr->n_segs; ++j) tr.draft_matched.push_back(rr->segs[j].matched);
-            tr.target_matched = o.target_retrieval ? rr->ext_matched : -1;
-            tr.target_source = source_name(rr->ext_source);
-
-            const std::vector<int32_t> committed_before = q.committed;
-            std::vector<int32_t> add, new_spec;
-            const std::vector<int32_t>& spec = q.spec;
-            if (smp) smp->spec_probs = nullptr;
-            if (rr->tgt_rej >= 0) {
-                const int k = rr->tgt_rej;
-                tr.accepted_pending = k;
-                tr.pending_reject = tr.rejected = true;
-                tr.kind = "pending_reject";
-                add.assign(spec.begin(), spec.begin() + k);
-                add.push_back(rr->tgt_correction);
-                std::vector<int32_t> pre_k = committed_before;
-                pre_k.insert(pre_k.end(), spec.begin(), spec.begin() + k);
-                record_run(st, 2, pre_k, spec.data() + k, spec.size() - k, S.main);
-                std::vector<int32_t> pre_d = committed_before;
-                pre_d.insert(pre_d.end(), spec.begin(), spec.end());
-                record_run(st, 2, pre_d, chain, n_chain, S.main);
-            } else {
-                tr.accepted_pending = ns;
-                add = spec;
-                add.insert(add.end(), ext, ext + ne);
-                const int cmp = std::min(n_chain, ne);
-                int j = 0;
-                while (j < cmp && chain[j] == ext[j]) ++j;
-                if (j == ne && n_chain > ne) {
-                    tr.kind = "extend_keep_draft";
-                    new_spec.assign(chain + ne, chain + n_chain);
-                    if (smp) {  // new_spec_probs = chain.probs[ne:] (pipeline.cpp:168-169)
-                        smp->spec_probs = smp->chain[smp->cur].p + static_cast<size_t>(ne) * smp->V;
-                        smp->cur ^= 1;
-                    }
-                } else if (j == cmp) {
-                    tr.kind = "extend_draft_subsumed";
-                } else {
-                    tr.kind = "extend_drop_draft";
-                    tr.rejected = true;
-                    std::vector<int32_t> pre_j = committed_before;
-                    pre_j.insert(pre_j.end(), spec.begin(), spec.end());
-                    pre_j.insert(pre_j.end(), chain, chain + j);
-                    record_run(st, 2, pre_j, chain + j, n_chain - j, S.main);
-                }
-            }
-            tr.committed_count = static_cast<int>(add.size());
-            record_run(st, 1, committed_before, add.data(), add.size(), S.main);
-            q.committed.insert(q.committed.end(), add.begin(), add.end());
-            // rollback(state, |committed|) (pipeline.cpp:15-30)
-            if (static_cast<long>(q.committed.size()) < q.last_committed_len)
-                throw_logic("rollback: keep_len below committed boundary");
-            q.spec = std::move(new_spec);
-            q.mode = q.spec.empty() ? 0 : 1;
-            q.prev_tokens = q.spec.empty() ? gamma : static_cast<int>(q.spec.size());
-            q.last_committed_len = static_cast<long>(q.committed.size());
-            ++q.round;
-            const double draft_time = gamma * (o.t_draft + (o.draft_retrieval ? o.t_lookup : 0.0));
-            const double target_time = o.t_target + (o.target_retrieval ? o.t_lookup : 0.0);
-            tr.clock_delta = std::max(draft_time, target_time) + o.t_sync;
-            q.res.traces.push_back(std::move(tr));
-            {  // decision log (see RunOutput::log)
-                auto& lg = q.res.log;
-                lg.push_back(rr->n_segs);
-                int at = 0;
-                for (int j = 0; j < rr->n_segs; ++j) {
-                    lg.push_back(rr->segs[j].matched);
-                    lg.insert(lg.end(), chain + at, chain + at + rr->segs[j].n_emit);
-                    at += rr->segs[j].n_emit;
-                }
-                lg.push_back(ns);
-                lg.push_back(rr->tgt_rej);
-                lg.push_back(rr->tgt_correction);
-                lg.push_back(rr->ext_matched);
-                lg.insert(lg.end(), ext, ext + ne);
-            }
-
-            // ---- lane cursors for the next round (KV commit by length)
-            std::vector<int32_t> X = q.committed;
-            X.insert(X.end(), q.spec.begin(), q.spec.end());
-            {
-                // the draft lane holds committed_before ⊕ spec ⊕ chain; KV valid below its last token
-                dl.mirror.resize(L);
-                dl.mirror.insert(dl.mirror.end(), chain, chain + n_chain);
-                const int dev_kv = L + n_chain - 1;
-                const int lcp = q.dio->sync_tokens(X, S.main);
-                dl.kv_len = std::min(dev_kv, lcp);
-                dl.set_state(static_cast<int>(X.size()), 0, dl.kv_len, static_cast<int>(X.size()) - 1, S.main);
-            }
-            {
-                tl.mirror.resize(L);
-                tl.mirror.insert(tl.mirror.end(), rr->ext_cands, rr->ext_cands + c_t);
-                const int dev_kv = L + c_t;
-                const int lcp = q.tio->sync_tokens(X, S.main);
-                tl.kv_len = std::min(dev_kv, lcp);
-                tl.set_state(static_cast<int>(X.size()), 0, tl.kv_len,
-                             static_cast<int>(q.committed.size()) - 1, S.main);
-            }
-
-            // ---- EOS / budget (pipeline.cpp:290-306)
+        E.round(act, o);
+        for (DoubleSeq* qp : act) {  // EOS / budget (pipeline.cpp:290-306)
+            DoubleSeq& q = *qp;
             for (; q.scanned < q.committed.size(); ++q.scanned) {
                 if (q.committed[q.scanned] == eos) {
                     q.committed.resize(q.scanned + 1);
@@ -706,7 +740,7 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     CUDA_CHECK(cudaStreamSynchronize(S.main));
 
     std::vector<RunOutput> out;
-    for (Seq& q : seqs) {
+    for (DoubleSeq& q : seqs) {
         RunOutput& res = q.res;
         finish_output(q.committed, q.n_prompt, max_new, res);
         compute_metrics(res.traces, o.t_target, &res.metrics);
@@ -719,8 +753,8 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
         res.metrics.device_ms = loop.ms();
         res.metrics.kernel_launches = launch_counter() - launches0;
         res.metrics.prefill_ms = pre.ms();
-        res.metrics.target_fwd_ms = tfwd_ms;
-        res.metrics.target_fwd_count = tfwd_n;
+        res.metrics.target_fwd_ms = E.tfwd_ms;
+        res.metrics.target_fwd_count = E.tfwd_n;
         res.metrics.target_rows = q.trows;
         q.st->flush_session(S.main);  // pipeline.cpp:321
         out.push_back(std::move(res));
@@ -736,6 +770,113 @@ RunOutput run_double(Model& dm, Model& tm, DeviceStore& st, const int32_t* promp
     std::vector<RunOutput> r = run_double_multi(dm, tm, {&st}, {std::vector<int32_t>(prompt, prompt + n_prompt)},
                                                 max_new, o);
     return std::move(r[0]);
+}
+
+// ------------------------------------------------------------------------ run_round session
+// A PipelineState driven one round at a time (run_round, pipeline.cpp:223-262).  The session keeps
+// the two lanes (token buffers + KV) between calls; each call re-synchronises them with the state it
+// is given by longest common prefix, so any state — a fresh one, a rolled-back one, a copy — runs
+// exactly as the reference would, and an unchanged state pays nothing.
+struct RoundSession::Impl {
+    DoubleEngine E;
+    std::unique_ptr<DoubleSeq> q;
+    int cap = 0, gamma = 0, depth = 0;
+    double temperature = 0.0;
+    uint64_t seed = 0;
+    bool dev_spec_valid = false;  // the sampled loop's spec_probs rows on the device belong to last_spec
+    std::vector<int32_t> last_spec;
+    const double* spec_dev = nullptr;
+    Impl(Model& d, Model& t) : E(d, t) {}
+};
+
+RoundSession::RoundSession(Model& dm, Model& tm) {
+    if (dm.device() != tm.device()) throw_invalid("draft and target must live on the same device");
+    DeviceGuard g(tm.device());
+    impl_ = std::make_unique<Impl>(dm, tm);
+}
+RoundSession::~RoundSession() = default;
+
+Trace RoundSession::run_round(HostPipelineState& st, DeviceStore& store, const dbl_pipeline_options& o,
+                              std::vector<double>* spec_probs_out) {
+    Impl& I = *impl_;
+    validate_opts(o);
+    // check_state (pipeline.cpp:208-219)
+    if (st.mode == 0 && !st.speculative.empty()) throw_logic("pre-verify mode with a speculative tail");
+    if (st.mode == 1 && st.prev_tokens != static_cast<int>(st.speculative.size()))
+        throw_logic("prev_tokens out of sync with speculative tail");
+    if (static_cast<long>(st.speculative.size()) != st.n_spec_probs)
+        throw_logic("speculative tokens and probs out of sync");
+    if (st.committed.empty()) throw_invalid("forward_batch: empty context");  // model.cpp:41
+    if (store.device() != I.E.tm.device()) throw_invalid("draft, target and datastore must live on the same device");
+    DeviceGuard g(store.device());
+    const int n = static_cast<int>(st.committed.size() + st.speculative.size());
+    const int need = n + 3 * o.gamma * (o.depth + 1) + 3 * o.depth + 64;
+    const bool sampled = o.temperature != 0.0;
+    if (!I.q || need > I.cap || o.gamma != I.gamma || o.depth != I.depth || o.temperature != I.temperature ||
+        o.rng_seed != I.seed) {
+        const int cap = std::max(need, I.cap) + 256;
+        I.q.reset();  // its lanes' caches go back to the models first
+        I.q = std::make_unique<DoubleSeq>();
+        I.E.init_seq(*I.q, &store, cap, o);
+        I.cap = cap;
+        I.gamma = o.gamma;
+        I.depth = o.depth;
+        I.temperature = o.temperature;
+        I.seed = o.rng_seed;
+        I.dev_spec_valid = false;
+    }
+    DoubleSeq& q = *I.q;
+    q.st = &store;
+    q.committed = st.committed;
+    q.spec = st.speculative;
+    q.mode = st.mode;
+    q.prev_tokens = st.prev_tokens;
+    q.round = st.round;
+    q.last_committed_len = st.last_committed_len;
+    q.res.traces.clear();
+    q.res.log.clear();
+    if (sampled) {
+        Sampled& sm = *q.smp;
+        sm.spec_probs = nullptr;
+        if (!q.spec.empty()) {
+            if (st.spec_probs_in) {  // the caller's rows -> the chain buffer the next draft does not write
+                const size_t rows = q.spec.size();
+                if (rows > static_cast<size_t>(sm.chain_rows)) throw_invalid("speculative tail longer than gamma * (depth + 1)");
+                double* dst = sm.chain[sm.cur ^ 1].p;
+                CUDA_CHECK(cudaMemcpyAsync(dst, st.spec_probs_in, rows * sm.V * sizeof(double), cudaMemcpyHostToDevice,
+                                           I.E.S.main));
+                sm.spec_probs = dst;
+            } else if (I.dev_spec_valid && I.last_spec == q.spec) {
+                sm.spec_probs = I.spec_dev;
+            } else {
+                throw_invalid("run_round: spec_probs rows are required at temperature > 0");
+            }
+        }
+    }
+    I.E.sync(q);
+    I.E.round({&q}, o);
+    Trace tr = q.res.traces.back();
+    st.committed = q.committed;
+    st.speculative = q.spec;
+    st.n_spec_probs = static_cast<long>(q.spec.size());
+    st.mode = q.mode;
+    st.prev_tokens = q.prev_tokens;
+    st.round = q.round;
+    st.last_committed_len = q.last_committed_len;
+    st.clock += tr.clock_delta;  // state.clock.charge (pipeline.cpp:203)
+    I.dev_spec_valid = sampled && !q.spec.empty();
+    I.last_spec = q.spec;
+    I.spec_dev = sampled ? q.smp->spec_probs : nullptr;
+    if (spec_probs_out) {
+        spec_probs_out->clear();
+        if (I.dev_spec_valid) {
+            spec_probs_out->resize(q.spec.size() * q.smp->V);
+            CUDA_CHECK(cudaMemcpyAsync(spec_probs_out->data(), I.spec_dev, spec_probs_out->size() * sizeof(double),
+                                       cudaMemcpyDeviceToHost, I.E.S.main));
+        }
+    }
+    CUDA_CHECK(cudaStreamSynchronize(I.E.S.main));
+    return tr;
 }
 
 // ----------------------------------------------------------------------------------- run (AR)
@@ -1092,7 +1233,7 @@ __global__ void gather_rows_kernel(const int32_t* argmax, int from, int n, int32
 }  // namespace
 
 void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,
-                       int32_t* out_argmax, float* out_logits, double* out_dists) {
+                       int32_t* out_argmax, float* out_logits, double* out_dists, DevBuf<double>* keep_dists) {
     if (L <= 0) throw_invalid("forward_batch: empty context");  // model.cpp:41
     if (c < 0) throw_invalid("negative candidate count");
     DeviceGuard g(m.device());
@@ -1105,7 +1246,9 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     catch_up(lane, L - 1, S.main);
     DevBuf<float> lg;
     DevBuf<double> dd;
-    if (out_dists) dd.alloc(static_cast<size_t>(c + 1) * m.vocab());
+    if (keep_dists) out_dists = nullptr;
+    const bool want_d = out_dists || keep_dists;
+    if (want_d) dd.alloc(static_cast<size_t>(c + 1) * m.vocab());
     else if (out_logits) lg.alloc(static_cast<size_t>(c + 1) * m.vocab());
     // rows [L-1, L+c): one forward, or (forward_batch has no row cap, model.cpp:37-53) consecutive
     // <= 256-row forwards — batch invariance makes each row bitwise the one-forward row
@@ -1116,7 +1259,7 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
         if (p1 == L + c) lane.set_state(L, c, lane.kv_len, p0, S.main);  // the last piece: L + c = p1
         else lane.set_state(p1, 0, lane.kv_len, p0, S.main);
         const size_t at = static_cast<size_t>(p0 - (L - 1)) * m.vocab();
-        if (out_dists) m.dists(lane, p1 - first, p1 - p0, dd.p + at, S.main);
+        if (want_d) m.dists(lane, p1 - first, p1 - p0, dd.p + at, S.main);
         else if (out_logits) m.logits(lane, p1 - first, lg.p + at, S.main);
         else m.forward(lane, p1 - first, S.main);
         lane.kv_len = std::max(lane.kv_len, p1);
@@ -1133,6 +1276,40 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     CUDA_CHECK(cudaStreamSynchronize(S.main));
     for (int i = 0; i <= c; ++i)
         if (out_argmax[i] < 0) throw_runtime("degenerate distribution");
+    if (keep_dists) *keep_dists = std::move(dd);
+}
+
+// retrieval_forward (speculation.cpp:54-66): lookup (if enabled) -> one forward_batch over ctx ⊕
+// candidates -> accept_with_model, all rows staying on the device
+RetrievalOut retrieval_forward(Model& m, DeviceStore* st, const int32_t* ctx, int L, int depth, double temperature,
+                               DeviceRng* rng, bool use_retrieval, bool want_probs) {
+    if (L <= 0) throw_invalid("lookup: empty context");
+    RetrievalOut r;
+    std::vector<int32_t> cands;
+    if (use_retrieval) {
+        if (!st) throw_invalid("retrieval_forward: a datastore is required with use_retrieval");
+        if (st->device() != m.device()) throw_invalid("model and datastore must live on the same device");
+        const int64_t off[2] = {0, L};
+        const int32_t dep = depth;
+        const int dc = std::max(depth, 1);
+        std::vector<int32_t> cbuf(dc);
+        int32_t n = 0, src = DBL_SRC_MISS, order = 0;
+        DeviceGuard g(st->device());
+        st->lookup_batch(1, off, ctx, &dep, dc, cbuf.data(), &n, &src, &order, 0);
+        cands.assign(cbuf.begin(), cbuf.begin() + n);
+        r.source = src;
+    }
+    const int c = static_cast<int>(cands.size());
+    DeviceGuard g(m.device());
+    std::vector<int32_t> am(c + 1);
+    DevBuf<double> dd;
+    forward_stateless(m, ctx, L, cands.data(), c, am.data(), nullptr, nullptr, &dd);
+    AcceptOut a = accept_with_model_dev(dd.p, m.vocab(), c + 1, cands.data(), c, temperature, rng, want_probs);
+    r.emitted = std::move(a.emitted);
+    r.matched_len = a.matched_len;
+    r.n_probs = a.n_probs;
+    r.probs = std::move(a.probs);
+    return r;
 }
 
 // ------------------------------------------------------------------------ forward profiling

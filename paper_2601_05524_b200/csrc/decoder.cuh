@@ -1,11 +1,13 @@
 // Host orchestrator of the device decode loop (replaces specpar::run / run_round / finish_round,
 // pipeline.cpp:15-323; run_vanilla_ar / run_serial_sd, harness.cpp:233-369).
 #pragma once
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "model.cuh"
 #include "store.cuh"
+#include "verify.cuh"
 
 namespace dbl {
 
@@ -53,11 +55,52 @@ std::vector<RunOutput> run_ar_batch(Model& target, const std::vector<std::vector
 RunOutput run_serial_sd(Model& draft, Model& target, DeviceStore& store, const int32_t* prompt,
                         int n_prompt, int max_new, const dbl_pipeline_options& o, bool use_retrieval);
 
+// PipelineState (pipeline.hpp:46-55) on the host side of the run_round boundary
+struct HostPipelineState {
+    std::vector<int32_t> committed, speculative;
+    long n_spec_probs = 0;                  // |spec_probs| (check_state compares it with |speculative|)
+    const double* spec_probs_in = nullptr;  // T > 0: |speculative| x vocab rows (host), or null = the
+                                            // session's own device rows from its previous round
+    int mode = 0;                           // Mode::PreVerify 0 / PostVerify 1
+    int prev_tokens = 0;
+    long round = 0;
+    double clock = 0.0;                     // SimClock::now
+    long last_committed_len = 0;
+};
+
+// run_round (pipeline.cpp:223-262) one call at a time: the draft/target lanes (KV) persist in the
+// session and are re-synchronised with whatever state is passed in (longest common prefix).
+class RoundSession {
+  public:
+    RoundSession(Model& draft, Model& target);
+    ~RoundSession();
+    // one round: st advanced in place (committed, speculative, mode, prev_tokens, round, clock,
+    // last_committed_len); spec_probs_out (T > 0) receives the new speculative tail's rows
+    Trace run_round(HostPipelineState& st, DeviceStore& store, const dbl_pipeline_options& o,
+                    std::vector<double>* spec_probs_out);
+
+  private:
+    struct Impl;
+    std::unique_ptr<Impl> impl_;
+};
+
 // forward of `rows` tokens after a ctx_len context, timed (out[8], see decoder.cu)
 void profile_forward(Model& m, int ctx_len, int rows, int iters, double* out);
 
 // forward_batch as a stateless call (fresh lane / KV): argmax rows (c+1) and optionally logits
 void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands, int c,
-                       int32_t* out_argmax, float* out_logits, double* out_dists = nullptr);
+                       int32_t* out_argmax, float* out_logits, double* out_dists = nullptr,
+                       DevBuf<double>* keep_dists = nullptr);
+
+struct RetrievalOut {  // RetrievalResult (speculation.hpp:12-17)
+    std::vector<int32_t> emitted;
+    int matched_len = 0;
+    int source = DBL_SRC_MISS;
+    int n_probs = 0;            // rows in probs (each vocab long)
+    std::vector<double> probs;  // filled when asked
+};
+// retrieval_forward (speculation.cpp:54-66); rng may be null when temperature == 0
+RetrievalOut retrieval_forward(Model& m, DeviceStore* st, const int32_t* ctx, int L, int depth, double temperature,
+                               DeviceRng* rng, bool use_retrieval, bool want_probs);
 
 }  // namespace dbl

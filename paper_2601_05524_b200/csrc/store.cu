@@ -237,6 +237,17 @@ __global__ void set_layer_kernel(StoreDesc* sd, int layer, LayerDesc v, int keep
     ly = v;
     if (keep_counts) { ly.n_tokens = nt; ly.n_seqs = ns; }
 }
+// bulk layer load (build_prior): sequence s owns tokens [start[s], start[s] + len[s])
+__global__ void fill_seq_of_kernel(int32_t* seq_of, const int32_t* __restrict__ start, const int32_t* __restrict__ len,
+                                   int n_seqs) {
+    for (int q = blockIdx.x; q < n_seqs; q += gridDim.x) {
+        const int a = start[q], n = len[q];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) seq_of[a + i] = q;
+    }
+}
+__global__ void set_stats_kernel(StoreDesc* sd, const StoreDesc* src) {
+    if (threadIdx.x < 6) sd->stats[threadIdx.x] = src->stats[threadIdx.x];
+}
 __global__ void set_store_kernel(StoreDesc* sd, int max_order, int rej) {
     sd->max_order = max_order;
     sd->rejected_enabled = rej;
@@ -387,6 +398,83 @@ void DeviceStore::clear_layer(int l, cudaStream_t s) {
     LayerDesc v{h.tokens.p, h.seq_of.p, h.seq_start.p, h.seq_len.p, h.seq_step.p, 0, 0, h.max_order, 0};
     set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 0);
     CUDA_LAUNCH_CHECK();
+}
+
+// a deep copy (the reference's HierarchicalDatastore is copied by value: test_pipeline.cpp:170-187)
+std::unique_ptr<DeviceStore> DeviceStore::clone() const {
+    auto c = std::make_unique<DeviceStore>(max_order_, depth_, device_);
+    DeviceGuard g(device_);
+    CUDA_CHECK(cudaDeviceSynchronize());  // every enqueued append of this store has landed
+    c->step_ = step_;
+    c->rejected_enabled_ = rejected_enabled_;
+    for (int l = 0; l < 3; ++l) {
+        const HostLayer& h = layers_[l];
+        HostLayer& d = c->layers_[l];
+        d.max_order = h.max_order;
+        c->grow(l, std::max(h.n_tokens, 1), std::max(h.n_seqs, 1), 0);
+        if (h.n_tokens) {
+            CUDA_CHECK(cudaMemcpy(d.tokens.p, h.tokens.p, h.n_tokens * 4, cudaMemcpyDeviceToDevice));
+            CUDA_CHECK(cudaMemcpy(d.seq_of.p, h.seq_of.p, h.n_tokens * 4, cudaMemcpyDeviceToDevice));
+        }
+        if (h.n_seqs) {
+            CUDA_CHECK(cudaMemcpy(d.seq_start.p, h.seq_start.p, h.n_seqs * 4, cudaMemcpyDeviceToDevice));
+            CUDA_CHECK(cudaMemcpy(d.seq_len.p, h.seq_len.p, h.n_seqs * 4, cudaMemcpyDeviceToDevice));
+            CUDA_CHECK(cudaMemcpy(d.seq_step.p, h.seq_step.p, h.n_seqs * 8, cudaMemcpyDeviceToDevice));
+        }
+        d.n_tokens = h.n_tokens;
+        d.n_seqs = h.n_seqs;
+        d.lens = h.lens;
+        LayerDesc v{d.tokens.p, d.seq_of.p, d.seq_start.p, d.seq_len.p, d.seq_step.p, d.n_tokens, d.n_seqs,
+                    d.max_order, 0};
+        set_layer_kernel<<<1, 1>>>(c->desc_dev_, l, v, 0);
+        CUDA_LAUNCH_CHECK();
+    }
+    set_store_kernel<<<1, 1>>>(c->desc_dev_, max_order_, rejected_enabled_ ? 1 : 0);
+    CUDA_LAUNCH_CHECK();
+    set_stats_kernel<<<1, 32>>>(c->desc_dev_, desc_dev_);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaDeviceSynchronize());
+    return c;
+}
+
+// layer l := n_seqs sequences (off[n_seqs + 1] into toks) with steps 0..n_seqs-1 and order max_order, in
+// one upload: tokens and the per-sequence records are copied once, seq_of is filled on the device
+void DeviceStore::load_layer(int l, int max_order, const int64_t* off, const int32_t* toks, int n_seqs, cudaStream_t s) {
+    if (l < 0 || l > 2) throw_invalid("bad datastore layer");
+    if (max_order < 1 || max_order > kMaxOrder) throw_invalid("layer max_order out of range");
+    if (n_seqs < 0) throw_invalid("negative sequence count");
+    const int64_t nt = n_seqs > 0 ? off[n_seqs] : 0;
+    if (n_seqs > 0 && off[0] != 0) throw_invalid("sequence offsets must start at 0");
+    for (int q = 0; q < n_seqs; ++q)
+        if (off[q + 1] <= off[q]) throw_invalid("insert: empty token sequence");  // datastore.cpp:10
+    if (nt >= (1L << 24) || n_seqs >= (1 << 24)) throw_runtime("datastore layer exceeds 2^24 tokens/sequences");
+    DeviceGuard g(device_);
+    clear_layer(l, s);
+    HostLayer& h = layers_[l];
+    h.max_order = max_order;
+    grow(l, static_cast<int>(std::max<int64_t>(nt, 1)), std::max(n_seqs, 1), s);
+    std::vector<int32_t> start(n_seqs), len(n_seqs);
+    std::vector<int64_t> step(n_seqs);
+    h.lens.resize(n_seqs);
+    for (int q = 0; q < n_seqs; ++q) {
+        start[q] = static_cast<int32_t>(off[q]);
+        len[q] = h.lens[q] = static_cast<int32_t>(off[q + 1] - off[q]);
+        step[q] = q;
+    }
+    if (n_seqs > 0) {
+        CUDA_CHECK(cudaMemcpyAsync(h.tokens.p, toks, nt * 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(h.seq_start.p, start.data(), n_seqs * 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(h.seq_len.p, len.data(), n_seqs * 4, cudaMemcpyHostToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(h.seq_step.p, step.data(), n_seqs * 8, cudaMemcpyHostToDevice, s));
+        fill_seq_of_kernel<<<std::min(n_seqs, 1184), 256, 0, s>>>(h.seq_of.p, h.seq_start.p, h.seq_len.p, n_seqs);
+        CUDA_LAUNCH_CHECK();
+    }
+    h.n_tokens = static_cast<int32_t>(nt);
+    h.n_seqs = n_seqs;
+    LayerDesc v{h.tokens.p, h.seq_of.p, h.seq_start.p, h.seq_len.p, h.seq_step.p, h.n_tokens, h.n_seqs, h.max_order, 0};
+    set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 0);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaStreamSynchronize(s));  // the host vectors above are pageable sources
 }
 
 void DeviceStore::lookup_lane(int32_t* buf, LaneState* lane, int d, cudaStream_t s) const {

@@ -13,6 +13,7 @@
 // over the context.  Inserts are O(len) appends — no index maintenance — which is what makes the
 // per-round datastore update (pipeline.cpp:146-184) a single tiny kernel.
 #pragma once
+#include <memory>
 #include <utility>
 #include <vector>
 
@@ -60,6 +61,9 @@ class DeviceStore {
         insert(layer, tokens, n, step_++, s);
     }
     void clear_layer(int layer, cudaStream_t s);
+    // layer := n_seqs sequences (offsets into toks) with steps 0..n-1 (build_prior, datastore.cpp:149-159)
+    void load_layer(int layer, int max_order, const int64_t* off, const int32_t* toks, int n_seqs, cudaStream_t s);
+    std::unique_ptr<DeviceStore> clone() const;
     void flush_session(cudaStream_t s) { clear_layer(1, s); clear_layer(2, s); }
 
     // one lookup for a lane: ctx = buf[0, lane.L); candidates -> buf[L, L+c), lane.c/src/order

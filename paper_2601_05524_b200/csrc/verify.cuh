@@ -48,4 +48,22 @@ VerifyOutcome guided_output(const int32_t* draft, int n_draft, const double* dpr
                             const int32_t* gtok, int n_gtok, const double* gprobs, const int64_t* goff, int n_gp,
                             int first_reject, double temperature, DeviceRng& rng);
 
+// the model-level helpers (model.hpp:40-48) over explicit fp64 rows
+void tempered(const double* p, int n, double temperature, double* out, int device);   // model.cpp:55-68
+void argmax_rows(const double* probs, const int64_t* off, int n_rows, int32_t* out, int device);  // model.cpp:70-81
+int sample(const double* p, int n, double temperature, DeviceRng* rng, int device);    // model.cpp:83-97
+
+struct AcceptOut {  // RetrievalResult (speculation.hpp:12-17) minus the source
+    std::vector<int32_t> emitted;
+    int matched_len = 0;
+    int n_probs = 0;             // rows of probs (ragged like the input rows 0..n_probs)
+    std::vector<double> probs;   // flattened; filled when asked
+};
+// accept_with_model (speculation.cpp:7-52) over ragged rows (|cands| + 1 of them)
+AcceptOut accept_with_model(const double* dists, const int64_t* off, int n_rows, const int32_t* cands, int c,
+                            double temperature, DeviceRng* rng, int device, bool want_probs);
+// the same over uniform rows already on the current device (n_rows x vocab fp64)
+AcceptOut accept_with_model_dev(const double* dists_dev, int vocab, int n_rows, const int32_t* cands, int c,
+                                double temperature, DeviceRng* rng, bool want_probs);
+
 }  // namespace dbl

@@ -31,7 +31,7 @@ from ._capi import (DoubleError, InvalidArgument, LogicError, PipelineOptions as
 SOURCES = ["prior", "dynamic", "rejected", "context", "miss"]
 PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
-__all__ = ["HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
+__all__ = ["NGramIndex", "HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
            "run_vanilla_ar", "run_vanilla_ar_batch", "run_batch", "link_tp_processes",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
@@ -131,7 +131,44 @@ class HierarchicalDatastore:
         self.max_order, self.depth, self.device = n, d, device
         self._orders = [n, n, n]
         self._rej = True
-        self.prior, self.dynamic, self.rejected = _Layer(self, 0), _Layer(self, 1), _Layer(self, 2)
+        self._layers = (_Layer(self, 0), _Layer(self, 1), _Layer(self, 2))
+
+    # the three NGramIndex layers; assigning a host NGramIndex (e.g. build_prior's) loads it in one upload
+    def _set_layer(self, layer: int, idx: "NGramIndex"):
+        if not isinstance(idx, NGramIndex):
+            raise InvalidArgument("a datastore layer can only be assigned an NGramIndex")
+        if layer == PRIOR and idx.steps == list(range(len(idx.sequences))):
+            flat, off = _flatten(idx.sequences)
+            check(lib().dbl_build_prior(self._h, _i64(off), _p32(flat), len(idx.sequences), int(idx.max_order),
+                                        len(idx.sequences)))
+            self._orders[layer] = int(idx.max_order)
+            return
+        L = self._layers[layer]
+        L.clear()
+        L.max_order = idx.max_order
+        for seq, step in zip(idx.sequences, idx.steps):
+            L.insert(seq, step)
+
+    prior = property(lambda self: self._layers[0], lambda self, v: self._set_layer(0, v))
+    dynamic = property(lambda self: self._layers[1], lambda self, v: self._set_layer(1, v))
+    rejected = property(lambda self: self._layers[2], lambda self, v: self._set_layer(2, v))
+
+    def copy(self) -> "HierarchicalDatastore":
+        """A deep copy on the device (the reference's store is a value type, test_pipeline.cpp:170-187)."""
+        h = C.c_void_p()
+        check(lib().dbl_store_clone(self._h, C.byref(h)))
+        c = HierarchicalDatastore.__new__(HierarchicalDatastore)
+        c._h = h
+        c.max_order, c.depth, c.device = self.max_order, self.depth, self.device
+        c._orders = list(self._orders)
+        c._rej = self._rej
+        c._layers = (_Layer(c, 0), _Layer(c, 1), _Layer(c, 2))
+        return c
+
+    __copy__ = copy
+
+    def __deepcopy__(self, memo):
+        return self.copy()
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -205,13 +242,59 @@ class HierarchicalDatastore:
         return LookupStats(*[int(x) for x in v])
 
 
-def build_prior(store: HierarchicalDatastore, corpora, rounds: int):
-    """build_prior (datastore.cpp:149-159): the first K sequences, step = index, into store.prior."""
+@dataclass
+class NGramIndex:
+    """A host-side NGramIndex value (datastore.hpp:19-27): the sequences and their steps.  Assign it to a
+    store layer (``store.prior = idx``) to load it into HBM; the device layers answer lookups."""
+    max_order: int = 3
+    sequences: list = field(default_factory=list)
+    steps: list = field(default_factory=list)
+
+    def insert(self, tokens, step: int):  # datastore.cpp:9-12
+        t = [int(x) for x in tokens]
+        if not t:
+            raise InvalidArgument("insert: empty token sequence")
+        self.sequences.append(t)
+        self.steps.append(int(step))
+
+    def occurrence_count(self) -> int:  # datastore.cpp:22-26
+        return sum(max(len(q) - k + 1, 0) for q in self.sequences for k in range(1, self.max_order + 1))
+
+    def clear(self):
+        self.sequences.clear()
+        self.steps.clear()
+
+
+def _flatten(seqs):
+    off = np.zeros(len(seqs) + 1, np.int64)
+    for i, q in enumerate(seqs):
+        off[i + 1] = off[i] + len(q)
+    flat = np.ascontiguousarray(np.concatenate([_i32(q) for q in seqs]) if seqs else np.zeros(1, np.int32))
+    return flat, off
+
+
+def build_prior(*args):
+    """build_prior (datastore.cpp:149-159): the first K corpus sequences with step = index.
+
+    ``build_prior(corpora, max_order, rounds) -> NGramIndex`` is the reference's signature (assign the
+    result to ``store.prior``); ``build_prior(store, corpora, rounds)`` loads straight into
+    ``store.prior`` (one bulk upload, dbl_build_prior) and returns the store."""
+    if len(args) == 3 and isinstance(args[0], HierarchicalDatastore):
+        store, corpora, rounds = args
+        if rounds < 0:
+            raise InvalidArgument("build_prior: rounds must be >= 0")
+        seqs = [list(q) for q in list(corpora)[:rounds]]
+        flat, off = _flatten(seqs)
+        check(lib().dbl_build_prior(store._h, _i64(off), _p32(flat), len(seqs), int(store._orders[PRIOR]),
+                                    len(seqs)))
+        return store
+    corpora, max_order, rounds = args
     if rounds < 0:
         raise InvalidArgument("build_prior: rounds must be >= 0")
-    for i, seq in enumerate(list(corpora)[:rounds]):
-        store.prior.insert(seq, i)
-    return store
+    idx = NGramIndex(int(max_order))
+    for i, q in enumerate(list(corpora)[:rounds]):
+        idx.insert(q, i)
+    return idx
 
 
 def save_model(model: "TableModel", path: str):
@@ -734,3 +817,296 @@ def guided_output(draft_tokens, draft_probs, guidance: GuidanceChain, first_reje
 
 __all__ += ["Rng", "derive_rng", "GuidanceChain", "VerifyOutcome", "accept_prob", "residual_sample",
             "residual_sample_point_mass", "verify_against_target", "guided_output", "VERIFY_KINDS"]
+
+
+# ------------------------------------------------------------------ model-level helpers (model.hpp:40-48)
+def tempered(dist, temperature: float, device: int = 0) -> np.ndarray:  # model.cpp:55-68
+    d = np.ascontiguousarray(dist, np.float64)
+    out = np.zeros(max(len(d), 1), np.float64)
+    check(lib().dbl_tempered(_f64(d), len(d), float(temperature), device, _f64(out)))
+    return out[:len(d)]
+
+
+def argmax_token(dist, device: int = 0) -> int:  # model.cpp:70-81
+    d = np.ascontiguousarray(dist, np.float64)
+    out = C.c_int32()
+    check(lib().dbl_argmax_token(_f64(d) if len(d) else None, len(d), device, C.byref(out)))
+    return out.value
+
+
+def argmax_rows(rows, device: int = 0) -> list:
+    """argmax_token of every row in one launch (one CTA per row, warp-shuffle reduction)."""
+    flat, off, n = _rows(rows)
+    out = np.zeros(max(n, 1), np.int32)
+    check(lib().dbl_argmax_rows(_f64(flat), _i64(off), n, device, _p32(out)))
+    return out[:n].tolist()
+
+
+def sample(dist, temperature: float, rng: "Rng | None", device: int = 0) -> int:  # model.cpp:83-97
+    d = np.ascontiguousarray(dist, np.float64)
+    out = C.c_int32()
+    check(lib().dbl_sample(_f64(d), len(d), float(temperature), rng._h if rng is not None else None, device,
+                           C.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------------ drafter (speculation.hpp:34-59)
+@dataclass
+class RetrievalResult:  # speculation.hpp:12-17
+    emitted: list
+    matched_len: int
+    probs: list
+    source: str = "miss"
+
+
+@dataclass
+class DraftChain:  # speculation.hpp:19-24
+    segments: list
+    tokens: list
+    probs: list
+    total_len: int
+
+
+def _split_rows(flat: np.ndarray, lengths) -> list:
+    out, at = [], 0
+    for n in lengths:
+        out.append(flat[at:at + n])
+        at += n
+    return out
+
+
+def accept_with_model(dists, cands, temperature: float = 0.0, rng: "Rng | None" = None,
+                      device: int = 0) -> RetrievalResult:  # speculation.cpp:7-52
+    flat, off, n = _rows(dists)
+    c = _i32(cands)
+    em = np.zeros(len(c) + 1, np.int32)
+    probs = np.zeros(max(int(off[-1]), 1), np.float64)
+    res = _RetrievalC()
+    check(lib().dbl_accept_with_model(_f64(flat), _i64(off), n, _p32(c), len(c), float(temperature),
+                                      rng._h if rng is not None else None, device, _p32(em), len(em),
+                                      _f64(probs), len(probs), C.byref(res)))
+    lens = [int(off[i + 1] - off[i]) for i in range(res.n_probs)]
+    return RetrievalResult(em[:res.n_emitted].tolist(), res.matched_len, _split_rows(probs, lens))
+
+
+def retrieval_forward(model: "_Model", store: "HierarchicalDatastore | None", context, depth: int,
+                      temperature: float = 0.0, rng: "Rng | None" = None, use_retrieval: bool = True,
+                      want_probs: bool = True) -> RetrievalResult:  # speculation.cpp:54-66
+    ctx = _i32(context)
+    V = model.vocab_size
+    em = np.zeros(max(int(depth), 0) + 1, np.int32)
+    probs = np.zeros((int(depth) + 1) * V if want_probs else 1, np.float64)
+    res = _RetrievalC()
+    check(lib().dbl_retrieval_forward(model._h, store._h if store is not None else None, _p32(ctx), len(ctx),
+                                      int(depth), float(temperature), rng._h if rng is not None else None,
+                                      int(bool(use_retrieval)), _p32(em), len(em),
+                                      _f64(probs) if want_probs else None, len(probs), C.byref(res)))
+    return RetrievalResult(em[:res.n_emitted].tolist(), res.matched_len,
+                           _split_rows(probs, [V] * res.n_probs) if want_probs else [], SOURCES[res.source])
+
+
+def iterative_draft(model: "_Model", store: "HierarchicalDatastore | None", context, gamma: int, depth: int,
+                    temperature: float = 0.0, rng: "Rng | None" = None, use_retrieval: bool = True,
+                    want_probs: bool = True) -> DraftChain:  # speculation.cpp:68-86
+    ctx = _i32(context)
+    V = model.vocab_size
+    cap = max(int(gamma), 1) * (max(int(depth), 0) + 1)
+    toks = np.zeros(cap, np.int32)
+    probs = np.zeros(cap * V if want_probs else 1, np.float64)
+    segs = (_RetrievalC * max(int(gamma), 1))()
+    n = C.c_int()
+    check(lib().dbl_iterative_draft(model._h, store._h if store is not None else None, _p32(ctx), len(ctx),
+                                    int(gamma), int(depth), float(temperature), rng._h if rng is not None else None,
+                                    int(bool(use_retrieval)), segs, _p32(toks), cap, C.byref(n),
+                                    _f64(probs) if want_probs else None, len(probs)))
+    tokens = toks[:n.value].tolist()
+    rows = _split_rows(probs, [V] * n.value) if want_probs else []
+    out, at = [], 0
+    for j in range(int(gamma)):
+        k = segs[j].n_emitted
+        out.append(RetrievalResult(tokens[at:at + k], segs[j].matched_len, rows[at:at + k], SOURCES[segs[j].source]))
+        at += k
+    return DraftChain(out, tokens, rows, n.value)
+
+
+def measure_amt(traces) -> float:  # speculation.cpp:88-94
+    m = _i32([t.matched_len if isinstance(t, RetrievalResult) else int(t) for t in traces])
+    out = C.c_double()
+    check(lib().dbl_measure_amt(_p32(m) if len(m) else None, len(m), C.byref(out)))
+    return out.value
+
+
+# ------------------------------------------------------------------ decoder state machine (pipeline.hpp)
+MODES = ["pre_verify", "post_verify", "ar", "serial"]
+KINDS = ["pending_reject", "extend_keep_draft", "extend_draft_subsumed", "extend_drop_draft", "ar_step", "reject",
+         "all_accepted"]
+
+
+@dataclass
+class PipelineState:  # pipeline.hpp:46-55
+    committed: list = field(default_factory=list)
+    speculative: list = field(default_factory=list)
+    spec_probs: list = field(default_factory=list)  # rows; greedy rows are not materialised (None entries)
+    mode: str = "pre_verify"
+    prev_tokens: int = 0
+    round: int = 0
+    clock: float = 0.0
+    last_committed_len: int = 0
+
+
+def _trace_dict(t) -> dict:  # RoundTrace (pipeline.hpp:57-71), keys in traces_to_jsonl order
+    return {"round": t.round, "mode": MODES[t.mode], "pending": t.pending, "draft_len": t.draft_len,
+            "draft_matched": list(t.draft_matched[:t.n_draft_matched]), "target_matched": t.target_matched,
+            "target_source": SOURCES[t.target_source], "accepted_pending": t.accepted_pending,
+            "pending_reject": bool(t.pending_reject), "rejected": bool(t.rejected), "committed": t.committed_count,
+            "kind": KINDS[t.kind], "clock_delta": t.clock_delta}
+
+
+def _trace_c(d: dict):
+    from ._capi import RoundTrace as _T
+    t = _T()
+    t.round = int(d.get("round", 0))
+    t.mode = MODES.index(d.get("mode", "pre_verify"))
+    t.pending = int(d.get("pending", 0))
+    t.draft_len = int(d.get("draft_len", 0))
+    dm = list(d.get("draft_matched", []))
+    t.n_draft_matched = len(dm)
+    for i, v in enumerate(dm):
+        t.draft_matched[i] = int(v)
+    t.target_matched = int(d.get("target_matched", -1))
+    t.target_source = SOURCES.index(d.get("target_source", "miss"))
+    t.accepted_pending = int(d.get("accepted_pending", 0))
+    t.pending_reject = int(bool(d.get("pending_reject", False)))
+    t.rejected = int(bool(d.get("rejected", False)))
+    t.committed_count = int(d.get("committed", d.get("committed_count", 0)))
+    t.kind = KINDS.index(d.get("kind", "extend_draft_subsumed"))
+    t.clock_delta = float(d.get("clock_delta", 0.0))
+    return t
+
+
+def _traces_c(traces):
+    from ._capi import RoundTrace as _T
+    arr = (_T * max(len(traces), 1))()
+    for i, d in enumerate(traces):
+        arr[i] = _trace_c(d)
+    return arr
+
+
+def rollback(state: PipelineState, keep_len: int):  # pipeline.cpp:15-30 (through the C-ABI)
+    st = _StateC()
+    com = _i32(state.committed)
+    st.committed, st.n_committed, st.committed_cap = _p32(com), len(com), len(com)
+    st.n_speculative = st.speculative_cap = len(state.speculative)
+    st.n_spec_probs = len(state.spec_probs)
+    st.mode = MODES.index(state.mode)
+    st.last_committed_len = int(state.last_committed_len)
+    check(lib().dbl_rollback(C.byref(st), int(keep_len)))
+    state.committed = com[:st.n_committed].tolist()
+    state.speculative, state.spec_probs, state.mode = [], [], "pre_verify"
+
+
+class Session:
+    """The device lanes (token buffers + KV) one PipelineState runs on between rounds."""
+
+    def __init__(self, draft: "_Model", target: "_Model"):
+        h = C.c_void_p()
+        check(lib().dbl_session_create(draft._h, target._h, C.byref(h)))
+        self._h, self._models = h, (draft, target)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().dbl_session_destroy(h)
+            except Exception:  # noqa: BLE001 (interpreter shutdown)
+                pass
+            self._h = None
+
+
+_SESSIONS: dict = {}
+
+
+def run_round(state: PipelineState, draft: "_Model", target: "_Model", store: "HierarchicalDatastore",
+              opts: "PipelineOptions | None" = None, session: Session | None = None) -> dict:
+    """run_round (pipeline.cpp:223-262): one DOUBLE round on the device; `state` advances in place and the
+    round's trace is returned.  Without an explicit session the (draft, target) pair's cached one is used."""
+    opts = opts or PipelineOptions()
+    if session is None:
+        key = (id(draft), id(target))
+        session = _SESSIONS.get(key)
+        if session is None or session._models != (draft, target):
+            session = _SESSIONS[key] = Session(draft, target)
+    V = target.vocab_size
+    gd = opts.gamma * (opts.depth + 1)
+    ncom = len(state.committed) + len(state.speculative) + opts.depth + 1
+    com = np.zeros(max(ncom, 1), np.int32)
+    com[:len(state.committed)] = state.committed
+    spec = np.zeros(max(gd, len(state.speculative), 1), np.int32)
+    spec[:len(state.speculative)] = state.speculative
+    st = _StateC()
+    st.committed, st.n_committed, st.committed_cap = _p32(com), len(state.committed), len(com)
+    st.speculative, st.n_speculative, st.speculative_cap = _p32(spec), len(state.speculative), len(spec)
+    st.n_spec_probs = len(state.spec_probs)
+    probs = None
+    if opts.temperature != 0.0:
+        rows = max(gd, len(state.speculative), 1)
+        probs = np.zeros(rows * V, np.float64)
+        have = [r for r in state.spec_probs if r is not None]
+        if len(have) == len(state.speculative):
+            if have:
+                probs[:len(have) * V] = np.concatenate([np.asarray(r, np.float64) for r in have])
+            st.spec_probs = _f64(probs)  # rows in, the new tail's rows out
+        else:
+            st.spec_probs = None  # the session's own device rows from its previous round
+        st.spec_probs_cap = rows
+    st.mode = MODES.index(state.mode)
+    st.prev_tokens = int(state.prev_tokens)
+    st.round = int(state.round)
+    st.clock = float(state.clock)
+    st.last_committed_len = int(state.last_committed_len)
+    o = opts._c()
+    tr = _TraceC()
+    check(lib().dbl_run_round(session._h, store._h, C.byref(o), C.byref(st), C.byref(tr)))
+    if not st.spec_probs:
+        probs = None
+    state.committed = com[:st.n_committed].tolist()
+    state.speculative = spec[:st.n_speculative].tolist()
+    if opts.temperature != 0.0 and probs is not None:
+        state.spec_probs = [probs[i * V:(i + 1) * V].copy() for i in range(st.n_speculative)]
+    else:
+        state.spec_probs = [None] * st.n_speculative
+    state.mode = MODES[st.mode]
+    state.prev_tokens = st.prev_tokens
+    state.round = st.round
+    state.clock = st.clock
+    state.last_committed_len = st.last_committed_len
+    return _trace_dict(tr)
+
+
+def compute_metrics(traces, t_target: float = 1.0) -> dict:  # pipeline.cpp:325-371
+    m = RunMetrics()
+    arr = _traces_c(traces)
+    check(lib().dbl_compute_metrics(arr, len(traces), float(t_target), C.byref(m)))
+    d = m.as_dict()
+    return {k: d[k] for k in ("tokens", "rounds", "clock", "m", "amt", "speedup")}
+
+
+def traces_to_jsonl(traces) -> str:  # pipeline.cpp:373-394
+    arr = _traces_c(traces)
+    n = C.c_int64()
+    check(lib().dbl_traces_to_jsonl(arr, len(traces), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().dbl_traces_to_jsonl(arr, len(traces), buf, len(buf), C.byref(n)))
+    return buf.value.decode()
+
+
+def write_traces(traces, path: str):  # pipeline.cpp:396-400
+    check(lib().dbl_write_traces(_traces_c(traces), len(traces), str(path).encode()))
+
+
+from ._capi import PipelineStateC as _StateC, RetrievalResult as _RetrievalC, RoundTrace as _TraceC  # noqa: E402
+
+__all__ += ["tempered", "argmax_token", "argmax_rows", "sample", "RetrievalResult", "DraftChain",
+            "accept_with_model", "retrieval_forward", "iterative_draft", "measure_amt", "PipelineState",
+            "rollback", "Session", "run_round", "compute_metrics", "traces_to_jsonl", "write_traces", "MODES",
+            "KINDS"]
