@@ -20,7 +20,6 @@ using namespace sm100;
 constexpr int kBM = 128, kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // one 128 x 64 bf16 weight tile
 constexpr unsigned long long kWatchdogNs = 4000000000ull;
-constexpr int kVRows = 8;              // attention: V rows loaded per round trip
 constexpr int kBatch = 2;               // split-K partials: 2 contributors x 16 columns of loads in flight
 
 // ------------------------------------------------------------------ small helpers
@@ -168,188 +167,185 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
     return v[0];
 }
 
-// One (q head, 64-key chunk) of split-KV causal attention for up to two consecutive tokens of one
-// sequence, one warp: the chunk's K and V rows are loaded once for both.  Scores: lane = key (the
-// whole key row's loads in flight at once); P*V: lane = HD/32 contiguous dims.  Each token keeps its
-// own causal limit, softmax and partial; chunks of a position combine in chunk order (the
-// last-arriving warp does it), so the result depends on the position only — never on how many
-// tokens the forward carries or how they are paired.
-template <int HD>
-__device__ __forceinline__ void attn_token_out(const FwdArgs& a, int t, int hq, int j, int nch, const float (&o)[HD / 32],
-                                               float mx, float l, int lane) {
-    constexpr int DPL = HD / 32;
-    const int nh = a.nh;
-    __nv_bfloat16* out = a.attn + static_cast<long long>(t) * a.q_dim + hq * HD + lane * DPL;
-    if (nch == 1) {
-        const float inv = 1.0f / l;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) out[e] = __float2bfloat16_rn(o[e] * inv);
-        return;
-    }
-    const long long slot = (static_cast<long long>(t) * nh + hq) * a.max_chunks + j;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) __stcg(a.part_o + slot * HD + lane * DPL + e, o[e]);
-    if (lane == 0) {
-        __stcg(a.part_ml + 2 * slot, mx);
-        __stcg(a.part_ml + 2 * slot + 1, l);
-    }
-    __syncwarp();
-    int last_in = 0;
-    if (lane == 0) {  // one acq_rel RMW (the warp's stores are ordered before it by __syncwarp)
-        int* cnt = a.attn_cnt + t * nh + hq;
-        last_in = atom_add_acq_rel_gpu(cnt, 1) == nch - 1;
-        if (last_in) *cnt = 0;
-    }
-    last_in = __shfl_sync(0xffffffffu, last_in, 0);
-    if (!last_in) return;
-    __syncwarp();  // lane 0's acquire orders the other lanes' reads of the partials
-    // combine this position's chunks in chunk order
-    const long long base = (static_cast<long long>(t) * nh + hq) * a.max_chunks;
-    // lane jj holds chunk jj's (max, sum) (32 chunks per pass); outputs 4 chunks per round trip, in
-    // chunk order
-    const float2* ml = reinterpret_cast<const float2*>(a.part_ml) + base;
-    float M = -INFINITY;
-    for (int jb = 0; jb < nch; jb += 32)
-        if (jb + lane < nch) M = fmaxf(M, __ldcg(ml + jb + lane).x);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    float den = 0.f, acc[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
-    for (int jb = 0; jb < nch; jb += 32) {
-        const bool mine = jb + lane < nch;
-        const float2 mv = mine ? __ldcg(ml + jb + lane) : make_float2(M, 0.f);
-        const float wl = mine ? __expf(mv.x - M) : 0.f;
-        const int n32 = min(32, nch - jb);
-        for (int i0 = 0; i0 < n32; i0 += 4) {
-            float v[4][DPL];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int e = 0; e < DPL; ++e)
-                    v[i][e] = i0 + i < n32 ? __ldcg(a.part_o + (base + jb + i0 + i) * HD + lane * DPL + e) : 0.f;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float wi = __shfl_sync(0xffffffffu, wl, (i0 + i) & 31);
-                const float li = __shfl_sync(0xffffffffu, mv.y, (i0 + i) & 31);
-                if (i0 + i < n32) {
-                    den = fmaf(li, wi, den);
-#pragma unroll
-                    for (int e = 0; e < DPL; ++e) acc[e] = fmaf(v[i][e], wi, acc[e]);
-                }
-            }
-        }
-    }
-    const float inv = 1.0f / den;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) out[e] = __float2bfloat16_rn(acc[e] * inv);
+// Split-KV causal attention, one (kv head, 64-key chunk, token block) item per CTA: the 4 aux warps
+// load the chunk's K and V rows and the block's q rows (all G q heads of the kv head x up to Tb
+// tokens: R = G * Tb <= 16 rows, one m16 tile) together — one round trip — then run scores and P*V
+// on the tensor cores (mma.sync m16n8k16 bf16 -> fp32: warp w takes keys [16w, 16w + 16) of the
+// scores and head dims [w HD/4, (w + 1) HD/4) of the output), the per-row softmax in fp32 (one warp
+// per row, fixed butterflies).  A position's chunk partials are combined by the next phase
+// (ATTN_COMBINE: one warp per (token, q head), chunks in order).  Every row's arithmetic is a
+// function of its position only — a tensor-core dot product never depends on the other rows — so
+// the result is the same however many tokens the forward carries (batch invariance).
+constexpr int kAttnRows = 16;
+constexpr int kQStride = 128 + 8;         // bf16 per q row (padded: conflict-free fragment loads)
+constexpr int kPStride = kAttnChunk + 4;  // fp32 per probability row (padded likewise)
+struct alignas(16) AttnSmem {
+    __nv_bfloat16 q[kAttnRows * kQStride];  // q rows of the item (row r = token tt * G + head hh)
+    float p[kAttnRows * kPStride];          // scores, then probabilities
+    float m[kAttnRows], l[kAttnRows];       // per-row max and sum of this chunk
+};
+
+// tokens per attention item: all G = nh / nkv q heads of a kv head x Tb tokens fill <= kAttnRows rows
+__device__ __forceinline__ int attn_block(const FwdArgs& a) { return max(1, kAttnRows / (a.nh / a.nkv)); }
+
+// opaque copy: values derived from it are not hoisted out of the forward's phase loop (attention-only
+// quantities would otherwise stay live through the GEMM epilogues and push them into local memory)
+__device__ __forceinline__ int opaque(int x) {
+    int y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
 }
 
-template <int HD, int NT>  // NT = 1: one token; NT = 2: up to two consecutive tokens
-__device__ __forceinline__ void attn_item(const FwdArgs& a, int t0, int nt, int hq, int j, int pos0,
+// D += A * B, m16n8k16, bf16 inputs, fp32 accumulate (fragment layouts: PTX ISA, mma.m16n8k16)
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int HD>
+__device__ __forceinline__ void attn_item(const FwdArgs& a, AttnSmem& S, int g, int j, int t0, int nt, int pos0,
                                           const int32_t* page_table, const __nv_bfloat16* kc,
-                                          const __nv_bfloat16* vc, float* q_s, float* p_s, int lane) {
-    constexpr int DPL = HD / 32;
-    const int nh = a.nh, kvh = hq / (nh / a.nkv);
+                                          const __nv_bfloat16* vc, int ph) {
+    constexpr int KS = HD / 16;  // k-steps of the scores
+    constexpr int NP = HD / 64;  // pairs of n8 output tiles per warp (HD / 4 dims per warp)
+    const int et = opaque(static_cast<int>(threadIdx.x)) - 64, ew = et >> 5, lane = et & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int nh = opaque(a.nh), nkv = opaque(a.nkv), Gq = nh / nkv;
     const int k0 = j * kAttnChunk;
-    // token tt sits at pos0 + tt and sees keys [k0, k0 + nk[tt]) of this chunk (nk <= 0: none)
-    const int nk0 = min(kAttnChunk, pos0 - k0 + 1);
-    const int nk1 = NT > 1 && nt > 1 ? min(kAttnChunk, pos0 + 1 - k0 + 1) : 0;
-    const int nk = max(nk0, nk1);
+    const int nk = min(kAttnChunk, pos0 + nt - k0);  // keys the block's last token sees
+    // tokens of the block that see this chunk: tt >= tt0 (earlier positions end before k0)
+    const int tt0 = max(0, k0 - pos0);
+    const int R = (nt - tt0) * Gq;
     const long long page = page_table[j];
-    const __nv_bfloat16* kp = kc + (page * a.nkv + kvh) * kPage * HD;
-    const __nv_bfloat16* vp = vc + (page * a.nkv + kvh) * kPage * HD;
+    const __nv_bfloat16* kp = kc + (page * nkv + g) * kPage * HD;
+    const __nv_bfloat16* vp = vc + (page * nkv + g) * kPage * HD;
+    // ---- loads, all in flight together: q rows -> shared (async); this warp's K fragments (keys
+    // 16 ew + [0, 16), every k-step) and V fragments (its head dims, every key; zero past the last key)
+    for (int i = et; i < R * (HD / 8); i += 128) {
+        const int r = i / (HD / 8), part = i % (HD / 8);
+        const int tt = tt0 + r / Gq, hq = g * Gq + r % Gq;
+        cp_async16(S.q + r * kQStride + part * 8, a.qbuf + (static_cast<long long>(t0 + tt) * nh + hq) * HD + part * 8);
+    }
+    uint32_t kb[2][KS][2];
 #pragma unroll
-    for (int tt = 0; tt < NT; ++tt) {
-        if (tt < nt) {
-            const __nv_bfloat16* qs = a.qbuf + (static_cast<long long>(t0 + tt) * nh + hq) * HD;
+    for (int n8 = 0; n8 < 2; ++n8) {
+        const uint32_t* kr = reinterpret_cast<const uint32_t*>(kp + static_cast<long long>(ew * 16 + n8 * 8 + gid) * HD);
 #pragma unroll
-            for (int e = 0; e < DPL; ++e) q_s[tt * HD + lane * DPL + e] = __bfloat162float(qs[lane * DPL + e]);
+        for (int ks = 0; ks < KS; ++ks) {
+            kb[n8][ks][0] = kr[ks * 8 + tig];
+            kb[n8][ks][1] = kr[ks * 8 + 4 + tig];
         }
     }
-    __syncwarp();
-    const float scale = rsqrtf(static_cast<float>(HD));
-    float sa[2], sb[2];  // scores of key lane / lane + 32 for tokens 0 and 1
-#pragma unroll 1
-    for (int h2 = 0; h2 < 2; ++h2) {
-        const int kk = lane + 32 * h2;
-        float acc0 = 0.f, acc1 = 0.f;
-        if (kk < nk) {
-            const uint4* kr = reinterpret_cast<const uint4*>(kp + static_cast<long long>(kk) * HD);
+    // V: column pair (base + 2 gid, + 1) of keys 16 ks + 2 tig + {0, 1, 8, 9}; n8 tile 2p holds the even
+    // dims of the pair block, tile 2p + 1 the odd ones
+    uint32_t vw[4][NP][4];
 #pragma unroll
-            for (int hh = 0; hh < HD / 64; ++hh) {  // 128-byte halves of the row: 8 loads in flight
-                uint4 w[8];
+    for (int ks = 0; ks < 4; ++ks)
 #pragma unroll
-                for (int d8 = 0; d8 < 8; ++d8) w[d8] = kr[hh * 8 + d8];
+        for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
-                for (int d8 = 0; d8 < 8; ++d8) {
-                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w[d8]);
+            for (int e = 0; e < 4; ++e) {
+                const int key = ks * 16 + 2 * tig + (e & 1) + (e >> 1) * 8;
+                vw[ks][pp][e] = key < nk ? *reinterpret_cast<const uint32_t*>(
+                                               vp + static_cast<long long>(key) * HD + ew * (HD / 4) + pp * 16 + 2 * gid)
+                                         : 0u;
+            }
+    cp_async_wait_all();
+    named_bar_sync(1, 128);
+    if (et == 0) stamp(a, ph, 12);
+    // ---- scores S = Q K^T for this warp's 16 keys, scaled and causally masked into shared memory
+    {
+        float sc[2][4] = {};
 #pragma unroll
-                    for (int e2 = 0; e2 < 4; ++e2) {
-                        const float2 kf = __bfloat1622float2(b2[e2]);
-                        const int d = (hh * 8 + d8) * 8 + 2 * e2;
-                        acc0 = fmaf(q_s[d], kf.x, acc0);
-                        acc0 = fmaf(q_s[d + 1], kf.y, acc0);
-                        if constexpr (NT > 1) {
-                            acc1 = fmaf(q_s[HD + d], kf.x, acc1);
-                            acc1 = fmaf(q_s[HD + d + 1], kf.y, acc1);
-                        }
-                    }
-                }
+        for (int ks = 0; ks < KS; ++ks) {
+            const __nv_bfloat16* qa = S.q + gid * kQStride + ks * 16 + tig * 2;
+            const uint32_t af[4] = {*reinterpret_cast<const uint32_t*>(qa),
+                                    *reinterpret_cast<const uint32_t*>(qa + 8 * kQStride),
+                                    *reinterpret_cast<const uint32_t*>(qa + 8),
+                                    *reinterpret_cast<const uint32_t*>(qa + 8 * kQStride + 8)};
+            mma16816(sc[0], af, kb[0][ks][0], kb[0][ks][1]);
+            mma16816(sc[1], af, kb[1][ks][0], kb[1][ks][1]);
+        }
+        const float scale = rsqrtf(static_cast<float>(HD));
+#pragma unroll
+        for (int n8 = 0; n8 < 2; ++n8)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = gid + 8 * (i >> 1), key = ew * 16 + n8 * 8 + tig * 2 + (i & 1);
+                const int tt = tt0 + row / Gq;
+                const bool ok = row < R && key < nk && k0 + key <= pos0 + tt;
+                S.p[row * kPStride + key] = ok ? sc[n8][i] * scale : -INFINITY;
+            }
+    }
+    named_bar_sync(1, 128);
+    if (et == 0) stamp(a, ph, 13);
+    // ---- softmax of each row over the chunk's keys (warp ew takes rows ew, ew + 4, ...)
+    for (int r = ew; r < R; r += 4) {
+        float* pr = S.p + r * kPStride;
+        const float s0 = pr[lane], s1 = pr[lane + 32];
+        float mx = fmaxf(s0, s1);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const float e0 = s0 == -INFINITY ? 0.f : __expf(s0 - mx), e1 = s1 == -INFINITY ? 0.f : __expf(s1 - mx);
+        float sum = e0 + e1;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        pr[lane] = e0;
+        pr[lane + 32] = e1;
+        if (lane == 0) {
+            S.m[r] = mx;
+            S.l[r] = sum;
+        }
+    }
+    named_bar_sync(1, 128);
+    if (et == 0) stamp(a, ph, 14);
+    // ---- O = P V for this warp's head dims (P rounded to bf16 for the tensor cores; keys past a
+    // row's limit carry p = 0 and zero V rows past the chunk's last key)
+    float oc[NP][2][4] = {};
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        const float* pa = S.p + gid * kPStride + ks * 16 + tig * 2;
+        const float2 x0 = *reinterpret_cast<const float2*>(pa), x1 = *reinterpret_cast<const float2*>(pa + 8 * kPStride);
+        const float2 x2 = *reinterpret_cast<const float2*>(pa + 8), x3 = *reinterpret_cast<const float2*>(pa + 8 * kPStride + 8);
+        const uint32_t af[4] = {pack_bf16(x0.x, x0.y), pack_bf16(x1.x, x1.y), pack_bf16(x2.x, x2.y),
+                                pack_bf16(x3.x, x3.y)};
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+            const uint32_t* w = vw[ks][pp];
+            mma16816(oc[pp][0], af, __byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410));
+            mma16816(oc[pp][1], af, __byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632));
+        }
+    }
+    // thread (gid, tig) holds dims base + 4 tig + [0, 4) of rows gid and gid + 8 for each pair block
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        const int row = gid + 8 * hr;
+        if (row >= R) continue;
+        const int tt = tt0 + row / Gq, hq = g * Gq + row % Gq, t = t0 + tt;
+        const int nch = (pos0 + tt) / kAttnChunk + 1;
+        const long long slot = (static_cast<long long>(t) * nh + hq) * a.max_chunks + j;
+        const float inv_l = 1.0f / S.l[row];
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) {
+            const int d = ew * (HD / 4) + pp * 16 + 4 * tig;
+            const float4 o = make_float4(oc[pp][0][2 * hr], oc[pp][1][2 * hr], oc[pp][0][2 * hr + 1], oc[pp][1][2 * hr + 1]);
+            if (nch == 1) {
+                __nv_bfloat16* out = a.attn + static_cast<long long>(t) * a.q_dim + hq * HD + d;
+                *reinterpret_cast<uint2*>(out) = make_uint2(pack_bf16(o.x * inv_l, o.y * inv_l), pack_bf16(o.z * inv_l, o.w * inv_l));
+            } else {
+                __stcg(reinterpret_cast<float4*>(a.part_o + slot * HD + d), o);
             }
         }
-        const float s0 = kk < nk0 ? acc0 * scale : -INFINITY, s1 = kk < nk1 ? acc1 * scale : -INFINITY;
-        if (h2 == 0) { sa[0] = s0; sa[1] = s1; } else { sb[0] = s0; sb[1] = s1; }
+        if (nch > 1 && ew == 0 && tig == 0)
+            __stcg(reinterpret_cast<float2*>(a.part_ml) + slot, make_float2(S.m[row], S.l[row]));
     }
-    float mx[2], l[2];
-#pragma unroll
-    for (int tt = 0; tt < NT; ++tt) {
-        const int ntk = tt == 0 ? nk0 : nk1;
-        float m = fmaxf(sa[tt], sb[tt]);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-        const float e0 = lane < ntk ? __expf(sa[tt] - m) : 0.f, e1 = lane + 32 < ntk ? __expf(sb[tt] - m) : 0.f;
-        p_s[tt * kAttnChunk + lane] = e0;
-        p_s[tt * kAttnChunk + lane + 32] = e1;
-        float s2 = e0 + e1;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, off);
-        mx[tt] = m;
-        l[tt] = s2;
-    }
-    __syncwarp();
-    float o0[DPL], o1[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) o0[e] = o1[e] = 0.f;
-    const __nv_bfloat16* vl = vp + lane * DPL;
-    using VT = typename std::conditional<DPL == 4, uint2, uint32_t>::type;  // this lane's DPL bf16 of a row
-#pragma unroll 1
-    for (int i0 = 0; i0 < nk; i0 += kVRows) {  // kVRows V rows in flight per round trip
-        VT raw[kVRows];
-#pragma unroll
-        for (int i = 0; i < kVRows; ++i)
-            if (i0 + i < nk) raw[i] = *reinterpret_cast<const VT*>(vl + static_cast<long long>(i0 + i) * HD);
-#pragma unroll
-        for (int i = 0; i < kVRows; ++i) {
-            if (i0 + i >= nk) break;
-            const float p0 = p_s[i0 + i];  // 0 beyond a token's limit
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw[i]);
-#pragma unroll
-            for (int e2 = 0; e2 < DPL / 2; ++e2) {
-                const float2 vf = __bfloat1622float2(b2[e2]);
-                o0[2 * e2] = fmaf(p0, vf.x, o0[2 * e2]);
-                o0[2 * e2 + 1] = fmaf(p0, vf.y, o0[2 * e2 + 1]);
-                if constexpr (NT > 1) {
-                    const float p1 = p_s[kAttnChunk + i0 + i];
-                    o1[2 * e2] = fmaf(p1, vf.x, o1[2 * e2]);
-                    o1[2 * e2 + 1] = fmaf(p1, vf.y, o1[2 * e2 + 1]);
-                }
-            }
-        }
-    }
-    if (nk0 > 0) attn_token_out<HD>(a, t0, hq, j, pos0 / kAttnChunk + 1, o0, mx[0], l[0], lane);
-    if constexpr (NT > 1)
-        if (nk1 > 0) attn_token_out<HD>(a, t0 + 1, hq, j, (pos0 + 1) / kAttnChunk + 1, o1, mx[1], l[1], lane);
 }
 
 struct BatchSmem {  // a batched forward's row -> lane map (the per-lane pointers stay in the
@@ -357,7 +353,7 @@ struct BatchSmem {  // a batched forward's row -> lane map (the per-lane pointer
     int n;
     int off[kMaxBatch + 1];
     int start[kMaxBatch], lc[kMaxBatch];
-    int poff[kMaxBatch + 1];  // attention token pairs before lane b
+    int poff[kMaxBatch + 1];  // attention token blocks before lane b
 };
 // forward row t -> its lane (return) and position (*pos)
 __device__ __forceinline__ int batch_row(const BatchSmem& B, int t, int* pos) {
@@ -378,61 +374,104 @@ struct FwdSmem {
     int sidx[128];
     TpPeers peers;  // copy of FwdArgs::peers (dynamic indexing of kernel parameters would use local memory)
     BatchSmem bt;   // batched forward only
-    union {
+    union alignas(16) {
         float pre[16 * 128];  // GEMM phases: a finisher's presummed split-K partials, parked across the accumulator wait
-        struct {
-            float q[4][2][128];  // ATTN phases: each aux warp's two query rows
-            float p[4][2][64];   //              and their probabilities over the chunk
-        } at;
+        AttnSmem at;          // ATTN phases
     };
 };
 static_assert(sizeof(FwdSmem) <= kFwdMiscBytes, "misc shared state exceeds its budget");
 
-// one attention phase of this warp.  Items = (token, q head, chunk), or — when there are more items
-// than warps — (token pair, q head, chunk): a pair shares the chunk's K/V loads (never spans
-// sequences).  Only the distribution of work changes; each token's arithmetic is the same either way.
+// ATTN_COMBINE: one warp per (forward row t, q head): the position's chunk partials in chunk order
+// (lane j holds chunk j's (max, sum); each lane HD/32 output dims; 8 chunks' loads per round trip).
 template <int HD, bool kB>
-__device__ __forceinline__ void attn_phase(const FwdArgs& a, const FwdPhase& P, int start, int T, int gw, int GW,
-                                        float* q_s, float* p_s, int lane, const BatchSmem& B) {
+__device__ __forceinline__ void attn_combine_phase(const FwdArgs& a, int start, int T, int gw, int GW, int lane,
+                                                   const BatchSmem& B) {
+    constexpr int DPL = HD / 32;
     const int nh = a.nh;
+    for (int item = gw; item < T * nh; item += GW) {
+        const int t = item / nh, hq = item % nh;
+        int pos = start + t;
+        if constexpr (kB) batch_row(B, t, &pos);
+        const int nch = pos / kAttnChunk + 1;
+        if (nch == 1) continue;  // written directly by the attention item
+        const long long base = (static_cast<long long>(t) * nh + hq) * a.max_chunks;
+        const float2* ml = reinterpret_cast<const float2*>(a.part_ml) + base;
+        float M = -INFINITY;
+        for (int jb = 0; jb < nch; jb += 32)
+            if (jb + lane < nch) M = fmaxf(M, __ldcg(ml + jb + lane).x);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        float den = 0.f, acc[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+        for (int jb = 0; jb < nch; jb += 32) {
+            const bool mine = jb + lane < nch;
+            const float2 mv = mine ? __ldcg(ml + jb + lane) : make_float2(M, 0.f);
+            const float wl = mine ? __expf(mv.x - M) : 0.f;
+            const int n32 = min(32, nch - jb);
+            for (int i0 = 0; i0 < n32; i0 += 8) {
+                float v[8][DPL];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e)
+                        v[i][e] = i0 + i < n32 ? __ldcg(a.part_o + (base + jb + i0 + i) * HD + lane * DPL + e) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float wi = __shfl_sync(0xffffffffu, wl, (i0 + i) & 31);
+                    const float li = __shfl_sync(0xffffffffu, mv.y, (i0 + i) & 31);
+                    if (i0 + i < n32) {
+                        den = fmaf(li, wi, den);
+#pragma unroll
+                        for (int e = 0; e < DPL; ++e) acc[e] = fmaf(v[i][e], wi, acc[e]);
+                    }
+                }
+            }
+        }
+        const float inv = 1.0f / den;
+        __nv_bfloat16* out = a.attn + static_cast<long long>(t) * a.q_dim + hq * HD + lane * DPL;
+#pragma unroll
+        for (int e = 0; e < DPL; e += 2)
+            *reinterpret_cast<__nv_bfloat162*>(out + e) = __floats2bfloat162_rn(acc[e] * inv, acc[e + 1] * inv);
+    }
+}
+
+// one attention phase of this CTA: items (token block, kv head, chunk) round-robin over the CTAs.  A
+// token block is up to Tb = kAttnRows / G consecutive tokens of one sequence.
+template <int HD, bool kB>
+__device__ __forceinline__ void attn_phase(const FwdArgs& a, const FwdPhase& P, int start, int T, int c, int G,
+                                           AttnSmem& S, const BatchSmem& B, int ph) {
+    const int nkv = opaque(a.nkv), Tb = opaque(attn_block(a));
     int max_pos = start + T - 1;
     if constexpr (kB) {
         max_pos = 0;
         for (int b = 0; b < B.n; ++b) max_pos = max(max_pos, B.lc[b] - 1);
     }
     const int nch_max = max_pos / kAttnChunk + 1;
-    const bool pairs = T * nh * nch_max > GW;
-    int units = T;
-    if (pairs) {
-        if constexpr (kB) units = B.poff[B.n];
-        else units = (T + 1) / 2;
-    }
-    const int items = units * nh * nch_max;
-    for (int item = gw; item < items; item += GW) {
+    int blocks = (T + Tb - 1) / Tb;
+    if constexpr (kB) blocks = B.poff[B.n];
+    const int items = blocks * nkv * nch_max;
+    for (int item = c; item < items; item += G) {
         const int j = item % nch_max, rest = item / nch_max;
-        const int hq = rest % nh, u = rest / nh;
-        int t0 = u, nt = 1, pos0, b = 0;
+        const int g = rest % nkv, blk = rest / nkv;
+        int t0, nt, pos0, b = 0;
         if constexpr (kB) {
-            if (pairs) {
-                while (b + 1 < B.n && u >= B.poff[b + 1]) ++b;
-                t0 = B.off[b] + 2 * (u - B.poff[b]);
-                nt = min(2, B.off[b + 1] - t0);
-                pos0 = B.start[b] + (t0 - B.off[b]);
-            } else {
-                b = batch_row(B, u, &pos0);
-            }
+            while (b + 1 < B.n && blk >= B.poff[b + 1]) ++b;
+            t0 = B.off[b] + (blk - B.poff[b]) * Tb;
+            nt = min(Tb, B.off[b + 1] - t0);
+            pos0 = B.start[b] + (t0 - B.off[b]);
         } else {
-            if (pairs) {
-                t0 = 2 * u;
-                nt = min(2, T - t0);
-            }
+            t0 = blk * Tb;
+            nt = min(Tb, T - t0);
             pos0 = start + t0;
         }
-        if (j * kAttnChunk > pos0 + nt - 1) continue;
+        if (j * kAttnChunk > pos0 + nt - 1) continue;  // the chunk is in every block token's future
         const int32_t* pt = kB ? a.batch.page_table[b] : a.page_table;
         const __nv_bfloat16* kc = kB ? P.kc + a.batch.koff[b] : P.kc;
         const __nv_bfloat16* vc = kB ? P.vc + a.batch.voff[b] : P.vc;
-        attn_item<HD, 2>(a, t0, nt, hq, j, pos0, pt, kc, vc, q_s, p_s, lane);  // one code path (registers)
+        attn_item<HD>(a, S, g, j, t0, nt, pos0, pt, kc, vc, ph);
+        named_bar_sync(1, 128);  // shared q / p are reused by the next item
+        if (threadIdx.x == 64) stamp(a, ph, 15);
     }
 }
 
@@ -529,10 +568,12 @@ __device__ __forceinline__ void wait_partials(const TileCtx& x) {
     }
     named_bar_sync(1, 128);
 }
-// pre[i] = p_1 + p_2 + ... + p_{n-1} for columns [ch, ch + 16) of this thread's row
-__device__ __forceinline__ void presum(const TileCtx& x, int ch, float (&pre)[16]) {
+// x.pre[i][r] = p_1 + p_2 + ... + p_{n-1} for columns [ch, ch + 16) of this thread's row, accumulated
+// in shared memory (the thread's own row: no barrier) so no register array lives across the tail
+__device__ __forceinline__ void presum(const TileCtx& x, int ch, const float* resid = nullptr) {
     const FwdArgs& a = *x.a;
     const int tp = x.tp, nc = min(16, tp - ch);
+    float* pre = x.pre + x.r;
     for (int jb = 1; jb < x.n_contrib; jb += kBatch) {
         float xs[kBatch][16];
 #pragma unroll
@@ -544,12 +585,16 @@ __device__ __forceinline__ void presum(const TileCtx& x, int ch, float (&pre)[16
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            float s2 = jb == 1 ? xs[0][i] : pre[i] + xs[0][i];
+            float s2 = jb == 1 ? xs[0][i] : pre[i * kBM] + xs[0][i];
 #pragma unroll
             for (int j = 1; j < kBatch; ++j)
                 if (jb + j < x.n_contrib) s2 += xs[j][i];
-            pre[i] = s2;
+            pre[i * kBM] = s2;
         }
+    }
+    if (resid) {  // a folded residual row: presum + resid, the one order on every path
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pre[i * kBM] += i < nc ? __ldcg(resid + static_cast<long long>(i) * a.h) : 0.f;
     }
 }
 
@@ -568,15 +613,9 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
             tmem_ld<CH>(x.taddr + ch, v);
             const int nc = min(CH, tp - ch);
             if (x.n_contrib > 1) {
-                float pre[16];
-                if (x.has_pre) {
+                if (!x.has_pre) presum(x, ch);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) pre[i] = x.pre[i * kBM + r];
-                } else {
-                    presum(x, ch, pre);
-                }
-#pragma unroll
-                for (int i = 0; i < CH; ++i) v[i] += pre[i];
+                for (int i = 0; i < CH; ++i) v[i] += x.pre[i * kBM + r];
             }
             for (int rr = 0; rr < a.tp_world; ++rr) {
                 float* dst = x.peers->xch[rr] + (static_cast<long long>(a.tp_rank * nth + m) * 256 + ch) * kBM + r;
@@ -617,20 +656,9 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         // accumulator is ready — every path (row count, early or not) uses this one order
         const bool fold = !kTP && P.epi == kFeResid && x.n_contrib > 1;
         if (x.n_contrib > 1 && !tp_resid) {
-            float pre[16];
-            if (x.has_pre) {
+            if (!x.has_pre) presum(x, ch, fold ? a.resid + static_cast<long long>(ch) * h + n : nullptr);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) pre[i] = x.pre[i * kBM + r];
-            } else {
-                presum(x, ch, pre);
-                if (fold) {
-                    const float* o = a.resid + static_cast<long long>(ch) * h + n;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) pre[i] += i < nc ? __ldcg(o + static_cast<long long>(i) * h) : 0.f;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < CH; ++i) v[i] += pre[i];
+            for (int i = 0; i < CH; ++i) v[i] += x.pre[i * kBM + r];
         }
         if (et == 0) stamp(a, x.p, 9);
         if (P.epi == kFeResid) {  // resid += acc; xb = bf16(resid); per-tile sum of squares
@@ -805,19 +833,20 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         if constexpr (kB) {
             BatchSmem& B = sm.bt;
             B.n = a.batch.n;
-            int off = 0, pairs = 0;
+            int off = 0, blocks = 0;
+            const int Tb = attn_block(a);
             for (int b = 0; b < B.n; ++b) {
                 const LaneState* Ls = a.batch.lane[b];
                 const int st = min(Ls->kv_len, Ls->row0), lc = Ls->L + Ls->c;
                 B.off[b] = off;
                 B.start[b] = st;
                 B.lc[b] = lc;
-                B.poff[b] = pairs;
+                B.poff[b] = blocks;
                 off += lc - st;
-                pairs += (lc - st + 1) / 2;
+                blocks += (lc - st + Tb - 1) / Tb;
             }
             B.off[B.n] = off;
-            B.poff[B.n] = pairs;
+            B.poff[B.n] = blocks;
             sint[0] = 0;
             sint[1] = off;
             sint[2] = 0;
@@ -1066,15 +1095,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     const bool early = finisher && n_contrib > 1 && tp == 16;
                     if (early) {  // the other contributors are (nearly always) done: sum them now
                         wait_partials(tc);
-                        float pre[16];
-                        presum(tc, 0, pre);
-                        if (!kTP && P.epi == kFeResid) {  // fold the residual in too (off the tail's chain)
-                            const float* o = a.resid + m * kBM + r;
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) pre[i] += __ldcg(o + static_cast<long long>(i) * a.h);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) sm.pre[i * kBM + r] = pre[i];  // own thread's row only
+                        // into sm.pre (own thread's row only), the residual folded in too (off the tail's chain)
+                        presum(tc, 0, !kTP && P.epi == kFeResid ? a.resid + m * kBM + r : nullptr);
                         tc.has_pre = true;
                     }
                     mbar_wait_wd(&tfull[buf], static_cast<uint32_t>((it / a.nacc) & 1), a.err, 6, p);
@@ -1108,9 +1130,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             } else if (P.kind == kPhAttn) {  // ------------------------- split-KV causal attention
                 acquire(P.dep);
                 stamp(a, p, 3);
-                if (a.hd == 128) attn_phase<128, kB>(a, P, start, T, gw, GW, &sm.at.q[ew][0][0], &sm.at.p[ew][0][0], lane, sm.bt);
-                else attn_phase<64, kB>(a, P, start, T, gw, GW, &sm.at.q[ew][0][0], &sm.at.p[ew][0][0], lane, sm.bt);
+                if (a.hd == 128) attn_phase<128, kB>(a, P, start, T, c, G, sm.at, sm.bt, p);
+                else attn_phase<64, kB>(a, P, start, T, c, G, sm.at, sm.bt, p);
                 if (lane == 0) stamp(a, p, 8 + ew);  // each aux warp's last item done
+                signal(p);
+            } else if (P.kind == kPhCombine) {  // --------------- split-KV partials -> attention output
+                acquire(P.dep);
+                if (a.hd == 128) attn_combine_phase<128, kB>(a, start, T, gw, GW, lane, sm.bt);
+                else attn_combine_phase<64, kB>(a, start, T, gw, GW, lane, sm.bt);
                 signal(p);
             } else {  // kPhArgmax ----------------------------------------- final argmax + cursor
                 acquire(P.dep);

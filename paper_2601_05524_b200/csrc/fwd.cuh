@@ -5,7 +5,7 @@
 // chain idles HBM for ~22 us per layer (profiles/r1_gemm_timeline.txt).  Here one CTA per SM runs
 // the whole forward as a fixed list of phases:
 //
-//   EMBED | per layer: QKV(gemm) ATTN O(gemm) GATE|UP(gemm) DOWN(gemm) | LM-HEAD(gemm) ARGMAX
+//   EMBED | per layer: QKV(gemm) ATTN COMBINE O(gemm) GATE|UP(gemm) DOWN(gemm) | LM-HEAD(gemm) ARGMAX
 //
 // and the only thing that waits on a data dependency is the consumer side of the tensor core: the
 // TMA producer streams every weight tile of the forward, phase after phase, into the shared-memory
@@ -37,7 +37,7 @@
 
 namespace dbl {
 
-enum FwdPhaseKind : int { kPhEmbed = 0, kPhGemm = 1, kPhAttn = 2, kPhArgmax = 3 };
+enum FwdPhaseKind : int { kPhEmbed = 0, kPhGemm = 1, kPhAttn = 2, kPhArgmax = 3, kPhCombine = 4 };
 enum FwdEpi : int { kFeQkv = 0, kFeResid = 1, kFeSilu = 2, kFeLogits = 3 };
 
 struct FwdPhase {
@@ -102,7 +102,6 @@ struct FwdArgs {
     float* ssq;          // [h/128][256] per-tile sums of squares of the residual
     float* part_o;       // attention split-KV partials [256][nh][max_chunks][hd]
     float* part_ml;      // [256][nh][max_chunks][2]
-    int* attn_cnt;       // [256][nh] chunk arrival counters (self-resetting)
     const float2* rope;  // [max_seq][hd/2] (cos, sin)
     int max_seq;
     const int32_t* page_table;
@@ -127,7 +126,8 @@ struct FwdArgs {
 static_assert(sizeof(FwdArgs) <= 4096, "FwdArgs must stay within 4 KiB of kernel parameters");
 
 constexpr int kFwdThreads = 192;  // warp 0 TMA producer, warp 1 MMA, warps 2..5 epilogue / aux work
-constexpr int kFwdMiscBytes = 16 * 1024;     // static shared state (barriers, reductions, attention)
+constexpr int kFwdMiscBytes = 16 * 1024;     // static shared state (barriers, reductions, attention);
+                                             // <= 16 KiB keeps 2 ring stages at 256 token columns
 constexpr int kFwdMaxStages = 24;
 constexpr int kFwdSmemBudget = 113 * 1024;  // two CTAs per SM: a draft and a target forward co-reside
 constexpr int kFwdMinUnits = 4;             // smallest stream-K range worth a CTA (4 x 16 KiB)

@@ -67,7 +67,7 @@ struct TfCache final : LaneCache {
     DevBuf<int32_t> page_table;
     DevBuf<float> resid, ssq, part_o, part_ml;
     DevBuf<__nv_bfloat16> xb, qbuf, attn, act;
-    DevBuf<int> attn_cnt, err;
+    DevBuf<int> err;
     DevBuf<float2> rope;                    // [capacity][hd/2] (cos, sin)
     DevBuf<FwdPhase> phases;
     CUtensorMap xmaps[3][5];  // xb, attn, act x boxes of 1, 2, 4, 8, 16 token rows
@@ -253,8 +253,6 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     c.act.zero();
     c.part_o.alloc(static_cast<size_t>(kMaxTp) * m.nh * c.max_chunks * m.hd);
     c.part_ml.alloc(static_cast<size_t>(kMaxTp) * m.nh * c.max_chunks * 2);
-    c.attn_cnt.alloc(static_cast<size_t>(kMaxTp) * m.nh);
-    c.attn_cnt.zero();
     c.err.alloc(1);
     c.err.zero();
     {  // RoPE table (rotate-half): angle(pos, i) = pos * theta^(-2i/hd)
@@ -337,6 +335,10 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
         at.kc = c.kbuf.p + c.layer_stride * l;
         at.vc = c.vbuf.p + c.layer_stride * l;
         add(at);
+        FwdPhase cb{};
+        cb.kind = kPhCombine;
+        cb.layer = l;
+        add(cb);
         gemm(kFeResid, 1, x_attn, m.h, m.q_dim, l);
         gemm(kFeSilu, 2, x_xb, 2 * m.ffn_l, m.h, l);
         gemm(kFeResid, 3, x_act, m.h, m.ffn_l, l);
@@ -423,7 +425,6 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
     a.ssq = c.ssq.p;
     a.part_o = c.part_o.p;
     a.part_ml = c.part_ml.p;
-    a.attn_cnt = c.attn_cnt.p;
     a.rope = c.rope.p;
     a.max_seq = c.capacity;
     a.page_table = c.page_table.p;

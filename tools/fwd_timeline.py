@@ -36,8 +36,8 @@ P, G = n_ph.value, grid.value
 st = st[:P * G * 16].reshape(P, G, 16).astype(np.int64)
 kinds, mb = ["embed"], [0.0]
 for _ in range(nl):
-    kinds += ["qkv", "attn", "o", "gate|up", "down"]
-    mb += [(nh + 2 * nkv) * hd * h * 2 / 1e6, 0.0, h * nh * hd * 2 / 1e6, 2 * f * h * 2 / 1e6, h * f * 2 / 1e6]
+    kinds += ["qkv", "attn", "combine", "o", "gate|up", "down"]
+    mb += [(nh + 2 * nkv) * hd * h * 2 / 1e6, 0.0, 0.0, h * nh * hd * 2 / 1e6, 2 * f * h * 2 / 1e6, h * f * 2 / 1e6]
 kinds += ["lm_head", "argmax"]
 mb += [V * h * 2 / 1e6, 0.0]
 assert len(kinds) == P, (len(kinds), P)
@@ -73,11 +73,11 @@ for k, (us, b) in tot.items():
 print(f"span {prev_done:.1f} us; weights {sum(mb):.0f} MB -> {sum(mb) * 1e6 / (prev_done * 1e3):.0f} GB/s")
 
 # ---- detail of one middle layer: per phase, percentiles over CTAs relative to the previous phase's end
-L0 = 1 + 5 * (nl // 2)
+L0 = 1 + 6 * (nl // 2)
 print(f"\nlayer {nl // 2} detail (us after the previous phase's last signal; min/median/max over CTAs)")
 names = {1: "dep", 4: "mma0", 5: "mma1", 6: "epi1", 2: "sig"}
 prev = col(L0 - 1, 2, np.max)
-for p in range(L0, L0 + 5):
+for p in range(L0, L0 + 6):
     parts = []
     for k in (1, 4, 5, 6, 2):
         v = st[p, :, k][st[p, :, k] > 0]
@@ -100,7 +100,7 @@ for p in range(P):
         units[p], active[p], offset[p], kbs[p] = U, A, off, K // 64
         off = (off + A) % sms
 print("\nstragglers (epilogue end - last MMA, us): top CTAs per phase")
-for p in range(L0, L0 + 5):
+for p in range(L0, L0 + 6):
     if p not in units:
         continue
     U, A, o, KB = units[p], active[p], offset[p], kbs[p]
@@ -116,10 +116,23 @@ for p in range(L0, L0 + 5):
                     "/".join(f"{x:.1f}" for x in sub) + "]")
     print(f"  {kinds[p]:>8} median {np.median(lag):.1f}:\n      " + "\n      ".join(desc))
 
-ap = L0 + 1  # the middle layer's attention phase
+ap = L0 + 1  # the middle layer's attention phase (its combine follows)
 w_end = st[ap, :, 8:12].max(axis=1)
 prev_done = col(L0, 2, np.max)
 print(f"\nattention (layer {nl // 2}): per-CTA last item done after QKV end: median "
       f"{(np.median(w_end) - prev_done) / 1e3:.1f} max {(w_end.max() - prev_done) / 1e3:.1f} us; "
       f"CTA signal max {(col(ap, 2, np.max) - prev_done) / 1e3:.1f} us; epilogue start median "
       f"{(np.median(st[ap, :, 3]) - prev_done) / 1e3:.1f}")
+
+# attention item internals (middle layer): per CTA with an item, us after the CTA's phase start (stamp 3)
+rows = []
+for c in range(G):
+    if st[ap, c, 15] > 0 and st[ap, c, 3] > 0:
+        b = st[ap, c, 3]
+        rows.append([(st[ap, c, k] - b) / 1e3 for k in (12, 13, 14, 15, 2)] + [(b - prev_done) / 1e3])
+if rows:
+    r = np.array(rows)
+    print("attention items: loads/scores/softmax/item-end/signal after phase start, and phase start after QKV end"
+          " (median / max over %d CTAs):" % len(rows))
+    print("  " + "  ".join(f"{n} {np.median(r[:, i]):.1f}/{r[:, i].max():.1f}" for i, n in
+                           enumerate(["loads", "scores", "softmax", "end", "signal", "start"])))
