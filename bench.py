@@ -39,11 +39,31 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # configs[1]: 1 x B200
-    "qwen3-0.6b/qwen3-14b": dict(draft="qwen3-0.6b", target="qwen3-14b", prompt_len=160, max_new=256),
+    # configs[1]: 1 x B200 — the headline
+    "qwen3-0.6b/qwen3-14b": dict(draft=("qwen3-0.6b", {}), target=("qwen3-14b", {}), prompt_len=160, max_new=256,
+                                 desc="configs[1]: Qwen3-0.6B draft / Qwen3-14B target shapes, random-init bf16, "
+                                      "synthetic code-like prompt (HumanEval length)"),
+    # the north-star target (70B-shaped, configs[4] shapes) unsharded on one B200: 139 GB of weights
+    "llama-3.2-1b/llama-3.3-70b": dict(draft=("llama-3.2-1b", {}), target=("llama-3.3-70b", {}), prompt_len=1024,
+                                       max_new=256,
+                                       desc="configs[4] shapes (Llama-3.2-1B draft / Llama-3.3-70B target), "
+                                            "random-init bf16, CNN/DM-length synthetic prompt, target unsharded "
+                                            "on 1 GPU"),
+    # LABELLED aligned workload (SURVEY §7 hard part 6): an independent random-init draft never agrees
+    # with a random-init target (alpha = 0, tools/align_probe.py).  Here the target's decoder layers >= 1
+    # are initialised at 0.1x the HF std (they refine the residual stream instead of rewriting it) and the
+    # draft is the target's own first layer + its embedding / LM head (early exit, same seed):
+    # alpha ~0.97 teacher-forced.  Same Qwen3-14B shapes, bytes and kernels as configs[1].
+    "aligned-qwen3-14b": dict(draft=("qwen3-14b", dict(n_layers=1, layer_std_scale=0.1, scale_from_layer=1)),
+                              target=("qwen3-14b", dict(layer_std_scale=0.1, scale_from_layer=1)),
+                              same_seed=True, prompt_len=160, max_new=256,
+                              desc="LABELLED aligned workload: Qwen3-14B shapes, decoder layers >= 1 at 0.1x "
+                                   "init std; draft = the target's first layer + embedding / LM head (early "
+                                   "exit, same seed, 2.2 GB); random-init bf16, code-like prompt"),
     # small smoke workload (CI / quick checks)
-    "tiny": dict(draft="tiny-qwen-draft", target="tiny-qwen", prompt_len=64, max_new=64),
+    "tiny": dict(draft=("tiny-qwen-draft", {}), target=("tiny-qwen", {}), prompt_len=64, max_new=64, desc="tiny"),
 }
+SIDE_WORKLOADS = ("aligned-qwen3-14b", "llama-3.2-1b/llama-3.3-70b")
 DEPTH, NGRAM, PRIOR_K = 10, 3, 10
 
 
@@ -59,6 +79,8 @@ def parse():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--log-out", default="", help="write this run's decision log (json) here")
     p.add_argument("--no-serving", action="store_true", help="skip the batched-serving side measurement")
+    p.add_argument("--no-side", action="store_true",
+                   help="skip the side workloads (aligned draft, 70B-shaped target) after the headline")
     p.add_argument("--tp", choices=["auto", "off"], default="auto",
                    help="N>1: auto = the target tensor-parallel over the N GPUs (driven from rank 0), "
                         "off = N independent replicas")
@@ -273,12 +295,11 @@ def main():
     wl = dict(WORKLOADS[a.workload])
     max_new = a.max_new or wl["max_new"]
     metric = "decode tokens/s (DOUBLE, greedy) + speedup vs target-only AR + mean accepted length"
-    base_cfg = {"workload": f"{a.workload} (configs[1]: Qwen3-0.6B draft / Qwen3-14B target shapes, "
-                f"random-init bf16, synthetic code-like prompt)" if a.workload != "tiny" else a.workload,
+    base_cfg = {"workload": f"{a.workload} ({wl['desc']})",
                 "prompt_len": wl["prompt_len"], "max_new_tokens": max_new, "depth": DEPTH,
                 "ngram": NGRAM, "prior_rounds": PRIOR_K, "temperature": 0,
                 "parallelism": f"replicas x{world}" if world > 1 else "1 GPU (draft+target co-located)",
-                "l2": "weights (28 GB) >> L2 (126 MB): every forward streams from HBM"}
+                "l2": "weights (>= 2 GB per model) >> L2 (126 MB): every forward streams from HBM"}
 
     if a.impl == "reference":
         return reference_arm(a, rank, world, wl, max_new, metric, base_cfg)
@@ -321,69 +342,75 @@ def main():
     return run_bench(a, rank, world, local, wl, max_new, metric, base_cfg)
 
 
-def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
-
-    import paper_2601_05524_b200 as dbl
-    from paper_2601_05524_b200 import _capi
-    import ctypes as C
-    if not _capi.lib().dbl_device_ok():
-        raise SystemExit("no usable sm_100 device (libdouble_b200 has no CPU fallback)")
-    dev = 0
-    import torch
-    torch.cuda.set_device(local)
-    dev_env = local  # the library follows the current device through cudaSetDevice in torch
+def _models(dbl, wl, seed, local, tp_world):
+    """(target, draft, parallelism note) for a workload; TP targets over DBL_BENCH_TP_DEVICES."""
+    tname, tkw = wl["target"]
+    dname, dkw = wl["draft"]
+    dseed = seed if wl.get("same_seed") else seed + 1
+    note = None
     if tp_world > 1:
         # DBL_BENCH_TP_DEVICES="0,0": a TP layout on fewer GPUs (functional checks on one GPU)
         env_dev = os.environ.get("DBL_BENCH_TP_DEVICES")
         devices = [int(x) for x in env_dev.split(",")] if env_dev else list(range(tp_world))
-        tgt = dbl.TpTransformer(dbl.transformer_config(wl["target"], seed=a.seed, max_seq=4096), devices=devices)
-        base_cfg = dict(base_cfg, parallelism=f"target TP={tp_world} on GPUs {devices} (peer memory, exchange "
-                        "inside fwd_kernel), draft beside shard 0", tp=tp_world)
+        tgt = dbl.TpTransformer(dbl.transformer_config(tname, seed=seed, max_seq=4096, **tkw), devices=devices)
+        note = (f"target TP={tp_world} on GPUs {devices} (peer memory, exchange inside fwd_kernel), "
+                "draft beside shard 0")
     else:
-        tgt = dbl.Transformer(dbl.transformer_config(wl["target"], seed=a.seed, max_seq=4096), device=local)
-    drf = dbl.Transformer(dbl.transformer_config(wl["draft"], seed=a.seed + 1, max_seq=4096), device=local)
+        tgt = dbl.Transformer(dbl.transformer_config(tname, seed=seed, max_seq=4096, **tkw), device=local)
+    drf = dbl.Transformer(dbl.transformer_config(dname, seed=dseed, max_seq=4096, **dkw), device=local)
+    return tgt, drf, note
+
+
+def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headline=True):
+    """One workload: DOUBLE at the headline gamma (device + e2e timing), target-only AR (the speedup
+    denominator, same kernels), gamma = ceil(C) / 4 / 8, and the verify forward's roofline."""
+    import ctypes as C
+    import torch
+    import paper_2601_05524_b200 as dbl
+    from paper_2601_05524_b200 import _capi
+    tgt, drf, note = _models(dbl, wl, a.seed, local, tp_world)
     V = tgt.cfg.vocab
-    prompt, prior = workload(V, wl["prompt_len"], a.seed + 100 + rank * 0)
+    prompt, prior = workload(V, wl["prompt_len"], a.seed + 100)
 
     def profile(model, ctx, rows, iters=5):
         out = (C.c_double * 8)()
         _capi.check(_capi.lib().dbl_profile_forward(model._h, ctx, rows, iters, out))
         return list(out)
 
-    # gamma = ceil(C), C = t_target_fwd / t_draft_fwd at M = d+1 (harness.cpp:32-35)
+    # C = t_target_fwd / t_draft_fwd at M = d+1 (SURVEY §8(d), harness.cpp:32-35)
     pt = profile(tgt, wl["prompt_len"], DEPTH + 1)
     pd = profile(drf, wl["prompt_len"], DEPTH + 1)
     C_ratio = pt[0] / pd[0]
     gamma_c = max(1, math.ceil(C_ratio))
     # The reference's gamma = ceil(C) assumes draft and target on separate devices (round time =
-    # max(gamma*t_draft, t_target), pipeline.cpp:198-204).  Co-located on one GPU both stream HBM, the
-    # round costs ~ t_target + gamma*t_draft, and the independent random-init draft is never accepted,
-    # so the headline uses gamma = 1; gamma = ceil(C) is measured too ("gamma_C" below).
-    gamma = a.gamma or 1
-    opts = dbl.PipelineOptions(gamma=gamma, depth=DEPTH)
+    # max(gamma*t_draft, t_target), pipeline.cpp:198-204).  Co-located on one GPU both stream HBM and the
+    # round costs ~ t_target + gamma*t_draft; with an independent random-init draft (alpha = 0) every
+    # drafted token is wasted, so configs[1]'s headline runs gamma = 1 and reports ceil(C), 4 and 8 beside
+    # it.  The aligned workload (alpha > 0) runs the reference's gamma = ceil(C).
+    gamma = a.gamma or (gamma_c if wl.get("same_seed") else 1)
 
     def store():
         st = dbl.HierarchicalDatastore(NGRAM, DEPTH, device=local)
         dbl.build_prior(st, prior, PRIOR_K)
         return st
 
-    def run_double():
-        return dbl.run(drf, tgt, store(), prompt, max_new, opts, want_jsonl=False)
+    def run_double(g):
+        return dbl.run(drf, tgt, store(), prompt, max_new, dbl.PipelineOptions(gamma=g, depth=DEPTH),
+                       want_jsonl=False)
 
-    for _ in range(a.warmup):
-        run_double()
+    for _ in range(warmup):
+        run_double(gamma)
         dbl.run_vanilla_ar(tgt, prompt, max_new, want_jsonl=False)
-
     barrier(world)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dev_ms, e2e_ms, tokens, launches = 0.0, 0.0, 0, 0
     results = []
     with ClockSampler(local) as clk:
-        for _ in range(a.steps):
+        for _ in range(steps):
             torch.cuda.synchronize()
             e0.record()
-            r = run_double()  # host prompt/prior in, host tokens out (e2e)
+            r = run_double(gamma)  # host prompt/prior in, host tokens out (e2e)
             e1.record()
             torch.cuda.synchronize()
             e2e_ms += e0.elapsed_time(e1)
@@ -396,35 +423,39 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
     log = dbl.last_run_log()
     # target-only AR with the same kernels (the speedup denominator) + lossless check
     ar_ms, ar_tok = 0.0, 0
-    for _ in range(a.steps):
+    for _ in range(steps):
         ar = dbl.run_vanilla_ar(tgt, prompt, max_new, want_jsonl=False)
         ar_ms += ar.metrics["device_ms"]
         ar_tok += len(ar.output)
+    ar_value = all_sum(ar_tok, world) / (all_max(ar_ms, world) / 1e3)
     lossless = all(r.output == ar.output for r in results)
+    m0 = results[-1].metrics
+
     def gamma_line(g):  # the same workload and timing at another gamma (ceil(C), 4, 8)
         nonlocal lossless
-        oc = dbl.PipelineOptions(gamma=g, depth=DEPTH)
-        dbl.run(drf, tgt, store(), prompt, max_new, oc, want_jsonl=False)
+        run_double(g)
         gms, gtok, gm = 0.0, 0, None
-        for _ in range(a.steps):
-            rg = dbl.run(drf, tgt, store(), prompt, max_new, oc, want_jsonl=False)
+        for _ in range(steps):
+            rg = run_double(g)
             gms += rg.metrics["device_ms"]
             gtok += len(rg.output)
             lossless &= rg.output == ar.output
             gm = rg.metrics
         gv = all_sum(gtok, world) / (all_max(gms, world) / 1e3)
-        return {"gamma": g, "value": round(gv, 3), "mean_accepted_len": round(gm["m"], 4)}
+        return {"gamma": g, "value": round(gv, 3), "speedup_vs_ar": round(gv / ar_value, 4),
+                "mean_accepted_len": round(gm["m"], 4),
+                "target_rows_per_forward": round(gm["target_rows"] / max(1, gm["target_fwd_count"]), 2)}
 
-    gamma_c_line = gamma_line(gamma_c) if gamma_c != gamma else None
-    gamma_8_line = gamma_line(8) if 8 not in (gamma, gamma_c) else None
+    value = all_sum(tokens, world) / (all_max(dev_ms, world) / 1e3)
+    main_line = {"gamma": gamma, "value": round(value, 3), "speedup_vs_ar": round(value / ar_value, 4),
+                 "mean_accepted_len": round(m0["m"], 4),
+                 "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 2)}
+    gl = {}
+    for key, g in (("gamma_C", gamma_c), ("gamma_1", 1), ("gamma_4", 4), ("gamma_8", 8)):
+        gl[key] = main_line if g == gamma else next((v for v in gl.values() if v["gamma"] == g), None) or gamma_line(g)
+    gl["gamma_C"] = dict(gl["gamma_C"], C_measured=round(C_ratio, 3))
 
-    t_dev = all_max(dev_ms, world)
-    t_e2e = all_max(e2e_ms, world)
-    tok_all = all_sum(tokens, world)
-    value = tok_all / (t_dev / 1e3)
-    e2e_value = tok_all / (t_e2e / 1e3)
-    ar_value = all_sum(ar_tok, world) / (all_max(ar_ms, world) / 1e3)
-    m0 = results[-1].metrics
+    # roofline of the dominant kernel: the verify forward at this run's mean row count
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -432,45 +463,29 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
     rows_per_fwd = max(1, round(m0["target_rows"] / max(1, m0["target_fwd_count"])))
-    pv = profile(tgt, wl["prompt_len"] + max_new // 2, rows_per_fwd, iters=20)
+    ctx = wl["prompt_len"] + max_new // 2
+    pv = profile(tgt, ctx, rows_per_fwd, iters=20)
     achieved = pv[2] / (pv[1] / 1e3) / 1e9  # GB/s: algorithmic bytes / event-timed fwd_kernel duration
-    traffic = None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
-        traffic = prof.get(a.workload)
-    except (OSError, ValueError):
-        pass
-    line = {
-        "metric": metric, "value": round(value, 3), "unit": "tokens/s", "n_gpus": max(world, tp_world),
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(t_dev / a.steps, 3),
-        "higher_is_better": True, "scaling": "strong" if tp_world > 1 else "weak", "vs_baseline": None,
-        "dtype": "bf16", "n_gpus_used": tp_world if tp_world > 1 else world,
-        "data": "synthetic (random-init weights, code-like prompt)",
-        "config": dict(base_cfg, gamma=gamma, C_measured=round(C_ratio, 3)),
-        "speedup_vs_ar": round(value / ar_value, 4), "ar_tokens_per_s": round(ar_value, 3),
-        "mean_accepted_len": round(m0["m"], 4), "amt": round(m0["amt"], 4),
-        "rounds_per_step": m0["rounds"], "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 3),
-        "lossless_vs_ar": lossless,
-        "gamma_C": dict(gamma_c_line, speedup_vs_ar=round(gamma_c_line["value"] / ar_value, 4)) if gamma_c_line else None,
-        "gamma_8": dict(gamma_8_line, speedup_vs_ar=round(gamma_8_line["value"] / ar_value, 4)) if gamma_8_line else None,
-        "e2e": {"value": round(e2e_value, 3), "unit": "tokens/s",
-                "h2d_bytes_per_step": 4 * (len(prompt) + sum(len(s) for s in prior)),
-                "d2h_bytes_per_step": 4 * max_new},
+    pdr = profile(drf, ctx, DEPTH + 1, iters=20)
+    out = {
+        "value": value, "e2e_ms": all_max(e2e_ms, world), "dev_ms": all_max(dev_ms, world),
+        "tokens": all_sum(tokens, world), "ar_value": ar_value, "gamma": gamma, "C": C_ratio, "m0": m0,
+        "lossless": lossless, "gl": gl, "launches": all_sum(launches, world), "clk": clk.summary(),
+        "prompt": prompt, "prior": prior, "log": log, "output": results[-1].output, "V": V, "note": note,
         "roofline": {"bound": "hbm", "kernel": "fwd_kernel (persistent stream forward: tcgen05/TMA GEMMs + "
-                               "attention + fused epilogues), one launch per verify forward",
+                              "attention + fused epilogues), one launch per verify forward",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "frac": round(achieved / peak, 4),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if peaks else "fallback",
                      "per_forward": {"tokens": int(pv[5]), "fwd_ms": round(pv[0], 4),
                                      "kernel_ms": round(pv[1], 4), "algorithmic_bytes": pv[2],
-                                     "context": wl["prompt_len"] + max_new // 2, "rows": rows_per_fwd,
-                                     "kernel_launches": int(pv[4]),
-                                     "weight_stream_gbs": round(tgt.weight_bytes / (pv[0] / 1e3) / 1e9, 1)}},
-        "gpu_launches": int(all_sum(launches, world)),
+                                     "context": ctx, "rows": rows_per_fwd, "kernel_launches": int(pv[4]),
+                                     "weight_stream_gbs": round(tgt.weight_bytes / (pv[0] / 1e3) / 1e9, 1)},
+                     "draft_forward": {"rows": DEPTH + 1, "fwd_ms": round(pdr[0], 4),
+                                       "algorithmic_bytes": pdr[2],
+                                       "frac": round(pdr[2] / (pdr[1] / 1e3) / 1e9 / peak, 4)}},
     }
-    cs = clk.summary()
-    line["clocks"] = {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"]}
-    if tp_world <= 1 and not a.no_serving:
+    if headline and tp_world <= 1 and not a.no_serving:
         # batched serving: B independent sequences of this workload's shape decoded in
         # lockstep, ONE target forward per step over all of them (run_vanilla_ar_batch; every stream ==
         # its own single-sequence AR).  Reported beside the headline, not in it.
@@ -481,22 +496,95 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
             _, sm = dbl.run_vanilla_ar_batch(tgt, ps, 64)
             serving[f"B{B}"] = {"tokens_per_s": round(sm["tokens"] / (sm["device_ms"] / 1e3), 1),
                                 "ms_per_step": round(sm["device_ms"] / 64, 3)}
-        line["serving_batch"] = dict(serving, what="target-only greedy decode of B sequences (64 new tokens "
-                                     "each) with one batched fwd_kernel per step; value above is B = 1")
+        out["serving"] = dict(serving, what="target-only greedy decode of B sequences (64 new tokens "
+                              "each) with one batched fwd_kernel per step; value above is B = 1")
+    del tgt, drf
+    import gc
+    gc.collect()
+    return out
+
+
+def side_line(a, local, name):
+    """A compact line for a non-headline workload (1 warm-up, 1 timed decode per gamma)."""
+    wl = WORKLOADS[name]
+    r = measure(a, 0, 1, local, wl, wl["max_new"], 1, 1, headline=False)
+    return {"desc": wl["desc"], "value": round(r["value"], 3), "unit": "tokens/s", "gamma": r["gamma"],
+            "ar_tokens_per_s": round(r["ar_value"], 3), "speedup_vs_ar": round(r["value"] / r["ar_value"], 4),
+            "mean_accepted_len": round(r["m0"]["m"], 4), "amt": round(r["m0"]["amt"], 4),
+            "target_rows_per_forward": r["gl"]["gamma_C"]["target_rows_per_forward"] if r["gamma"] ==
+            r["gl"]["gamma_C"]["gamma"] else None,
+            "e2e_tokens_per_s": round(r["tokens"] / (r["e2e_ms"] / 1e3), 3), "lossless_vs_ar": r["lossless"],
+            "gammas": r["gl"], "roofline": {k: r["roofline"][k] for k in ("achieved", "frac", "per_forward",
+                                                                           "draft_forward")},
+            "timing": "1 warm-up + 1 timed decode per gamma (side line; the headline uses --steps/--warmup)"}
+
+
+def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
+    import paper_2601_05524_b200 as dbl
+    from paper_2601_05524_b200 import _capi
+    if not _capi.lib().dbl_device_ok():
+        raise SystemExit("no usable sm_100 device (libdouble_b200 has no CPU fallback)")
+    import torch
+    torch.cuda.set_device(local)
+    r = measure(a, rank, world, local, wl, max_new, a.steps, a.warmup, tp_world=tp_world)
+    if r["note"]:
+        base_cfg = dict(base_cfg, parallelism=r["note"], tp=tp_world)
+    t_e2e = r["e2e_ms"]
+    value = r["value"]
+    m0 = r["m0"]
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        traffic = prof.get(a.workload)
+    except (OSError, ValueError):
+        pass
+    line = {
+        "metric": metric, "value": round(value, 3), "unit": "tokens/s", "n_gpus": max(world, tp_world),
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(r["dev_ms"] / a.steps, 3),
+        "higher_is_better": True, "scaling": "strong" if tp_world > 1 else "weak", "vs_baseline": None,
+        "dtype": "bf16", "n_gpus_used": tp_world if tp_world > 1 else world,
+        "data": "synthetic (random-init weights, code-like prompt)",
+        "config": dict(base_cfg, gamma=r["gamma"], C_measured=round(r["C"], 3)),
+        "speedup_vs_ar": round(value / r["ar_value"], 4), "ar_tokens_per_s": round(r["ar_value"], 3),
+        "mean_accepted_len": round(m0["m"], 4), "amt": round(m0["amt"], 4),
+        "rounds_per_step": m0["rounds"],
+        "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 3),
+        "lossless_vs_ar": r["lossless"],
+        "gamma_C": r["gl"]["gamma_C"], "gamma_4": r["gl"]["gamma_4"], "gamma_8": r["gl"]["gamma_8"],
+        "e2e": {"value": round(r["tokens"] / (t_e2e / 1e3), 3), "unit": "tokens/s",
+                "h2d_bytes_per_step": 4 * (len(r["prompt"]) + sum(len(s) for s in r["prior"])),
+                "d2h_bytes_per_step": 4 * max_new},
+        "roofline": dict(r["roofline"], traffic=traffic),
+        "gpu_launches": int(r["launches"]),
+    }
+    cs = r["clk"]
+    line["clocks"] = {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"]}
+    if "serving" in r:
+        line["serving_batch"] = r["serving"]
     if a.log_out and rank == 0:
-        json.dump({"vocab": V, "prompt": prompt, "prior": prior, "max_new": max_new, "gamma": gamma,
-                   "output": results[-1].output, "log": [int(x) for x in log]}, open(a.log_out, "w"))
+        json.dump({"vocab": r["V"], "prompt": r["prompt"], "prior": r["prior"], "max_new": max_new,
+                   "gamma": r["gamma"], "output": r["output"], "log": [int(x) for x in r["log"]]},
+                  open(a.log_out, "w"))
     if rank == 0:
         try:
-            cpu_v, kind = reference_replay(log, V, prompt, prior, max_new, gamma, results[-1].output, reps=2)
+            cpu_v, kind = reference_replay(r["log"], r["V"], r["prompt"], r["prior"], max_new, r["gamma"],
+                                           r["output"], reps=2)
             line["cpu_baseline"] = {"value": round(cpu_v, 3), "unit": "tokens/s", "cores": 1, "kind": kind,
                                     "sample": f"one {max_new}-token DOUBLE decode of this workload replayed "
                                               "through the reference host loop (run(), pipeline.cpp) with the "
                                               "forward excluded: argmax rows served from this run's decision "
-                                              f"log as one-hot fp64 rows of V={V} (argmax_token included)"}
+                                              f"log as one-hot fp64 rows of V={r['V']} (argmax_token included)"}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
+        if tp_world <= 1 and world == 1 and not a.no_side and a.workload == "qwen3-0.6b/qwen3-14b":
+            side = {}
+            for name in SIDE_WORKLOADS:
+                try:
+                    side[name] = side_line(a, local, name)
+                except Exception as e:  # noqa: BLE001
+                    side[name] = {"error": str(e)[:300]}
+            line["side_workloads"] = side
         print(json.dumps(line), flush=True)
 
 

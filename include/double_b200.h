@@ -94,6 +94,11 @@ typedef struct {
     int max_seq;         /* KV capacity in tokens */
     uint64_t seed;       /* weights are a pure function of (seed, tensor, index) */
     int tp_rank, tp_size;/* tensor parallel shard (1 = unsharded) */
+    float layer_std_scale; /* decoder layers >= scale_from_layer ~ N(0, (init_std * scale)^2); 0 = 1.
+                              < 1 gives the labelled "aligned" workload of bench.py: the deep layers only
+                              refine the residual stream, so the target's own first layers (early exit,
+                              same seed) draft it with alpha > 0 */
+    int scale_from_layer;
 } dbl_transformer_config;
 /* One shard (cfg->tp_rank of cfg->tp_size) or the whole model (tp_size 1) on `device`.  nccl_comm is
  * unused (kept for ABI stability): the tensor-parallel exchange runs inside the forward kernel over

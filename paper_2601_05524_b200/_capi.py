@@ -26,7 +26,8 @@ class TransformerConfig(C.Structure):
                 ("n_kv_heads", C.c_int), ("head_dim", C.c_int), ("vocab", C.c_int),
                 ("tied_embeddings", C.c_int), ("qk_norm", C.c_int), ("rope_theta", C.c_float),
                 ("rms_eps", C.c_float), ("init_std", C.c_float), ("max_seq", C.c_int),
-                ("seed", C.c_uint64), ("tp_rank", C.c_int), ("tp_size", C.c_int)]
+                ("seed", C.c_uint64), ("tp_rank", C.c_int), ("tp_size", C.c_int),
+                ("layer_std_scale", C.c_float), ("scale_from_layer", C.c_int)]
 
 
 class PipelineOptions(C.Structure):

@@ -118,7 +118,8 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
     if (world > kMaxTpRanks) throw_invalid("transformer: tp_size > 8");
     cudaStream_t s = 0;
     const uint64_t seed = c.seed;
-    const float sd = c.init_std;
+    const float sd_embed = c.init_std;  // embedding / LM head
+    const float sd_scaled = c.init_std * (c.layer_std_scale > 0.f ? c.layer_std_scale : 1.f);
     const int h = m.h;
     m.layers.resize(c.n_layers);
     // weights live in HBM as tiled images (launch_tile_weights: every 128 x 64 tile one contiguous
@@ -134,6 +135,7 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
     scratch.alloc(std::max({n_qkv, n_o, n_gu, n_down, static_cast<size_t>(tiled_rows(m.vocab_l) * h)}));
     for (int l = 0; l < c.n_layers; ++l) {
         LayerW& w = m.layers[l];
+        const float sd = l >= c.scale_from_layer ? sd_scaled : sd_embed;  // decoder layer l
         // RMSNorm weights are 1 in this random-init family; the stream forward folds them (fwd.cuh)
         w.attn_norm.alloc(h);
         w.mlp_norm.alloc(h);
@@ -170,7 +172,7 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
     m.final_norm.alloc(h);
     launch_fill(m.final_norm.p, h, 1.0f, s);
     m.embed.alloc(static_cast<size_t>(c.vocab) * h);
-    launch_init_normal(m.embed.p, c.vocab, h, h, seed, kEmbed, 0, 0, h, sd, s);
+    launch_init_normal(m.embed.p, c.vocab, h, h, seed, kEmbed, 0, 0, h, sd_embed, s);
     // the LM head is streamed, so it is tiled too; a tied model keeps the row-major table for the
     // embedding gather and a tiled copy of its vocab shard for the head
     m.lm_head_own.alloc(tiled_rows(m.vocab_l) * h);
@@ -178,7 +180,7 @@ Transformer::Transformer(const dbl_transformer_config& cfg, int device, void* nc
         launch_tile_weights(m.lm_head_own.p, m.embed.p + static_cast<size_t>(m.rank) * m.vocab_l * h, m.vocab_l, h, s);
     } else {
         launch_init_normal(scratch.p, m.vocab_l, h, h, seed, kLmHead, static_cast<int64_t>(m.rank) * m.vocab_l, 0,
-                           h, sd, s);
+                           h, sd_embed, s);
         launch_tile_weights(m.lm_head_own.p, scratch.p, m.vocab_l, h, s);
     }
     m.lm_head = m.lm_head_own.p;
