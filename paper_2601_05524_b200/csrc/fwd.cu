@@ -613,7 +613,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
             tmem_ld<CH>(x.taddr + ch, v);
             const int nc = min(CH, tp - ch);
             if (x.n_contrib > 1) {
-                if (!x.has_pre) presum(x, ch);
+                if (!x.has_pre || ch > 0) presum(x, ch);
 #pragma unroll
                 for (int i = 0; i < CH; ++i) v[i] += x.pre[i * kBM + r];
             }
@@ -656,7 +656,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         // accumulator is ready — every path (row count, early or not) uses this one order
         const bool fold = !kTP && P.epi == kFeResid && x.n_contrib > 1;
         if (x.n_contrib > 1 && !tp_resid) {
-            if (!x.has_pre) presum(x, ch, fold ? a.resid + static_cast<long long>(ch) * h + n : nullptr);
+            if (!x.has_pre || ch > 0) presum(x, ch, fold ? a.resid + static_cast<long long>(ch) * h + n : nullptr);
 #pragma unroll
             for (int i = 0; i < CH; ++i) v[i] += x.pre[i * kBM + r];
         }
@@ -895,12 +895,17 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             // issued as soon as a slot frees — across phase boundaries, never waiting on data; a stage's
             // barrier expects both byte counts, so the activation load can follow later (once the phase's
             // input is complete) and simply completes the transaction.  Only the T valid token rows are
-            // loaded (boxes of 1..16 rows): rows >= T keep stale data that reaches only padded columns.
+            // loaded, in as few copies as possible (the producer's issue rate bounds the stream): one box of
+            // 4 / 8 / 16 rows up to 16 tokens, else 64-row boxes + one 32 and / or one 16 (tp is a multiple of
+            // 16, so every box lands inside the stage).  Rows >= T keep stale data that reaches only padded
+            // columns.
             for (int i = 0; i < 5; ++i) tma_prefetch_desc(&a.wmaps[i]);
-            const int xb_i = T <= 1 ? 0 : T <= 2 ? 1 : T <= 4 ? 2 : T <= 8 ? 3 : 4;
-            const int x_rows = 1 << xb_i, n_xbox = T <= 16 ? 1 : (T + 15) / 16;
-            const uint32_t stage_tx = static_cast<uint32_t>(kABytes + n_xbox * x_rows * kBK * 2);
-            for (int i = 0; i < 3; ++i) tma_prefetch_desc(&a.xmaps[i][xb_i]);
+            const int n16 = (T + 15) / 16;
+            const int xb_i = T <= 4 ? 0 : T <= 8 ? 1 : 2;  // single box (T <= 16): 4 << xb_i rows
+            const int x_rows_total = T <= 16 ? (4 << xb_i) : n16 * 16;
+            const uint32_t stage_tx = static_cast<uint32_t>(kABytes + x_rows_total * kBK * 2);
+            for (int i = 0; i < 3; ++i)
+                for (int b = 0; b < 5; ++b) tma_prefetch_desc(&a.xmaps[i][b]);
             Cur w{}, x{};
             seek(w, a, c, G);
             seek(x, a, c, G);
@@ -934,9 +939,21 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         stamp(a, x.p, 1);
                     }
                     if (ok) {
-                        for (int j = 0; j < n_xbox; ++j)
-                            tma_load_2d(sB + xr.st * bbytes + j * 2048, &a.xmaps[x.xmap][xb_i], &full[xr.st],
-                                        x.kb * kBK, j * 16, kEvictLast);
+                        uint8_t* dst = sB + xr.st * bbytes;
+                        const CUtensorMap* xm = a.xmaps[x.xmap];
+                        if (T <= 16) {
+                            tma_load_2d(dst, &xm[xb_i], &full[xr.st], x.kb * kBK, 0, kEvictLast);
+                        } else {
+                            const int q64 = n16 >> 2, rem = n16 & 3;
+                            for (int j = 0; j < q64; ++j)
+                                tma_load_2d(dst + j * 64 * kBK * 2, &xm[4], &full[xr.st], x.kb * kBK, j * 64, kEvictLast);
+                            int row = q64 * 64;
+                            if (rem & 2) {
+                                tma_load_2d(dst + row * kBK * 2, &xm[3], &full[xr.st], x.kb * kBK, row, kEvictLast);
+                                row += 32;
+                            }
+                            if (rem & 1) tma_load_2d(dst + row * kBK * 2, &xm[2], &full[xr.st], x.kb * kBK, row, kEvictLast);
+                        }
                         xr.next(S);
                         --pending;
                         step(x, a, c, G);
@@ -1092,8 +1109,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
                                q, lane, et, r, rs, red, sval, sidx, tag, (tp_ep << 12) | static_cast<unsigned long long>(p + 1),
                                false, sm.pre, &sm.peers, &sm.bt};
-                    const bool early = finisher && n_contrib > 1 && tp == 16;
-                    if (early) {  // the other contributors are (nearly always) done: sum them now
+                    const bool early = finisher && n_contrib > 1;
+                    if (early) {  // the other contributors are (nearly always) done: sum them now (first
+                                  // 16-column chunk; finish_tile presums any further chunks itself)
                         wait_partials(tc);
                         // into sm.pre (own thread's row only), the residual folded in too (off the tail's chain)
                         presum(tc, 0, !kTP && P.epi == kFeResid ? a.resid + m * kBM + r : nullptr);

@@ -42,7 +42,7 @@ enum FwdEpi : int { kFeQkv = 0, kFeResid = 1, kFeSilu = 2, kFeLogits = 3 };
 
 struct FwdPhase {
     int kind, epi;
-    int wmap, xmap;      // FwdArgs::wmaps / xmaps index (weights box 128x64, activations box 16x64)
+    int wmap, xmap;      // FwdArgs::wmaps / xmaps index (weights box 128x64, activations boxes 4..64 x 64)
     int w_row0;          // first row of this phase's weights in its (all-layers) tensor map
     int n_out, K, n_tiles, kb;
     int units;           // n_tiles * kb (stream-K units; < 2^31 / #SMs, host-checked)
@@ -83,7 +83,7 @@ struct FwdBatch {
 
 struct FwdArgs {
     CUtensorMap wmaps[5];  // qkv, o, gate|up, down (all layers stacked), lm head
-    CUtensorMap xmaps[3][5];  // xb, attn, act; boxes of 1, 2, 4, 8, 16 token rows
+    CUtensorMap xmaps[3][5];  // xb, attn, act; boxes of 4, 8, 16, 32, 64 token rows
     const FwdPhase* ph;
     int n_ph;
     int dbg;               // DBL_FWD_DBG (timing experiments only; results invalid): 1 no X loads, 2 no MMA

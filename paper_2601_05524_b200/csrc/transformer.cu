@@ -70,7 +70,7 @@ struct TfCache final : LaneCache {
     DevBuf<int> err;
     DevBuf<float2> rope;                    // [capacity][hd/2] (cos, sin)
     DevBuf<FwdPhase> phases;
-    CUtensorMap xmaps[3][5];  // xb, attn, act x boxes of 1, 2, 4, 8, 16 token rows
+    CUtensorMap xmaps[3][5];  // xb, attn, act x boxes of 4, 8, 16, 32, 64 token rows
     DevBuf<unsigned long long> done, epoch, slot_flag;
     DevBuf<int> row_base;  // batched forwards: per-lane forward-row base (FwdBatch::row_base)
     // tensor parallel: this rank's exchange buffers (written by every rank) and all ranks' addresses
@@ -280,9 +280,9 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     // ---- the forward's phase list (fwd.cuh); tensor maps: W 0..4 = qkv, o, gate|up, down, lm head;
     // X 0..2 = xb, attn, act
     for (int b = 0; b < 5; ++b) {
-        c.xmaps[0][b] = make_tmap_bf16_2d(c.xb.p, kMaxTp, m.h, 1 << b);
-        c.xmaps[1][b] = make_tmap_bf16_2d(c.attn.p, kMaxTp, m.q_dim, 1 << b);
-        c.xmaps[2][b] = make_tmap_bf16_2d(c.act.p, kMaxTp, m.ffn_l, 1 << b);
+        c.xmaps[0][b] = make_tmap_bf16_2d(c.xb.p, kMaxTp, m.h, 4 << b);
+        c.xmaps[1][b] = make_tmap_bf16_2d(c.attn.p, kMaxTp, m.q_dim, 4 << b);
+        c.xmaps[2][b] = make_tmap_bf16_2d(c.act.p, kMaxTp, m.ffn_l, 4 << b);
     }
     const int x_xb = 0, x_attn = 1, x_act = 2;
     std::vector<FwdPhase> ph;
