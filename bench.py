@@ -485,6 +485,8 @@ def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headl
                                        "algorithmic_bytes": pdr[2],
                                        "frac": round(pdr[2] / (pdr[1] / 1e3) / 1e9 / peak, 4)}},
     }
+    if headline:
+        out["retrieval"] = retrieval_probe(dbl, local, prompt, prior, V)
     if headline and tp_world <= 1 and not a.no_serving:
         # batched serving: B independent sequences of this workload's shape decoded in
         # lockstep, ONE target forward per step over all of them (run_vanilla_ar_batch; every stream ==
@@ -502,6 +504,29 @@ def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headl
     import gc
     gc.collect()
     return out
+
+
+def retrieval_probe(dbl, local, prompt, prior, V):
+    """Device lookup latency (K1): on this workload's store, and on a paper-scale prior (~9.6 MB of
+    tokens, the paper's K = 10 prior is ~9.5 MB) loaded by build_prior into the device
+    n-gram index (store.cuh)."""
+    st = dbl.HierarchicalDatastore(NGRAM, DEPTH, device=local)
+    dbl.build_prior(st, prior, PRIOR_K)
+    us_small = st.profile_lookup(prompt, DEPTH, 200)
+    seq_len, n_seq = 64, 37500
+    flat = code_like_stream(V, seq_len * n_seq, 4242)
+    seqs = [flat[i * seq_len:(i + 1) * seq_len] for i in range(n_seq)]
+    big = dbl.HierarchicalDatastore(NGRAM, DEPTH, device=local)
+    t0 = time.perf_counter()
+    dbl.build_prior(big, seqs, n_seq)
+    build_ms = (time.perf_counter() - t0) * 1e3
+    ctxs = [flat[i:i + 32] for i in range(1000, len(flat) - 64, len(flat) // 8)]
+    us_big = statistics.median(big.profile_lookup(c, DEPTH, 100) for c in ctxs)
+    return {"kernel": "lookup (K1, one CTA per query: index probes + tail scan)",
+            "workload_store_lookup_us": round(us_small, 2),
+            "paper_scale_prior": {"tokens": len(flat), "mbytes": round(4 * len(flat) / 1e6, 2),
+                                  "index_entries": big.prior.index_entries,
+                                  "build_prior_ms": round(build_ms, 1), "lookup_us_median": round(us_big, 2)}}
 
 
 def side_line(a, local, name):
@@ -561,6 +586,8 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
     line["clocks"] = {"sm_mhz": cs["sm_mhz"], "sm_max_mhz": cs["sm_max_mhz"], "reasons": cs["reasons"]}
     if "serving" in r:
         line["serving_batch"] = r["serving"]
+    if "retrieval" in r:
+        line["retrieval"] = r["retrieval"]
     if a.log_out and rank == 0:
         json.dump({"vocab": r["V"], "prompt": r["prompt"], "prior": r["prior"], "max_new": max_new,
                    "gamma": r["gamma"], "output": r["output"], "log": [int(x) for x in r["log"]]},

@@ -75,6 +75,13 @@ int dbl_store_lookup_batch(dbl_store_t s, int n_q, const int64_t* q_offsets, con
                            int32_t* out_source, int32_t* out_order);
 /* LookupStats (datastore.hpp:39-67): lookups, prior, dynamic, rejected, fallback, misses */
 int dbl_store_stats(dbl_store_t s, int64_t out[6]);
+/* Device n-gram index over a layer's current sequences: the device form of NGramIndex's n-gram ->
+ * occurrence map (datastore.cpp:9-20); build_prior / a dstore-v1 prior build it automatically, later
+ * inserts into the layer are scanned until the next build.  Lookup results are identical either way. */
+int dbl_store_build_index(dbl_store_t s, int layer);
+int dbl_store_index_entries(dbl_store_t s, int layer, int64_t* entries); /* 0: layer not indexed */
+/* mean device time of one lookup (iters back-to-back single-CTA lookups on one stream, CUDA events) */
+int dbl_store_profile_lookup(dbl_store_t s, const int32_t* ctx, int L, int d, int iters, double* us_per_lookup);
 
 /* ===================================================================== models
  * Replaces specpar::TableModel + forward / forward_batch / argmax_token (model.hpp:18-48,

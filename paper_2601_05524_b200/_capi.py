@@ -92,6 +92,9 @@ PROTOTYPES = {
                          C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "dbl_store_lookup_batch": [VP, C.c_int, I64P, I32P, I32P, C.c_int, I32P, I32P, I32P, I32P],
     "dbl_store_stats": [VP, I64P],
+    "dbl_store_build_index": [VP, C.c_int],
+    "dbl_store_index_entries": [VP, C.c_int, I64P],
+    "dbl_store_profile_lookup": [VP, I32P, C.c_int, C.c_int, C.c_int, F64P],
     "dbl_table_create": [C.c_int, C.c_int, C.c_int64, I32P, F64P, F64P, C.c_int, C.POINTER(VP)],
     "dbl_transformer_create": [C.POINTER(TransformerConfig), C.c_int, VP, C.POINTER(VP)],
     "dbl_tp_transformer_create": [C.POINTER(TransformerConfig), I32P, C.c_int, C.POINTER(VP)],

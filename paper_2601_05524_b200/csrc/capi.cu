@@ -209,6 +209,22 @@ int dbl_store_flush_session(dbl_store_t s) {
 int dbl_store_clear_layer(dbl_store_t s, int layer) {
     return guarded([&] { need(s, "store"); s->impl->clear_layer(layer, 0); });
 }
+int dbl_store_build_index(dbl_store_t s, int layer) {
+    return guarded([&] { need(s, "store"); s->impl->build_index(layer, 0); });
+}
+int dbl_store_index_entries(dbl_store_t s, int layer, int64_t* entries) {
+    return guarded([&] { need(s, "store"); need(entries, "entries"); *entries = s->impl->index_entries(layer); });
+}
+int dbl_store_profile_lookup(dbl_store_t s, const int32_t* ctx, int L, int d, int iters, double* us) {
+    return guarded([&] {
+        need(s, "store");
+        need(ctx, "ctx");
+        need(us, "us_per_lookup");
+        if (L <= 0) dbl::throw_invalid("lookup: empty context");
+        if (iters < 1) dbl::throw_invalid("iters must be >= 1");
+        *us = s->impl->profile_lookup(ctx, L, d, iters);
+    });
+}
 int dbl_store_get_step(dbl_store_t s, int64_t* step) {
     return guarded([&] { need(s, "store"); need(step, "step"); *step = s->impl->step(); });
 }

@@ -3,11 +3,30 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cub/cub.cuh>
+
 #include "store.cuh"
 
 namespace dbl {
 
 namespace {
+
+// 64-bit hash of an n-gram given newest-first (k_0 = its last token): the index key.  Bit 63 is
+// clear and 0 is never produced, so 0 marks an empty table slot and ~0 an invalid entry.
+constexpr unsigned long long kNoKey = ~0ull;
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ unsigned long long ngram_step(unsigned long long h, int tok) {
+    return mix64(h ^ (static_cast<unsigned long long>(static_cast<uint32_t>(tok)) * 0x9E3779B97F4A7C15ull));
+}
+__host__ __device__ __forceinline__ unsigned long long ngram_key(unsigned long long h, int n) {
+    unsigned long long k = mix64(h + static_cast<unsigned long long>(n) * 0xD6E8FEB86659FD93ull) & 0x7FFFFFFFFFFFFFFFull;
+    return k ? k : 1ull;
+}
+constexpr unsigned long long kHashSeed = 0x243F6A8885A308D3ull;
 
 constexpr int kLookupThreads = 512;
 constexpr int kWarps = kLookupThreads / 32;
@@ -41,60 +60,150 @@ struct LookupOut {
 __device__ void lookup_cta(const StoreDesc* __restrict__ sd, const int32_t* __restrict__ ctx, int L,
                            int d, int32_t* __restrict__ out, LookupOut* res) {
     __shared__ int32_t s_key[kMaxOrder];   // s_key[j] = ctx[L-1-j]
-    __shared__ Key s_red[kWarps];
     __shared__ Key s_best[3][kMaxOrder + 1];
     __shared__ int s_pld[kWarps];
     __shared__ int s_pld_end[kMaxOrder + 1];
     __shared__ int s_choice[4];  // src, order, from, layer-seq
+    __shared__ uint2 s_run[3][kMaxOrder + 1];  // index probes: (run start, length) per (layer, order)
+    __shared__ Key s_red3[3][kWarps];
+    __shared__ Key s_redn[kMaxOrder][kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = sd->max_order;
     const int nkey = min(N, L);
     if (tid < kMaxOrder) s_key[tid] = tid < nkey ? ctx[L - 1 - tid] : -1;
     __syncthreads();
 
-    // ---- layer scans: for each layer, the best occurrence per order n (all orders in one pass)
+    // ---- index probes, all in flight together: thread l * kMaxOrder + n - 1 hashes the context's
+    // order-n suffix and probes layer l's table (one 16-byte load per slot)
+    {
+        const int l = tid / kMaxOrder, n = tid % kMaxOrder + 1;
+        if (l < 3) {
+            const LayerDesc& ly = sd->layer[l];
+            uint2 run = make_uint2(0u, 0u);
+            if (ly.idx_tokens > 0 && (l != 2 || sd->rejected_enabled) && n <= nkey &&
+                n <= min(ly.max_order, ly.idx_order)) {
+                unsigned long long hk = kHashSeed;
+                for (int j = 0; j < n; ++j) hk = ngram_step(hk, s_key[j]);
+                hk = ngram_key(hk, n);
+                for (unsigned slot = static_cast<unsigned>(hk) & ly.idx_mask;; slot = (slot + 1) & ly.idx_mask) {
+                    const uint4 e = __ldg(reinterpret_cast<const uint4*>(ly.idx_table + slot));
+                    const unsigned long long k = (static_cast<unsigned long long>(e.y) << 32) | e.x;
+                    if (k == 0ull) break;
+                    if (k == hk) {
+                        run = make_uint2(e.z, e.w);
+                        break;
+                    }
+                }
+            }
+            s_run[l][n] = run;
+        }
+    }
+
+    // ---- unindexed tails [idx_tokens, n_tokens) (the dynamic / rejected layers): the best occurrence
+    // per order n, all orders in one pass; a candidate's loads (its n-gram, its sequence record) are
+    // issued together
     for (int l = 0; l < 3; ++l) {
         const LayerDesc ly = sd->layer[l];
-        const bool enabled = (l != 2 || sd->rejected_enabled) && ly.n_tokens > 0;
+        const bool enabled = (l != 2 || sd->rejected_enabled) && ly.n_tokens > ly.idx_tokens;
         const int Nl = min(nkey, ly.max_order);
+        if (!enabled || Nl < 1) {  // uniform: nothing to scan, no reduction
+            if (tid <= kMaxOrder) s_best[l][tid] = Key{0ull, 0ull};
+            continue;
+        }
         Key best[kMaxOrder + 1];
 #pragma unroll
         for (int n = 0; n <= kMaxOrder; ++n) best[n] = Key{0ull, 0ull};
-        if (enabled && Nl >= 1) {
-            const int k0 = s_key[0];
-            for (int p = tid; p < ly.n_tokens; p += kLookupThreads) {
-                if (__ldg(ly.tokens + p) != k0) continue;  // cheap filter: last token must match
-                const int q = __ldg(ly.seq_of + p);
-                const int st = __ldg(ly.seq_start + q);
-                const int len = __ldg(ly.seq_len + q);
-                const int e = p - st;
-                const int remaining = len - e - 1;
-                const int avail = min(remaining, d);
-                if (avail <= 0) continue;
-                int m = 1;
-                const int mmax = min(Nl, e + 1);
-                while (m < mmax && __ldg(ly.tokens + p - m) == s_key[m]) ++m;
-                Key k;
-                k.hi = static_cast<unsigned long long>(__ldg(ly.seq_step + q)) ^ 0x8000000000000000ull;
-                k.lo = (static_cast<unsigned long long>(avail) << 48) |
-                       (static_cast<unsigned long long>(q) << 24) | static_cast<unsigned long long>(e);
+        const int k0 = s_key[0];
+        for (int p = ly.idx_tokens + tid; p < ly.n_tokens; p += kLookupThreads) {
+            if (__ldg(ly.tokens + p) != k0) continue;  // cheap filter: last token must match
+            const int q = __ldg(ly.seq_of + p);
+            int tk[kMaxOrder];
 #pragma unroll
-                for (int n = 1; n <= kMaxOrder; ++n)
-                    if (n <= m && key_gt(k, best[n])) best[n] = k;
-            }
+            for (int j = 1; j < kMaxOrder; ++j) tk[j] = (j < Nl && p - j >= 0) ? __ldg(ly.tokens + p - j) : -1;
+            const int st = __ldg(ly.seq_start + q);
+            const int len = __ldg(ly.seq_len + q);
+            const long long stp = __ldg(ly.seq_step + q);
+            const int e = p - st;
+            const int avail = min(len - e - 1, d);
+            if (avail <= 0) continue;
+            const int mmax = min(Nl, e + 1);
+            int m = 1;
+#pragma unroll
+            for (int j = 1; j < kMaxOrder; ++j)
+                if (m == j && j < mmax && tk[j] == s_key[j]) m = j + 1;
+            Key k;
+            k.hi = static_cast<unsigned long long>(stp) ^ 0x8000000000000000ull;
+            k.lo = (static_cast<unsigned long long>(avail) << 48) |
+                   (static_cast<unsigned long long>(q) << 24) | static_cast<unsigned long long>(e);
+#pragma unroll
+            for (int n = 1; n <= kMaxOrder; ++n)
+                if (n <= m && key_gt(k, best[n])) best[n] = k;
         }
-        for (int n = 1; n <= kMaxOrder; ++n) {  // block max-reduce per order (uniform loop)
-            if (n > N) break;
-            Key k = key_shfl_max(best[n]);
-            if (lane == 0) s_red[warp] = k;
+        // block max-reduce, every order at once: warp maxima -> shared, then warp n - 1 reduces order n
+#pragma unroll
+        for (int n = 1; n <= kMaxOrder; ++n) {
+            const Key k = key_shfl_max(best[n]);
+            if (lane == 0 && n <= N) s_redn[n - 1][warp] = k;
+        }
+        __syncthreads();
+        if (warp < N) {
+            Key r = lane < kWarps ? s_redn[warp][lane] : Key{0ull, 0ull};
+            r = key_shfl_max(r);
+            if (lane == 0) s_best[l][warp + 1] = r;
+        }
+        __syncthreads();
+    }
+    __syncthreads();  // s_run, and s_best of skipped layers
+
+    // ---- indexed runs, from the highest order down: merge each layer's run into its best occurrence
+    // at that order; stop at the first order where any layer has one (the choice below never looks at
+    // lower orders then).  Hash collisions are rejected by comparing the n-gram's tokens.
+    for (int n = nkey; n >= 1; --n) {
+        if (s_run[0][n].y + s_run[1][n].y + s_run[2][n].y > 0u) {  // uniform
+            Key bl[3] = {{0ull, 0ull}, {0ull, 0ull}, {0ull, 0ull}};
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+                const LayerDesc& ly = sd->layer[l];
+                const uint2 run = s_run[l][n];
+                for (int i = tid; i < static_cast<int>(run.y); i += kLookupThreads) {
+                    const unsigned long long oc = __ldg(ly.idx_occ + run.x + i);
+                    const int p = static_cast<int>(oc & 0xFFFFFFFFull), q = static_cast<int>(oc >> 32);
+                    int tk[kMaxOrder];
+#pragma unroll
+                    for (int j = 0; j < kMaxOrder; ++j) tk[j] = j < n ? __ldg(ly.tokens + p - j) : 0;
+                    const int st = __ldg(ly.seq_start + q);
+                    const int len = __ldg(ly.seq_len + q);
+                    const long long stp = __ldg(ly.seq_step + q);
+                    bool match = true;
+#pragma unroll
+                    for (int j = 0; j < kMaxOrder; ++j) match &= j >= n || tk[j] == s_key[j];
+                    const int e = p - st;
+                    const int avail = min(len - e - 1, d);
+                    if (!match || avail <= 0) continue;
+                    Key k;
+                    k.hi = static_cast<unsigned long long>(stp) ^ 0x8000000000000000ull;
+                    k.lo = (static_cast<unsigned long long>(avail) << 48) |
+                           (static_cast<unsigned long long>(q) << 24) | static_cast<unsigned long long>(e);
+                    if (key_gt(k, bl[l])) bl[l] = k;
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+                const Key k = key_shfl_max(bl[l]);
+                if (lane == 0) s_red3[l][warp] = k;
+            }
             __syncthreads();
-            if (warp == 0) {
-                Key r = lane < kWarps ? s_red[lane] : Key{0ull, 0ull};
+            if (warp < 3) {
+                Key r = lane < kWarps ? s_red3[warp][lane] : Key{0ull, 0ull};
                 r = key_shfl_max(r);
-                if (lane == 0) s_best[l][n] = r;
+                if (lane == 0 && key_gt(r, s_best[warp][n])) s_best[warp][n] = r;
             }
             __syncthreads();
         }
+        bool hit = false;
+        for (int l = 0; l < 3; ++l)
+            if ((l != 2 || sd->rejected_enabled) && s_best[l][n].lo != 0ull) hit = true;
+        if (hit) break;
     }
 
     // ---- choose: order desc, then prior > dynamic > rejected (datastore.cpp:88-107)
@@ -253,7 +362,120 @@ __global__ void set_store_kernel(StoreDesc* sd, int max_order, int rej) {
     sd->rejected_enabled = rej;
 }
 
+// n-gram index build: one (key, position) entry per (position p, order n) whose n-gram lies inside p's
+// sequence and whose sequence continues after p (an occurrence with nothing after it is never
+// returned: avail = min(remaining, d) <= 0, datastore.cpp:57-58); others get kNoKey (sorted last)
+__global__ void index_entries_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ seq_of,
+                                     const int32_t* __restrict__ seq_start, const int32_t* __restrict__ seq_len,
+                                     int nt, int N, unsigned long long* keys, unsigned long long* vals) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nt; p += gridDim.x * blockDim.x) {
+        const int q = seq_of[p];
+        const int e = p - seq_start[q];
+        const bool cont = seq_len[q] - e - 1 >= 1;
+        unsigned long long h = kHashSeed;
+        for (int n = 1; n <= N; ++n) {
+            const bool ok = cont && e >= n - 1;
+            if (ok) h = ngram_step(h, tokens[p - n + 1]);
+            keys[static_cast<long long>(p) * N + n - 1] = ok ? ngram_key(h, n) : kNoKey;
+            vals[static_cast<long long>(p) * N + n - 1] =
+                (static_cast<unsigned long long>(q) << 32) | static_cast<uint32_t>(p);
+        }
+    }
+}
+// run r of the sorted entries -> its table slot (linear probing; keys are unique)
+__global__ void index_table_kernel(const unsigned long long* __restrict__ ukeys, const uint32_t* __restrict__ start,
+                                   const uint32_t* __restrict__ count, const int* __restrict__ n_runs,
+                                   IdxSlot* table, uint32_t mask) {
+    const int R = *n_runs;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+        const unsigned long long k = ukeys[r];
+        if (k == kNoKey) continue;  // the run of invalid entries
+        unsigned slot = static_cast<unsigned>(k) & mask;
+        while (atomicCAS(&table[slot].key, 0ull, k) != 0ull) slot = (slot + 1) & mask;
+        table[slot].start = start[r];
+        table[slot].count = count[r];
+    }
+}
+
 }  // namespace
+
+LayerDesc DeviceStore::desc_of(const HostLayer& h) const {
+    LayerDesc v{};
+    v.tokens = h.tokens.p;
+    v.seq_of = h.seq_of.p;
+    v.seq_start = h.seq_start.p;
+    v.seq_len = h.seq_len.p;
+    v.seq_step = h.seq_step.p;
+    v.n_tokens = h.n_tokens;
+    v.n_seqs = h.n_seqs;
+    v.max_order = h.max_order;
+    v.idx_tokens = h.idx_tokens;
+    v.idx_table = h.idx_table.p;
+    v.idx_occ = h.idx_occ.p;
+    v.idx_mask = h.idx_mask;
+    v.idx_order = h.idx_order;
+    return v;
+}
+
+// Index the layer's current tokens (all orders 1..max_order): entries -> radix sort by key -> run-length
+// encode -> exclusive scan (run starts) -> open-addressing table of >= 2x the distinct n-grams.  The
+// layer's tokens / seq_of / seq_start / seq_len must be complete on stream s.
+void DeviceStore::build_index(int l, cudaStream_t s) {
+    if (l < 0 || l > 2) throw_invalid("bad datastore layer");
+    DeviceGuard g(device_);
+    HostLayer& h = layers_[l];
+    h.idx_tokens = 0;
+    const int nt = h.n_tokens, N = h.max_order;
+    if (nt <= 0) {
+        LayerDesc v = desc_of(h);
+        set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 1);
+        CUDA_LAUNCH_CHECK();
+        return;
+    }
+    const long long E = static_cast<long long>(nt) * N;
+    if (E >= (1LL << 31)) throw_runtime("datastore index exceeds 2^31 entries");
+    const int En = static_cast<int>(E);
+    DevBuf<unsigned long long> k_in(En), k_out(En), ukeys(En), v_in(En);
+    h.idx_occ.alloc(En);
+    DevBuf<uint32_t> cnt(En), st(En);
+    DevBuf<int> n_runs(1);
+    index_entries_kernel<<<std::min((nt + 255) / 256, 4096), 256, 0, s>>>(h.tokens.p, h.seq_of.p, h.seq_start.p,
+                                                                            h.seq_len.p, nt, N, k_in.p, v_in.p);
+    CUDA_LAUNCH_CHECK();
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, b1, k_in.p, k_out.p, v_in.p, h.idx_occ.p, En, 0, 64, s));
+    CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, b2, k_out.p, ukeys.p, cnt.p, n_runs.p, En, s));
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, b3, cnt.p, st.p, En, s));
+    DevBuf<uint8_t> tmp(std::max({b1, b2, b3, size_t(1)}));
+    size_t tb = tmp.n;
+    CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k_in.p, k_out.p, v_in.p, h.idx_occ.p, En, 0, 64, s));
+    tb = tmp.n;
+    CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(tmp.p, tb, k_out.p, ukeys.p, cnt.p, n_runs.p, En, s));
+    int R = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&R, n_runs.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    tb = tmp.n;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, st.p, R, s));
+    uint32_t cap = 1024;
+    while (cap < 2u * static_cast<uint32_t>(R)) cap <<= 1;
+    h.idx_table.alloc(cap);
+    h.idx_table.zero(s);
+    index_table_kernel<<<std::min((R + 255) / 256 + 1, 4096), 256, 0, s>>>(ukeys.p, st.p, cnt.p, n_runs.p,
+                                                                           h.idx_table.p, cap - 1);
+    CUDA_LAUNCH_CHECK();
+    h.idx_mask = cap - 1;
+    h.idx_order = N;
+    h.idx_tokens = nt;
+    LayerDesc v = desc_of(h);
+    set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 1);
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaStreamSynchronize(s));  // the temporaries above are freed on return
+}
+
+int64_t DeviceStore::index_entries(int l) const {
+    if (l < 0 || l > 2) throw_invalid("bad datastore layer");
+    return layers_[l].idx_tokens > 0 ? static_cast<int64_t>(layers_[l].idx_occ.n) : 0;
+}
 
 DeviceStore::DeviceStore(int max_order, int depth, int device)
     : device_(device), max_order_(max_order), depth_(depth) {
@@ -334,8 +556,7 @@ void DeviceStore::grow(int l, int need_tok, int need_seq, cudaStream_t s) {
         changed = true;
     }
     if (changed) {
-        LayerDesc v{h.tokens.p, h.seq_of.p, h.seq_start.p, h.seq_len.p, h.seq_step.p,
-                    h.n_tokens, h.n_seqs, h.max_order, 0};
+        LayerDesc v = desc_of(h);
         set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 1);
         CUDA_LAUNCH_CHECK();
     }
@@ -354,8 +575,8 @@ void DeviceStore::set_layer_order(int l, int order, cudaStream_t s) {
     DeviceGuard g(device_);
     HostLayer& h = layers_[l];
     h.max_order = order;
-    LayerDesc v{h.tokens.p, h.seq_of.p, h.seq_start.p, h.seq_len.p, h.seq_step.p,
-                h.n_tokens, h.n_seqs, h.max_order, 0};
+    if (order > h.idx_order) h.idx_tokens = 0;  // orders above the index's: scan the whole layer
+    LayerDesc v = desc_of(h);
     set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 1);
     CUDA_LAUNCH_CHECK();
 }
@@ -394,8 +615,9 @@ void DeviceStore::clear_layer(int l, cudaStream_t s) {
     DeviceGuard g(device_);
     HostLayer& h = layers_[l];
     h.n_tokens = h.n_seqs = 0;
+    h.idx_tokens = 0;  // the index buffers are kept for reuse
     h.lens.clear();
-    LayerDesc v{h.tokens.p, h.seq_of.p, h.seq_start.p, h.seq_len.p, h.seq_step.p, 0, 0, h.max_order, 0};
+    LayerDesc v = desc_of(h);
     set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 0);
     CUDA_LAUNCH_CHECK();
 }
@@ -424,11 +646,12 @@ std::unique_ptr<DeviceStore> DeviceStore::clone() const {
         d.n_tokens = h.n_tokens;
         d.n_seqs = h.n_seqs;
         d.lens = h.lens;
-        LayerDesc v{d.tokens.p, d.seq_of.p, d.seq_start.p, d.seq_len.p, d.seq_step.p, d.n_tokens, d.n_seqs,
-                    d.max_order, 0};
+        LayerDesc v = desc_of(d);
         set_layer_kernel<<<1, 1>>>(c->desc_dev_, l, v, 0);
         CUDA_LAUNCH_CHECK();
     }
+    for (int l = 0; l < 3; ++l)
+        if (layers_[l].idx_tokens > 0) c->build_index(l, 0);  // covers at least what the source's index does
     set_store_kernel<<<1, 1>>>(c->desc_dev_, max_order_, rejected_enabled_ ? 1 : 0);
     CUDA_LAUNCH_CHECK();
     set_stats_kernel<<<1, 32>>>(c->desc_dev_, desc_dev_);
@@ -471,10 +694,10 @@ void DeviceStore::load_layer(int l, int max_order, const int64_t* off, const int
     }
     h.n_tokens = static_cast<int32_t>(nt);
     h.n_seqs = n_seqs;
-    LayerDesc v{h.tokens.p, h.seq_of.p, h.seq_start.p, h.seq_len.p, h.seq_step.p, h.n_tokens, h.n_seqs, h.max_order, 0};
+    LayerDesc v = desc_of(h);
     set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 0);
     CUDA_LAUNCH_CHECK();
-    CUDA_CHECK(cudaStreamSynchronize(s));  // the host vectors above are pageable sources
+    build_index(l, s);  // synchronises s (the host vectors above are pageable sources)
 }
 
 void DeviceStore::lookup_lane(int32_t* buf, LaneState* lane, int d, cudaStream_t s) const {
@@ -507,6 +730,39 @@ void DeviceStore::lookup_batch(int n_q, const int64_t* offsets, const int32_t* t
     CUDA_CHECK(cudaMemcpyAsync(out_src, dsrc.p, n_q * 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaMemcpyAsync(out_order, dord.p, n_q * 4, cudaMemcpyDeviceToHost, s));
     CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+double DeviceStore::profile_lookup(const int32_t* ctx, int L, int d, int iters) {
+    DeviceGuard g(device_);
+    if (d > 65535) throw_invalid("lookup depth must be <= 65535");
+    const int dcap = std::max(d, 1);
+    DevBuf<int64_t> doff(2);
+    DevBuf<int32_t> dtok(L), ddep(1), dc(dcap), dn(1), dsrc(1), dord(1);
+    const int64_t off[2] = {0, L};
+    CUDA_CHECK(cudaMemcpy(doff.p, off, 16, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(dtok.p, ctx, static_cast<size_t>(L) * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(ddep.p, &d, 4, cudaMemcpyHostToDevice));
+    cudaStream_t s;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    CUDA_CHECK(cudaEventCreate(&e0));
+    CUDA_CHECK(cudaEventCreate(&e1));
+    auto launch = [&] {
+        lookup_batch_kernel<<<1, kLookupThreads, 0, s>>>(desc_dev_, doff.p, dtok.p, ddep.p, dcap, dc.p, dn.p, dsrc.p, dord.p);
+    };
+    for (int i = 0; i < 3; ++i) launch();
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i) launch();
+    CUDA_LAUNCH_CHECK();
+    CUDA_CHECK(cudaEventRecord(e1, s));
+    CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    return 1e3 * static_cast<double>(ms) / iters;
 }
 
 void DeviceStore::stats(int64_t out[6], cudaStream_t s) const {

@@ -84,6 +84,16 @@ class _Layer:
     def clear(self):
         check(lib().dbl_store_clear_layer(self._s._h, self._l))
 
+    def build_index(self):
+        """Device n-gram index over the layer's current sequences (lookups unchanged, scans avoided)."""
+        check(lib().dbl_store_build_index(self._s._h, self._l))
+
+    @property
+    def index_entries(self) -> int:
+        v = C.c_int64()
+        check(lib().dbl_store_index_entries(self._s._h, self._l, C.byref(v)))
+        return v.value
+
     def _info(self):
         n_s, n_t, occ = C.c_int64(), C.c_int64(), C.c_int64()
         check(lib().dbl_store_layer_info(self._s._h, self._l, C.byref(n_s), C.byref(n_t),
@@ -234,6 +244,13 @@ class HierarchicalDatastore:
 
     def flush_session(self):  # datastore.cpp:144-147
         check(lib().dbl_store_flush_session(self._h))
+
+    def profile_lookup(self, context, d: int, iters: int = 100) -> float:
+        """Device microseconds per lookup (back-to-back single-CTA lookups, CUDA events)."""
+        ctx = _i32(context)
+        v = C.c_double()
+        check(lib().dbl_store_profile_lookup(self._h, _p32(ctx), len(ctx), int(d), int(iters), C.byref(v)))
+        return v.value
 
     @property
     def stats(self) -> LookupStats:
