@@ -132,43 +132,88 @@ struct Timer {
     }
 };
 
+// The round's streams.  Target side (verify forward, finish_round's datastore appends, the target
+// lane): `main` + `target` on the target's device.  Draft side: `draft` (+ `dmain` for its lane and
+// datastore-mirror updates) on the draft's device — the same device (dmain aliases main) or its own
+// GPU (PSD draft-while-verify across devices: the host joins both sides at the round boundary).
 struct Streams {
-    cudaStream_t main = nullptr, draft = nullptr, target = nullptr;
+    cudaStream_t main = nullptr, draft = nullptr, target = nullptr, dmain = nullptr;
     cudaEvent_t ready = nullptr, tf0 = nullptr, tf1 = nullptr;
-    Streams() {
+    cudaEvent_t dready = nullptr;  // on the draft's device (events record only on their own device)
+    int tdev = 0, ddev = 0;
+    Streams() : Streams(current_device(), current_device()) {}
+    Streams(int target_dev, int draft_dev) : tdev(target_dev), ddev(draft_dev) {
         // The target's verify forward is the round's critical path: its stream gets the highest
         // priority so a co-located draft chain fills SM gaps instead of delaying target CTAs.
         int lo = 0, hi = 0;
-        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        CUDA_CHECK(cudaStreamCreateWithPriority(&main, cudaStreamNonBlocking, hi));
+        {
+            DeviceGuard g(tdev);
+            CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&main, cudaStreamNonBlocking, hi));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&target, cudaStreamNonBlocking, hi));
+            own_target = target;
+            CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            CUDA_CHECK(cudaEventCreate(&tf0));
+            CUDA_CHECK(cudaEventCreate(&tf1));
+            // The API's store / model calls run on the legacy stream and are asynchronous; these streams
+            // are non-blocking, so order the loop after everything already enqueued there (e.g. the
+            // prior's inserts of build_prior) explicitly.
+            CUDA_CHECK(cudaEventRecord(ready, 0));
+            CUDA_CHECK(cudaStreamWaitEvent(main, ready, 0));
+        }
+        DeviceGuard g(ddev);
         CUDA_CHECK(cudaStreamCreateWithPriority(&draft, cudaStreamNonBlocking, lo));
-        CUDA_CHECK(cudaStreamCreateWithPriority(&target, cudaStreamNonBlocking, hi));
-        own_target = target;
-        CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        CUDA_CHECK(cudaEventCreate(&tf0));
-        CUDA_CHECK(cudaEventCreate(&tf1));
-        // The API's store / model calls run on the legacy stream and are asynchronous; these streams
-        // are non-blocking, so order the loop after everything already enqueued there (e.g. the prior's
-        // inserts of build_prior) explicitly.
-        CUDA_CHECK(cudaEventRecord(ready, 0));
-        CUDA_CHECK(cudaStreamWaitEvent(main, ready, 0));
+        CUDA_CHECK(cudaEventCreateWithFlags(&dready, cudaEventDisableTiming));
+        if (ddev != tdev) {
+            CUDA_CHECK(cudaStreamCreateWithPriority(&dmain, cudaStreamNonBlocking, hi));
+            CUDA_CHECK(cudaEventRecord(dready, 0));
+            CUDA_CHECK(cudaStreamWaitEvent(dmain, dready, 0));
+        } else {
+            dmain = main;
+        }
     }
-    cudaStream_t own_target = nullptr;  // target may alias draft (see run_double)
+    cudaStream_t own_target = nullptr;  // target may alias draft (see DoubleEngine)
     ~Streams() {
         cudaStreamSynchronize(main);
         cudaStreamSynchronize(draft);
         cudaStreamSynchronize(own_target);
+        if (dmain != main) cudaStreamSynchronize(dmain);
         cudaStreamDestroy(main);
         cudaStreamDestroy(draft);
         cudaStreamDestroy(own_target);
+        if (dmain != main) cudaStreamDestroy(dmain);
         cudaEventDestroy(ready);
+        cudaEventDestroy(dready);
         cudaEventDestroy(tf0);
         cudaEventDestroy(tf1);
     }
-    void fork() {  // lanes start after everything enqueued on main
+    static int current_device() {
+        int d = 0;
+        CUDA_CHECK(cudaGetDevice(&d));
+        return d;
+    }
+    void fork() {  // each side starts after everything enqueued on its own main stream
         CUDA_CHECK(cudaEventRecord(ready, main));
-        CUDA_CHECK(cudaStreamWaitEvent(draft, ready, 0));
         CUDA_CHECK(cudaStreamWaitEvent(target, ready, 0));
+        if (dmain == main) {
+            CUDA_CHECK(cudaStreamWaitEvent(draft, ready, 0));
+        } else {
+            DeviceGuard g(ddev);
+            CUDA_CHECK(cudaEventRecord(dready, dmain));
+            CUDA_CHECK(cudaStreamWaitEvent(draft, dready, 0));
+        }
+    }
+    void join_draft_into_main() {  // main (target device) waits for the draft stream's work
+        if (dmain == main) {
+            CUDA_CHECK(cudaEventRecord(ready, draft));
+            CUDA_CHECK(cudaStreamWaitEvent(main, ready, 0));
+        } else {
+            {
+                DeviceGuard g(ddev);
+                CUDA_CHECK(cudaEventRecord(dready, draft));
+            }
+            CUDA_CHECK(cudaStreamWaitEvent(main, dready, 0));
+        }
     }
 };
 
@@ -345,6 +390,12 @@ namespace {
 // its datastore and its round record.
 struct DoubleSeq {
     DeviceStore* st = nullptr;
+    // the draft side's datastore: `st` itself, or (draft on another GPU) a replica on the draft's
+    // device that receives the same appends in the same order (SURVEY §8(b) threading: "inserts are
+    // applied at the boundary in identical order on every device mirror")
+    DeviceStore* dst = nullptr;
+    std::unique_ptr<DeviceStore> mirror;
+    int64_t mirror_base[6] = {};
     std::unique_ptr<Lane> dl, tl;
     std::unique_ptr<LaneIO> dio, tio;
     PinBuf<RoundResult> rr_buf;
@@ -373,16 +424,56 @@ struct DoubleEngine {
     double tfwd_ms = 0.0;
     int64_t tfwd_n = 0;
 
-    DoubleEngine(Model& d, Model& t) : dm(d), tm(t) {
+    DoubleEngine(Model& d, Model& t) : dm(d), tm(t), S(t.device(), d.device()) {
         // draft and target run concurrently unless that would put more than two persistent forwards on
-        // this GPU (tensor-parallel shards sharing it): then both workers share one stream — the round's
-        // results are identical either way (frozen snapshot, pipeline.cpp:239-261)
-        if (dm.persistent_grids() + tm.persistent_grids() > 2) S.target = S.draft;
+        // the draft's GPU (tensor-parallel shards sharing it): then both workers share one stream — the
+        // round's results are identical either way (frozen snapshot, pipeline.cpp:239-261)
+        if (dm.device() == tm.device() && dm.persistent_grids() + tm.persistent_grids_on(dm.device()) > 2)
+            S.target = S.draft;
+        if (dm.device() != tm.device() && tm.persistent_grids_on(dm.device()) > 1)
+            throw_invalid("draft GPU hosts more than one target shard (at most two persistent forwards per GPU)");
+    }
+    bool split() const { return S.dmain != S.main; }
+    // the draft side's datastore for sequence q (see DoubleSeq::dst); DBL_STORE_MIRROR=1 forces a replica
+    // on the same device (tests the replication path on one GPU)
+    void bind_store(DoubleSeq& q, DeviceStore* st) const {
+        q.st = st;
+        q.mirror.reset();
+        q.dst = st;
+        const char* fe = std::getenv("DBL_STORE_MIRROR");
+        const bool force = fe && fe[0] == '1';
+        if (split() || force) {
+            CUDA_CHECK(cudaStreamSynchronize(S.main));
+            q.mirror = st->clone_to(dm.device());
+            q.dst = q.mirror.get();
+            q.dst->stats(q.mirror_base, S.dmain);
+        }
+    }
+    // finish_round's datastore appends, applied to both replicas in the same order
+    void record(DoubleSeq& q, int layer, const std::vector<int32_t>& before, const int32_t* add, size_t na) const {
+        record_run(*q.st, layer, before, add, na, S.main);
+        if (q.dst != q.st) {
+            DeviceGuard g(q.dst->device());
+            record_run(*q.dst, layer, before, add, na, S.dmain);
+        }
+    }
+    // the replica's lookups count in the datastore's stats (LookupStats, datastore.hpp:39-67)
+    void unbind_store(DoubleSeq& q) const {
+        if (!q.mirror) return;
+        int64_t now[6], delta[6];
+        q.mirror->stats(now, S.dmain);
+        for (int i = 0; i < 6; ++i) delta[i] = now[i] - q.mirror_base[i];
+        q.st->add_stats(delta, S.main);
+        q.mirror.reset();
+        q.dst = q.st;
     }
 
     // lanes (capacity `cap` tokens), round record and sampled-loop buffers of one sequence
     void init_seq(DoubleSeq& q, DeviceStore* st, int cap, const dbl_pipeline_options& o) const {
         q.st = st;
+        q.dst = st;
+        if (o.temperature != 0.0 && dm.device() != tm.device())
+            throw_invalid("sampled decoding (temperature > 0) needs the draft and target on one device");
         q.dl = std::make_unique<Lane>(dm, cap);
         q.tl = std::make_unique<Lane>(tm, cap);
         q.dio = std::make_unique<LaneIO>(q.dl.get());
@@ -449,13 +540,14 @@ struct DoubleEngine {
         // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
         std::vector<Lane*> dls, tls;
         std::vector<int> bounds;
+        DeviceGuard gd(dm.device());
         for (int j = 0; j < gamma; ++j) {
             dls.clear();
             bounds.clear();
             for (DoubleSeq* qp : act) {
                 DoubleSeq& q = *qp;
                 const int first = j == 0 ? split_long_forward(*q.dl, q.L, q.L - 1, c_max, q.smp != nullptr, S.draft) : 0;
-                if (o.draft_retrieval) q.st->lookup_lane(q.dl->buf.p, q.dl->state, d, S.draft);
+                if (o.draft_retrieval) q.dst->lookup_lane(q.dl->buf.p, q.dl->state, d, S.draft);
                 dls.push_back(q.dl.get());
                 bounds.push_back(j == 0 ? q.L + c_max - first : 1 + c_max);
             }
@@ -479,6 +571,7 @@ struct DoubleEngine {
             }
         }
         // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
+        DeviceGuard gt(tm.device());
         bounds.clear();
         for (DoubleSeq* qp : act) {
             DoubleSeq& q = *qp;
@@ -525,7 +618,6 @@ struct DoubleEngine {
     void finish(DoubleSeq& q, const dbl_pipeline_options& o) {
         const int gamma = o.gamma;
         RoundResult* rr = q.rr;
-        DeviceStore& st = *q.st;
         Lane& dl = *q.dl;
         Lane& tl = *q.tl;
         Sampled* smp = q.smp.get();
@@ -564,10 +656,10 @@ struct DoubleEngine {
             add.push_back(rr->tgt_correction);
             std::vector<int32_t> pre_k = committed_before;
             pre_k.insert(pre_k.end(), spec.begin(), spec.begin() + k);
-            record_run(st, 2, pre_k, spec.data() + k, spec.size() - k, S.main);
+            record(q, 2, pre_k, spec.data() + k, spec.size() - k);
             std::vector<int32_t> pre_d = committed_before;
             pre_d.insert(pre_d.end(), spec.begin(), spec.end());
-            record_run(st, 2, pre_d, chain, n_chain, S.main);
+            record(q, 2, pre_d, chain, n_chain);
         } else {
             tr.accepted_pending = ns;
             add = spec;
@@ -590,11 +682,11 @@ struct DoubleEngine {
                 std::vector<int32_t> pre_j = committed_before;
                 pre_j.insert(pre_j.end(), spec.begin(), spec.end());
                 pre_j.insert(pre_j.end(), chain, chain + j);
-                record_run(st, 2, pre_j, chain + j, n_chain - j, S.main);
+                record(q, 2, pre_j, chain + j, n_chain - j);
             }
         }
         tr.committed_count = static_cast<int>(add.size());
-        record_run(st, 1, committed_before, add.data(), add.size(), S.main);
+        record(q, 1, committed_before, add.data(), add.size());
         q.committed.insert(q.committed.end(), add.begin(), add.end());
         // rollback(state, |committed|) (pipeline.cpp:15-30)
         if (static_cast<long>(q.committed.size()) < q.last_committed_len)
@@ -643,8 +735,11 @@ struct DoubleEngine {
         const int n = static_cast<int>(X.size()), nc = static_cast<int>(q.committed.size());
         Lane& dl = *q.dl;
         Lane& tl = *q.tl;
-        dl.kv_len = std::min(dl.kv_len, q.dio->sync_tokens(X, S.main));
-        dl.set_state(n, 0, dl.kv_len, n - 1, S.main);
+        {
+            DeviceGuard g(dm.device());
+            dl.kv_len = std::min(dl.kv_len, q.dio->sync_tokens(X, S.dmain));
+            dl.set_state(n, 0, dl.kv_len, n - 1, S.dmain);
+        }
         tl.kv_len = std::min(tl.kv_len, q.tio->sync_tokens(X, S.main));
         tl.set_state(n, 0, tl.kv_len, nc - 1, S.main);
     }
@@ -667,8 +762,7 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
         if (p.empty()) throw_invalid("prompt must be nonempty");
     validate_opts(o);
     for (DeviceStore* st : stores)
-        if (dm.device() != st->device() || tm.device() != st->device())
-            throw_invalid("draft, target and datastore must live on the same device");
+        if (tm.device() != st->device()) throw_invalid("the datastore must live on the target's device");
     for (int i = 0; i < B; ++i)
         for (int k = i + 1; k < B; ++k)
             if (stores[i] == stores[k]) throw_invalid("batched run: every sequence needs its own datastore");
@@ -684,6 +778,7 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     for (int b = 0; b < B; ++b) {
         DoubleSeq& q = seqs[b];
         E.init_seq(q, stores[b], cap, o);
+        E.bind_store(q, stores[b]);
         device_counts(*q.st, S.main, &q.base_lookups, &q.base_hits);
         q.n_prompt = static_cast<int>(prompts[b].size());
         q.committed = prompts[b];
@@ -691,24 +786,34 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
         q.last_committed_len = q.n_prompt;
         q.scanned = q.n_prompt;
         q.st->record(1, prompts[b].data(), q.n_prompt, S.main);  // store.record_accepted(prompt), pipeline.cpp:282
+        if (q.dst != q.st) q.dst->record(1, prompts[b].data(), q.n_prompt, S.dmain);
         // lanes hold the prompt; transformers prefill KV for positions [0, P-1)
-        q.dio->sync_tokens(q.committed, S.main);
+        {
+            DeviceGuard gd(dm.device());
+            q.dio->sync_tokens(q.committed, S.dmain);
+        }
         q.tio->sync_tokens(q.committed, S.main);
     }
     Timer pre;
     CUDA_CHECK(cudaEventRecord(pre.a, S.main));
     S.fork();
     for (DoubleSeq& q : seqs) {
-        catch_up(*q.dl, q.n_prompt - 1, S.draft);
+        {
+            DeviceGuard gd(dm.device());
+            catch_up(*q.dl, q.n_prompt - 1, S.draft);
+        }
         catch_up(*q.tl, q.n_prompt - 1, S.target);
     }
-    CUDA_CHECK(cudaEventRecord(S.ready, S.draft));
-    CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
+    S.join_draft_into_main();
+    if (E.split()) CUDA_CHECK(cudaStreamWaitEvent(S.dmain, S.dready, 0));  // the draft lane's cursor after its prefill
     CUDA_CHECK(cudaEventRecord(S.ready, S.target));
     CUDA_CHECK(cudaStreamWaitEvent(S.main, S.ready, 0));
     CUDA_CHECK(cudaEventRecord(pre.b, S.main));
     for (DoubleSeq& q : seqs) {
-        q.dl->set_state(q.n_prompt, 0, q.dl->kv_len, q.n_prompt - 1, S.main);
+        {
+            DeviceGuard gd(dm.device());
+            q.dl->set_state(q.n_prompt, 0, q.dl->kv_len, q.n_prompt - 1, S.dmain);
+        }
         q.tl->set_state(q.n_prompt, 0, q.tl->kv_len, q.n_prompt - 1, S.main);
     }
 
@@ -738,9 +843,11 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     }
     CUDA_CHECK(cudaEventRecord(loop.b, S.main));
     CUDA_CHECK(cudaStreamSynchronize(S.main));
+    CUDA_CHECK(cudaStreamSynchronize(S.dmain));
 
     std::vector<RunOutput> out;
     for (DoubleSeq& q : seqs) {
+        E.unbind_store(q);
         RunOutput& res = q.res;
         finish_output(q.committed, q.n_prompt, max_new, res);
         compute_metrics(res.traces, o.t_target, &res.metrics);
@@ -807,7 +914,8 @@ Trace RoundSession::run_round(HostPipelineState& st, DeviceStore& store, const d
     if (static_cast<long>(st.speculative.size()) != st.n_spec_probs)
         throw_logic("speculative tokens and probs out of sync");
     if (st.committed.empty()) throw_invalid("forward_batch: empty context");  // model.cpp:41
-    if (store.device() != I.E.tm.device()) throw_invalid("draft, target and datastore must live on the same device");
+    if (store.device() != I.E.tm.device() || I.E.dm.device() != I.E.tm.device())
+        throw_invalid("run_round: draft, target and datastore must live on the same device");
     DeviceGuard g(store.device());
     const int n = static_cast<int>(st.committed.size() + st.speculative.size());
     const int need = n + 3 * o.gamma * (o.depth + 1) + 3 * o.depth + 64;
@@ -827,6 +935,7 @@ Trace RoundSession::run_round(HostPipelineState& st, DeviceStore& store, const d
     }
     DoubleSeq& q = *I.q;
     q.st = &store;
+    q.dst = &store;  // one device (checked above): the draft side reads the same datastore
     q.committed = st.committed;
     q.spec = st.speculative;
     q.mode = st.mode;

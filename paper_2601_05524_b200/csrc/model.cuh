@@ -72,6 +72,8 @@ class Model {
     // persistent (all-SM, cooperatively launched) grids one forward places on device(): at most two may
     // co-run on a GPU, so the decoder serializes draft and target work when the sum would exceed it
     virtual int persistent_grids() const { return 0; }
+    // persistent grids one forward places on GPU `dev` (tensor-parallel shards may span several GPUs)
+    virtual int persistent_grids_on(int dev) const { return dev == device() ? persistent_grids() : 0; }
     virtual void set_profiler(GemmProfiler*) {}
     virtual std::string kind() const = 0;
 };

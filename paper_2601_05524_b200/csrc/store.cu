@@ -354,8 +354,10 @@ __global__ void fill_seq_of_kernel(int32_t* seq_of, const int32_t* __restrict__ 
         for (int i = threadIdx.x; i < n; i += blockDim.x) seq_of[a + i] = q;
     }
 }
-__global__ void set_stats_kernel(StoreDesc* sd, const StoreDesc* src) {
-    if (threadIdx.x < 6) sd->stats[threadIdx.x] = src->stats[threadIdx.x];
+__global__ void add_stats_kernel(StoreDesc* sd, long long d0, long long d1, long long d2, long long d3,
+                                 long long d4, long long d5) {
+    const long long d[6] = {d0, d1, d2, d3, d4, d5};
+    if (threadIdx.x < 6) sd->stats[threadIdx.x] += static_cast<unsigned long long>(d[threadIdx.x]);
 }
 __global__ void set_store_kernel(StoreDesc* sd, int max_order, int rej) {
     sd->max_order = max_order;
@@ -562,6 +564,12 @@ void DeviceStore::grow(int l, int need_tok, int need_seq, cudaStream_t s) {
     }
 }
 
+void DeviceStore::add_stats(const int64_t delta[6], cudaStream_t s) {
+    DeviceGuard g(device_);
+    add_stats_kernel<<<1, 32, 0, s>>>(desc_dev_, delta[0], delta[1], delta[2], delta[3], delta[4], delta[5]);
+    CUDA_LAUNCH_CHECK();
+}
+
 void DeviceStore::set_rejected_enabled(bool on, cudaStream_t s) {
     DeviceGuard g(device_);
     rejected_enabled_ = on;
@@ -623,10 +631,13 @@ void DeviceStore::clear_layer(int l, cudaStream_t s) {
 }
 
 // a deep copy (the reference's HierarchicalDatastore is copied by value: test_pipeline.cpp:170-187)
-std::unique_ptr<DeviceStore> DeviceStore::clone() const {
-    auto c = std::make_unique<DeviceStore>(max_order_, depth_, device_);
-    DeviceGuard g(device_);
-    CUDA_CHECK(cudaDeviceSynchronize());  // every enqueued append of this store has landed
+std::unique_ptr<DeviceStore> DeviceStore::clone_to(int device) const {
+    {
+        DeviceGuard g0(device_);
+        CUDA_CHECK(cudaDeviceSynchronize());  // every enqueued append of this store has landed
+    }
+    auto c = std::make_unique<DeviceStore>(max_order_, depth_, device);
+    DeviceGuard g(device);
     c->step_ = step_;
     c->rejected_enabled_ = rejected_enabled_;
     for (int l = 0; l < 3; ++l) {
@@ -654,7 +665,14 @@ std::unique_ptr<DeviceStore> DeviceStore::clone() const {
         if (layers_[l].idx_tokens > 0) c->build_index(l, 0);  // covers at least what the source's index does
     set_store_kernel<<<1, 1>>>(c->desc_dev_, max_order_, rejected_enabled_ ? 1 : 0);
     CUDA_LAUNCH_CHECK();
-    set_stats_kernel<<<1, 32>>>(c->desc_dev_, desc_dev_);
+    {  // stats: through the host (the source may be on another GPU)
+        StoreDesc hs;
+        {
+            DeviceGuard g0(device_);
+            CUDA_CHECK(cudaMemcpy(&hs, desc_dev_, sizeof hs, cudaMemcpyDeviceToHost));
+        }
+        CUDA_CHECK(cudaMemcpy(c->desc_dev_->stats, hs.stats, sizeof hs.stats, cudaMemcpyHostToDevice));
+    }
     CUDA_LAUNCH_CHECK();
     CUDA_CHECK(cudaDeviceSynchronize());
     return c;

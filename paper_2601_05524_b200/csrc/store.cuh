@@ -80,7 +80,9 @@ class DeviceStore {
     // (re)build the n-gram index over the layer's current tokens (load_layer does this for the prior)
     void build_index(int layer, cudaStream_t s);
     int64_t index_entries(int layer) const;
-    std::unique_ptr<DeviceStore> clone() const;
+    std::unique_ptr<DeviceStore> clone() const { return clone_to(device_); }
+    std::unique_ptr<DeviceStore> clone_to(int device) const;  // a replica on another GPU (draft-side lookups)
+    void add_stats(const int64_t delta[6], cudaStream_t s);   // fold a replica's lookup counts in
     void flush_session(cudaStream_t s) { clear_layer(1, s); clear_layer(2, s); }
 
     // one lookup for a lane: ctx = buf[0, lane.L); candidates -> buf[L, L+c), lane.c/src/order

@@ -38,6 +38,11 @@ class TpTransformer final : public Model {
         for (int d : devices_) k += d == devices_[0];
         return k;
     }
+    int persistent_grids_on(int dev) const override {
+        int k = 0;
+        for (int d : devices_) k += d == dev;
+        return k;
+    }
     void set_profiler(GemmProfiler* p) override { shards_[0]->set_profiler(p); }
     int world() const { return static_cast<int>(shards_.size()); }
     Transformer& shard(int r) { return *shards_[static_cast<size_t>(r)]; }
