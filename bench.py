@@ -222,6 +222,16 @@ def all_max(x, world):
     return float(t.item())
 
 
+def all_min(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t.item())
+
+
 def all_sum(x, world):
     if world == 1:
         return x
@@ -306,49 +316,77 @@ def main():
     if os.environ.get("DBL_BENCH_TP_DEVICES") and world == 1 and a.impl == "ours":
         return run_bench(a, 0, 1, 0, wl, max_new, metric, base_cfg,
                          tp_world=len(os.environ["DBL_BENCH_TP_DEVICES"].split(",")))
+    tc = os.environ.get("DBL_TP_CHILD")
+    if tc:  # one tensor-parallel rank (spawned by tp_children below): its own gloo group for the handles
+        import torch.distributed as dist
+        r, n, port = (int(x) for x in tc.split(","))
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=r, world_size=n)
+        return run_bench(a, r, n, r, wl, max_new, metric, base_cfg, tp_world=n, tp_ipc=True)
     if world > 1 and a.tp == "auto":
-        # Target tensor-parallel over the box's N GPUs: rank 0 drives every shard
-        # in-process (peer memory over NVLink, the exchange inside fwd_kernel) with the draft beside
-        # shard 0; the other ranks hold the rendezvous only.  On failure: replicas, reason recorded.
-        # The TP run happens in a child process with a fresh CUDA context: a failure there (even a
-        # device-side trap, which poisons the context) leaves this process able to fall back.
+        # Target tensor-parallel over the box's N GPUs, one process per GPU: every rank
+        # builds its shard on its GPU, the ranks link their exchange buffers over CUDA IPC and run the same
+        # decode loop (the O / down and argmax exchange inside fwd_kernel; the draft beside every shard —
+        # BASELINE config 5's layout).  Each rank's TP run is a child process with a fresh CUDA context:
+        # if any rank's child fails (even a device-side trap, which poisons the context), every rank falls
+        # back to an independent replica (weak scaling) and the reason is recorded.
         barrier(world)
-        if rank == 0:
-            env = dict(os.environ, DBL_BENCH_TP_DEVICES=",".join(str(i) for i in range(world)))
-            for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK",
-                      "TORCHELASTIC_RUN_ID", "MASTER_PORT"):
-                env.pop(k, None)
-            cmd = [sys.executable, os.path.abspath(__file__), "--gpus", "1", "--steps", str(a.steps),
-                   "--warmup", str(a.warmup), "--workload", a.workload, "--gamma", str(a.gamma),
-                   "--max-new", str(a.max_new), "--seed", str(a.seed)]
-            line, err = None, ""
-            try:
-                r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
-                outs = [x for x in r.stdout.splitlines() if x.startswith("{")]
-                if r.returncode == 0 and outs:
-                    line = outs[-1]
-                else:
-                    err = (r.stderr.strip().splitlines() or ["no output"])[-1]
-            except subprocess.TimeoutExpired:
-                err = "timed out"
-            if line:
+        line, err = tp_children(a, rank, world)
+        if line is not None:
+            if rank == 0:
                 print(line, flush=True)
-            else:
-                print(f"tensor-parallel bench failed ({err}); falling back to replicas", file=sys.stderr)
-                base_cfg = dict(base_cfg, tp_error=err[:200])
-                run_bench(a, 0, 1, 0, wl, max_new, metric, base_cfg)
-        barrier(world)
-        return None
+            barrier(world)
+            return None
+        if rank == 0:
+            print(f"tensor-parallel bench failed ({err}); falling back to replicas", file=sys.stderr)
+        base_cfg = dict(base_cfg, tp_error=err[:200])
     return run_bench(a, rank, world, local, wl, max_new, metric, base_cfg)
 
 
-def _models(dbl, wl, seed, local, tp_world):
-    """(target, draft, parallelism note) for a workload; TP targets over DBL_BENCH_TP_DEVICES."""
+def tp_children(a, rank, world, cmd=None, timeout=1500):
+    """Run this rank's tensor-parallel child (bench.py with DBL_TP_CHILD=rank,world,port) and agree
+    across ranks: returns (rank 0's JSON line — "" on other ranks — or None if any rank failed, the
+    first error)."""
+    import torch.distributed as dist
+    port = int(os.environ.get("MASTER_PORT", "29500")) + 101
+    env = dict(os.environ, DBL_TP_CHILD=f"{rank},{world},{port}")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "GROUP_RANK", "ROLE_RANK",
+              "TORCHELASTIC_RUN_ID", "MASTER_PORT"):
+        env.pop(k, None)
+    if cmd is None:
+        cmd = [sys.executable, os.path.abspath(__file__), "--gpus", "1", "--steps", str(a.steps),
+               "--warmup", str(a.warmup), "--workload", a.workload, "--gamma", str(a.gamma),
+               "--max-new", str(a.max_new), "--seed", str(a.seed), "--no-side"]
+    line, err = None, ""
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+        outs = [x for x in r.stdout.splitlines() if x.startswith("{")]
+        if r.returncode == 0 and (outs or rank != 0):
+            line = outs[-1] if rank == 0 else ""
+        else:
+            err = f"rank {rank}: " + ((r.stderr.strip().splitlines() or ["no output"])[-1])
+    except subprocess.TimeoutExpired:
+        err = f"rank {rank}: timed out"
+    ok = all_min(0.0 if line is None else 1.0, world) > 0.5
+    errs = [None] * world
+    dist.all_gather_object(errs, err)
+    first = next((e for e in errs if e), "")
+    return (line if ok else None), first
+
+
+def _models(dbl, wl, seed, local, tp_world, tp_ipc=False, rank=0):
+    """(target, draft, parallelism note) for a workload: a TP target is this rank's shard linked with
+    the other processes' (tp_ipc), or all shards in-process over DBL_BENCH_TP_DEVICES."""
     tname, tkw = wl["target"]
     dname, dkw = wl["draft"]
     dseed = seed if wl.get("same_seed") else seed + 1
     note = None
-    if tp_world > 1:
+    if tp_ipc:
+        tgt = dbl.Transformer(dbl.transformer_config(tname, seed=seed, max_seq=4096, tp_rank=rank, tp_size=tp_world,
+                                                     **tkw), device=local)
+        dbl.link_tp_processes(tgt)
+        note = (f"target TP={tp_world}, one process per GPU (CUDA IPC; the O / down and argmax exchange inside "
+                "fwd_kernel), the draft beside every shard")
+    elif tp_world > 1:
         # DBL_BENCH_TP_DEVICES="0,0": a TP layout on fewer GPUs (functional checks on one GPU)
         env_dev = os.environ.get("DBL_BENCH_TP_DEVICES")
         devices = [int(x) for x in env_dev.split(",")] if env_dev else list(range(tp_world))
@@ -361,14 +399,18 @@ def _models(dbl, wl, seed, local, tp_world):
     return tgt, drf, note
 
 
-def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headline=True):
+def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headline=True, tp_ipc=False):
     """One workload: DOUBLE at the headline gamma (device + e2e timing), target-only AR (the speedup
-    denominator, same kernels), gamma = ceil(C) / 4 / 8, and the verify forward's roofline."""
+    denominator, same kernels), gamma = ceil(C) / 4 / 8, and the verify forward's roofline.  Ranks are
+    independent replicas (tokens summed) unless they are the tensor-parallel ranks of one request."""
     import ctypes as C
     import torch
     import paper_2601_05524_b200 as dbl
     from paper_2601_05524_b200 import _capi
-    tgt, drf, note = _models(dbl, wl, a.seed, local, tp_world)
+    tgt, drf, note = _models(dbl, wl, a.seed, local, tp_world, tp_ipc=tp_ipc, rank=rank)
+
+    def tok_sum(x):
+        return x if tp_ipc else all_sum(x, world)
     V = tgt.cfg.vocab
     prompt, prior = workload(V, wl["prompt_len"], a.seed + 100)
 
@@ -427,7 +469,7 @@ def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headl
         ar = dbl.run_vanilla_ar(tgt, prompt, max_new, want_jsonl=False)
         ar_ms += ar.metrics["device_ms"]
         ar_tok += len(ar.output)
-    ar_value = all_sum(ar_tok, world) / (all_max(ar_ms, world) / 1e3)
+    ar_value = tok_sum(ar_tok) / (all_max(ar_ms, world) / 1e3)
     lossless = all(r.output == ar.output for r in results)
     m0 = results[-1].metrics
 
@@ -441,12 +483,12 @@ def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headl
             gtok += len(rg.output)
             lossless &= rg.output == ar.output
             gm = rg.metrics
-        gv = all_sum(gtok, world) / (all_max(gms, world) / 1e3)
+        gv = tok_sum(gtok) / (all_max(gms, world) / 1e3)
         return {"gamma": g, "value": round(gv, 3), "speedup_vs_ar": round(gv / ar_value, 4),
                 "mean_accepted_len": round(gm["m"], 4),
                 "target_rows_per_forward": round(gm["target_rows"] / max(1, gm["target_fwd_count"]), 2)}
 
-    value = all_sum(tokens, world) / (all_max(dev_ms, world) / 1e3)
+    value = tok_sum(tokens) / (all_max(dev_ms, world) / 1e3)
     main_line = {"gamma": gamma, "value": round(value, 3), "speedup_vs_ar": round(value / ar_value, 4),
                  "mean_accepted_len": round(m0["m"], 4),
                  "target_rows_per_forward": round(m0["target_rows"] / max(1, m0["target_fwd_count"]), 2)}
@@ -469,8 +511,8 @@ def measure(a, rank, world, local, wl, max_new, steps, warmup, tp_world=1, headl
     pdr = profile(drf, ctx, DEPTH + 1, iters=20)
     out = {
         "value": value, "e2e_ms": all_max(e2e_ms, world), "dev_ms": all_max(dev_ms, world),
-        "tokens": all_sum(tokens, world), "ar_value": ar_value, "gamma": gamma, "C": C_ratio, "m0": m0,
-        "lossless": lossless, "gl": gl, "launches": all_sum(launches, world), "clk": clk.summary(),
+        "tokens": tok_sum(tokens), "ar_value": ar_value, "gamma": gamma, "C": C_ratio, "m0": m0,
+        "lossless": lossless, "gl": gl, "launches": tok_sum(launches), "clk": clk.summary(),
         "prompt": prompt, "prior": prior, "log": log, "output": results[-1].output, "V": V, "note": note,
         "roofline": {"bound": "hbm", "kernel": "fwd_kernel (persistent stream forward: tcgen05/TMA GEMMs + "
                               "attention + fused epilogues), one launch per verify forward",
@@ -544,14 +586,15 @@ def side_line(a, local, name):
             "timing": "1 warm-up + 1 timed decode per gamma (side line; the headline uses --steps/--warmup)"}
 
 
-def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
+def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1, tp_ipc=False):
     import paper_2601_05524_b200 as dbl
     from paper_2601_05524_b200 import _capi
     if not _capi.lib().dbl_device_ok():
         raise SystemExit("no usable sm_100 device (libdouble_b200 has no CPU fallback)")
     import torch
     torch.cuda.set_device(local)
-    r = measure(a, rank, world, local, wl, max_new, a.steps, a.warmup, tp_world=tp_world)
+    r = measure(a, rank, world, local, wl, max_new, a.steps, a.warmup, tp_world=tp_world,
+                headline=tp_world <= 1, tp_ipc=tp_ipc)
     if r["note"]:
         base_cfg = dict(base_cfg, parallelism=r["note"], tp=tp_world)
     t_e2e = r["e2e_ms"]
@@ -567,7 +610,7 @@ def run_bench(a, rank, world, local, wl, max_new, metric, base_cfg, tp_world=1):
         "metric": metric, "value": round(value, 3), "unit": "tokens/s", "n_gpus": max(world, tp_world),
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(r["dev_ms"] / a.steps, 3),
         "higher_is_better": True, "scaling": "strong" if tp_world > 1 else "weak", "vs_baseline": None,
-        "dtype": "bf16", "n_gpus_used": tp_world if tp_world > 1 else world,
+        "dtype": "bf16", "n_gpus_used": max(world, tp_world),
         "data": "synthetic (random-init weights, code-like prompt)",
         "config": dict(base_cfg, gamma=r["gamma"], C_measured=round(r["C"], 3)),
         "speedup_vs_ar": round(value / r["ar_value"], 4), "ar_tokens_per_s": round(r["ar_value"], 3),
