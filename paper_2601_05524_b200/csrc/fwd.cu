@@ -19,30 +19,47 @@ using namespace sm100;
 
 constexpr int kBM = 128, kBK = 64;
 constexpr int kABytes = kBM * kBK * 2;  // one 128 x 64 bf16 weight tile
-constexpr unsigned long long kWatchdogNs = 4000000000ull;
 constexpr int kBatch = 2;               // split-K partials: 2 contributors x 16 columns of loads in flight
 
 // ------------------------------------------------------------------ small helpers
-__device__ __noinline__ void watchdog_fire(int* err, int code, int phase) {
-    atomicExch(err, code);
-    printf("dbl fwd_kernel watchdog: CTA %d thread %d stuck (role %d, phase %d)\n", blockIdx.x, threadIdx.x, code,
-           phase);
-    __trap();
+// Watchdog: a wait that makes no progress for a.wd_ns (a missing tensor-parallel peer, a host contract
+// violation) aborts the forward instead of trapping: the first stuck thread writes the forward's tag
+// (epoch-derived, so a later forward ignores it) into a.err, every other wait sees it within 128
+// polls and gives up, the kernel drains its in-flight copies and MMAs and exits, and the argmax rows
+// come back as -1 (a degenerate row: the API raises runtime_error).  The CUDA context stays usable.
+__shared__ int g_wdtag;  // this forward's abort tag (set at kernel start from the lane's epoch)
+__device__ __forceinline__ int wd_tag(const FwdArgs&) { return g_wdtag; }
+__device__ __forceinline__ bool aborted(const FwdArgs& a) {
+    return *reinterpret_cast<volatile int*>(a.err) == wd_tag(a);
+}
+__device__ __noinline__ void watchdog_fire(const FwdArgs& a, int code, int phase) {
+    if (atomicExch(a.err, wd_tag(a)) != wd_tag(a))
+        printf("dbl fwd_kernel watchdog: CTA %d thread %d stuck (role %d, phase %d): forward aborted\n", blockIdx.x,
+               threadIdx.x, code, phase);
 }
 struct Spin {
     unsigned long long t0 = 0;
     unsigned n = 0;
-    __device__ __forceinline__ void tick(int* err, int code, int phase) {
+    // true: give up (this forward was aborted)
+    __device__ __forceinline__ bool tick(const FwdArgs& a, int code, int phase) {
         if ((++n & 127u) == 0) {
+            if (aborted(a)) return true;
             const unsigned long long t = globaltimer();
-            if (!t0) t0 = t;
-            else if (t - t0 > kWatchdogNs) watchdog_fire(err, code, phase);
+            if (!t0) {
+                t0 = t;
+            } else if (t - t0 > a.wd_ns) {
+                watchdog_fire(a, code, phase);
+                return true;
+            }
         }
+        return false;
     }
 };
-__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t par, int* err, int code, int phase) {
+__device__ __forceinline__ bool mbar_wait_wd(uint64_t* bar, uint32_t par, const FwdArgs& a, int code, int phase) {
     Spin s;
-    while (!mbar_try(bar, par)) s.tick(err, code, phase);
+    while (!mbar_try(bar, par))
+        if (s.tick(a, code, phase)) return true;
+    return false;
 }
 
 // A phase's stream-K split: phase-local CTA ci takes units [ci*U/A, (ci+1)*U/A).  Unit counts fit in
@@ -67,13 +84,16 @@ __device__ __forceinline__ int owner_of(int u, int U, int A) { return ((u + 1) *
 
 __device__ __forceinline__ bool dep_ok(const FwdArgs& a, int p, unsigned long long ep) {
     if (p < 0) return true;
+    if (a.dbg == 3 && p == a.n_ph / 2) return false;  // DBL_FWD_DBG=3: a dependency that never resolves (watchdog test)
     if (ld_relaxed_u64(a.done + p) < (ep + 1) * static_cast<unsigned long long>(a.ph[p].count)) return false;
     fence_acq_rel_gpu();
     return true;
 }
-__device__ __forceinline__ void wait_dep(const FwdArgs& a, int p, unsigned long long ep, int code) {
+__device__ __forceinline__ bool wait_dep(const FwdArgs& a, int p, unsigned long long ep, int code) {
     Spin s;
-    while (!dep_ok(a, p, ep)) s.tick(a.err, code, p);  // each probe is an L2 round trip
+    while (!dep_ok(a, p, ep))  // each probe is an L2 round trip
+        if (s.tick(a, code, p)) return true;
+    return false;
 }
 __device__ __forceinline__ void stamp(const FwdArgs& a, int p, int k) {
     if (a.trace) a.trace[(static_cast<long long>(p) * gridDim.x + blockIdx.x) * 16 + k] = globaltimer();
@@ -364,7 +384,7 @@ __device__ __forceinline__ int batch_row(const BatchSmem& B, int t, int* pos) {
 }
 
 struct FwdSmem {
-    uint64_t full[kFwdMaxStages], empty[kFwdMaxStages], tfull[2], tempty[2];
+    uint64_t full[kFwdMaxStages], empty[kFwdMaxStages], tfull[2], tempty[2], drain;
     unsigned long long ep, tp_ep;
     uint32_t tslot;
     int sint[12];
@@ -563,7 +583,8 @@ __device__ __forceinline__ void wait_partials(const TileCtx& x) {
     for (int j = 1 + x.et; j < x.n_contrib; j += 128) {
         const unsigned long long* f = x.a->slot_flag + slot_of(x, j);
         Spin sp;
-        while (ld_relaxed_u64(f) != x.tag) sp.tick(x.a->err, 8, x.p);
+        while (ld_relaxed_u64(f) != x.tag)
+            if (sp.tick(*x.a, 8, x.p)) break;
         fence_acq_rel_gpu();
     }
     named_bar_sync(1, 128);
@@ -632,7 +653,8 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
             st_release_sys_u64(x.peers->xflag[et] + a.tp_rank * nth + m, x.xtag);
             const unsigned long long* f = x.peers->xflag[a.tp_rank] + et * nth + m;
             Spin sp;
-            while (ld_acquire_sys_u64(f) != x.xtag) sp.tick(a.err, 9, x.p);
+            while (ld_acquire_sys_u64(f) != x.xtag)
+                if (sp.tick(a, 9, x.p)) break;
         }
         named_bar_sync(1, 128);
     }
@@ -858,6 +880,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             sint[2] = Lc;
         }
         *sep = *reinterpret_cast<volatile unsigned long long*>(a.epoch);
+        g_wdtag = static_cast<int>(*sep & 0x3fffffffull) + 1;
         sm.tp_ep = a.tp_epoch ? *reinterpret_cast<volatile unsigned long long*>(a.tp_epoch) : *sep;
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
@@ -867,6 +890,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 128);
         }
+        mbar_init(&sm.drain, 1);
         fence_barrier_init();
         if constexpr (kTP) sm.peers = a.peers;
     }
@@ -910,7 +934,25 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             seek(w, a, c, G);
             seek(x, a, c, G);
             Ring wr, xr;
+            auto issue_x = [&]() {  // the activation rows of unit x into stage xr
+                uint8_t* dst = sB + xr.st * bbytes;
+                const CUtensorMap* xm = a.xmaps[x.xmap];
+                if (T <= 16) {
+                    tma_load_2d(dst, &xm[xb_i], &full[xr.st], x.kb * kBK, 0, kEvictLast);
+                } else {
+                    const int q64 = n16 >> 2, rem = n16 & 3;
+                    for (int j = 0; j < q64; ++j)
+                        tma_load_2d(dst + j * 64 * kBK * 2, &xm[4], &full[xr.st], x.kb * kBK, j * 64, kEvictLast);
+                    int row = q64 * 64;
+                    if (rem & 2) {
+                        tma_load_2d(dst + row * kBK * 2, &xm[3], &full[xr.st], x.kb * kBK, row, kEvictLast);
+                        row += 32;
+                    }
+                    if (rem & 1) tma_load_2d(dst + row * kBK * 2, &xm[2], &full[xr.st], x.kb * kBK, row, kEvictLast);
+                }
+            };
             int pending = 0;  // units whose weights are issued but whose activations are not
+            int n_fill = 0;   // stages issued (watchdog abort: the copies to wait for)
             int dep_phase = -1, stamped = -1;
             Spin spin;
             while (w.p < a.n_ph || pending > 0) {
@@ -925,6 +967,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     tma_load_2d(sA + wr.st * kABytes, &a.wmaps[w.wmap], &full[wr.st], 0,
                                 ((w.wrow / kBM + w.m) * w.KB + w.kb) * kBM,
                                 kEvictFirst);
+                    ++n_fill;
                     wr.next(S);
                     ++pending;
                     step(w, a, c, G);
@@ -939,21 +982,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         stamp(a, x.p, 1);
                     }
                     if (ok) {
-                        uint8_t* dst = sB + xr.st * bbytes;
-                        const CUtensorMap* xm = a.xmaps[x.xmap];
-                        if (T <= 16) {
-                            tma_load_2d(dst, &xm[xb_i], &full[xr.st], x.kb * kBK, 0, kEvictLast);
-                        } else {
-                            const int q64 = n16 >> 2, rem = n16 & 3;
-                            for (int j = 0; j < q64; ++j)
-                                tma_load_2d(dst + j * 64 * kBK * 2, &xm[4], &full[xr.st], x.kb * kBK, j * 64, kEvictLast);
-                            int row = q64 * 64;
-                            if (rem & 2) {
-                                tma_load_2d(dst + row * kBK * 2, &xm[3], &full[xr.st], x.kb * kBK, row, kEvictLast);
-                                row += 32;
-                            }
-                            if (rem & 1) tma_load_2d(dst + row * kBK * 2, &xm[2], &full[xr.st], x.kb * kBK, row, kEvictLast);
-                        }
+                        issue_x();
                         xr.next(S);
                         --pending;
                         step(x, a, c, G);
@@ -966,7 +995,19 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     // Nothing issuable: park on the next ring slot (the hardware wakes the thread when it
                     // frees).  While activations wait on a dependency, bound the park so the flag is
                     // polled again within ~0.25 us.
-                    spin.tick(a.err, 1, pending > 0 ? x.p : w.p);
+                    if (spin.tick(a, 1, pending > 0 ? x.p : w.p)) {
+                        // abort: complete every issued stage's transaction (the pending units' activation
+                        // rows, stale) and wait until all issued copies have landed before exiting
+                        for (; pending > 0; --pending) {
+                            issue_x();
+                            xr.next(S);
+                            step(x, a, c, G);
+                        }
+                        for (int i = 0; i < S && i < n_fill; ++i)
+                            while (!mbar_try(&full[i], static_cast<uint32_t>(((n_fill - 1 - i) / S) & 1))) {
+                            }
+                        break;
+                    }
                     if (w.p < a.n_ph) {
                         if (pending > 0) mbar_try_hint(&empty[wr.st], wr.ph ^ 1u, 250);
                         else mbar_try(&empty[wr.st], wr.ph ^ 1u);
@@ -981,14 +1022,18 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             seek(k, a, c, G);
             Ring rr, tr;  // stage ring; TMEM accumulator ring (nacc buffers)
             int mma_stamped = -1;
-            while (k.p < a.n_ph) {
+            bool abort = false;
+            while (k.p < a.n_ph && !abort) {
                 const int p = k.p;
                 const int n = min(k.e - k.u, k.KB - k.kb);  // units of this tile in this CTA's range
-                mbar_wait_wd(&tempty[tr.st], tr.ph ^ 1u, a.err, 2, p);
+                abort = mbar_wait_wd(&tempty[tr.st], tr.ph ^ 1u, a, 2, p);
                 tc_fence_after();
                 const uint32_t d = tmem + static_cast<uint32_t>(tr.st * a.acc_cols);
-                for (int i = 0; i < n; ++i) {
-                    mbar_wait_wd(&full[rr.st], rr.ph, a.err, 3, p);
+                for (int i = 0; i < n && !abort; ++i) {
+                    if (mbar_wait_wd(&full[rr.st], rr.ph, a, 3, p)) {
+                        abort = true;
+                        break;
+                    }
                     tc_fence_after();
                     if (p != mma_stamped) {
                         stamp(a, p, 4);  // first MMA of the phase
@@ -1003,9 +1048,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     rr.next(S);
                     step(k, a, c, G);
                 }
+                if (abort) break;
                 mma_commit(&tfull[tr.st]);
                 tr.next(a.nacc);
                 stamp(a, p, 5);  // last MMA issued (so far) for the phase
+            }
+            if (abort) {  // the issued MMAs retire before the accumulator memory is released
+                mma_commit(&sm.drain);
+                while (!mbar_try(&sm.drain, 0u)) {
+                }
             }
         }
     } else {  // ============================================ epilogue + aux work (128 threads)
@@ -1117,7 +1168,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         presum(tc, 0, !kTP && P.epi == kFeResid ? a.resid + m * kBM + r : nullptr);
                         tc.has_pre = true;
                     }
-                    mbar_wait_wd(&tfull[buf], static_cast<uint32_t>((it / a.nacc) & 1), a.err, 6, p);
+                    mbar_wait_wd(&tfull[buf], static_cast<uint32_t>((it / a.nacc) & 1), a, 6, p);
                     tc_fence_after();
                     if (et == 0) stamp(a, p, 7);  // accumulator of this CTA's latest tile ready
                     if (!finisher) {  // partial -> slot, then release the slot flag
@@ -1178,9 +1229,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         if constexpr (kB) {
                             int pos;
                             const int b = batch_row(sm.bt, t, &pos);
-                            a.batch.argmax[b][pos] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                            a.batch.argmax[b][pos] = (bi == 0x7fffffff || bv != bv || aborted(a)) ? -1 : bi;
                         } else if constexpr (!kTP) {
-                            a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                            a.argmax[start + t] = (bi == 0x7fffffff || bv != bv || aborted(a)) ? -1 : bi;
                         } else {  // this rank's shard winner -> every rank's exchange slot [my rank][t]
                             for (int rr = 0; rr < a.tp_world; ++rr)
                                 sm.peers.axch[rr][a.tp_rank * 256 + t] = make_float2(bv, __int_as_float(bi));
@@ -1197,7 +1248,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                         for (int rr = 0; rr < a.tp_world; ++rr) st_release_sys_u64(sm.peers.aflag[rr] + a.tp_rank, tag);
                         for (int src = 0; src < a.tp_world; ++src) {
                             Spin sp;
-                            while (ld_acquire_sys_u64(sm.peers.aflag[a.tp_rank] + src) != tag) sp.tick(a.err, 10, p);
+                            while (ld_acquire_sys_u64(sm.peers.aflag[a.tp_rank] + src) != tag)
+                                if (sp.tick(a, 10, p)) break;
                         }
                         for (int t = 0; t < T; ++t) {
                             float bv = -INFINITY;
@@ -1207,7 +1259,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                                 const int wi = __float_as_int(w.y);
                                 if (w.x > bv || (w.x == bv && wi < bi)) { bv = w.x; bi = wi; }
                             }
-                            a.argmax[start + t] = (bi == 0x7fffffff || bv != bv) ? -1 : bi;
+                            a.argmax[start + t] = (bi == 0x7fffffff || bv != bv || aborted(a)) ? -1 : bi;
                         }
                     }
                     if constexpr (kB) {

@@ -112,7 +112,8 @@ struct FwdArgs {
     int ld_logits;
     unsigned long long* done;   // [n_ph] monotone completion counters
     unsigned long long* epoch;  // forwards completed on this cache
-    int* err;                   // watchdog code (0 = fine)
+    int* err;                   // watchdog: the tag of the aborted forward (fwd.cu), else stale / 0
+    unsigned long long wd_ns;   // watchdog: a wait without progress for this long aborts the forward
     unsigned long long* trace;  // optional [n_ph][G][16] %globaltimer stamps
     int tp_world, tp_rank, vocab_off;  // tensor parallel (world 1: none); vocab_off = rank * vocab_l
     TpPeers peers;

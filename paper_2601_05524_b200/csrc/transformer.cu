@@ -438,6 +438,11 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
     a.done = c.done.p;
     a.epoch = c.epoch.p;
     a.err = c.err.p;
+    a.wd_ns = [] {  // DBL_FWD_WATCHDOG_MS (tests shorten it); default 4 s
+        const char* e = std::getenv("DBL_FWD_WATCHDOG_MS");
+        const long long ms = e ? std::atoll(e) : 4000;
+        return static_cast<unsigned long long>(ms > 0 ? ms : 4000) * 1000000ull;
+    }();
     a.trace = fwd_trace_buffer(c.n_ph, c.grid);
     a.tp_world = m.world;
     a.tp_rank = m.rank;

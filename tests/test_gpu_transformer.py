@@ -164,3 +164,24 @@ def test_verify_forward_above_256_rows_is_split(dbl):
         assert r.output == ar.output, (gamma, depth)
         longest = max(longest, max(t["pending"] + depth + 1 for t in r.traces))
     assert longest > 256, f"workload never needed a split forward ({longest} rows)"
+
+
+def test_watchdog_aborts_without_poisoning_the_context(dbl):
+    """A forward whose dependency never resolves (DBL_FWD_DBG=3; in production: a missing tensor-parallel
+    peer) is aborted by the watchdog: the call raises RuntimeError and the next forward on the same
+    model and context is correct (no __trap, no sticky CUDA error)."""
+    import os
+    m, _ = make(dbl, "tiny-qwen", 5)
+    ctx, cands = list(range(1, 40)), [3, 4, 5]
+    want = dbl.forward_batch(m, ctx, cands)
+    os.environ["DBL_FWD_DBG"], os.environ["DBL_FWD_WATCHDOG_MS"] = "3", "200"
+    try:
+        with pytest.raises(dbl._capi.DoubleError) as ei:
+            dbl.forward_batch(m, ctx, cands)
+        assert not isinstance(ei.value, dbl._capi.CudaError), ei.value  # a runtime error, not a dead context
+    finally:
+        os.environ.pop("DBL_FWD_DBG")
+        os.environ.pop("DBL_FWD_WATCHDOG_MS")
+    assert dbl.forward_batch(m, ctx, cands) == want
+    assert dbl.run(m, m, dbl.HierarchicalDatastore(3, 10), ctx, 16, dbl.PipelineOptions(gamma=2)).output == \
+        dbl.run_vanilla_ar(m, ctx, 16).output
