@@ -515,6 +515,9 @@ struct TileCtx {
     float* pre;              // shared memory [16][128] (column-major: thread r reads pre[i*128 + r])
     const TpPeers* peers;    // tensor-parallel exchange buffers (shared-memory copy)
     const BatchSmem* bt;     // batched forward: rows -> lanes
+    uint32_t tpre;           // TMEM columns (this warp's lanes) holding every chunk's presum (tp <= 64),
+                             // valid when pre_all; else only chunk 0 lives in `pre`
+    bool pre_all;
 };
 
 template <int CH>
@@ -619,6 +622,31 @@ __device__ __forceinline__ void presum(const TileCtx& x, int ch, const float* re
     }
 }
 
+// the presum of chunk ch (+ the folded residual) added into v: from TMEM (every chunk presummed early),
+// from `pre` (chunk 0 presummed early), or computed now
+__device__ __forceinline__ void add_presum(const TileCtx& x, int ch, const float* resid, float (&v)[16]) {
+    if (x.pre_all) {
+        float pv[16];
+        tmem_ld16(x.tpre + ch, pv);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += pv[i];
+        return;
+    }
+    if (!x.has_pre || ch > 0) presum(x, ch, resid);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += x.pre[i * kBM + x.r];
+}
+// early: every chunk's presum into TMEM (the accumulator is not ready yet; the partials are)
+__device__ __forceinline__ void presum_all_to_tmem(const TileCtx& x, const float* resid0, long long resid_ld) {
+    for (int ch = 0; ch < x.tp; ch += 16) {
+        presum(x, ch, resid0 ? resid0 + static_cast<long long>(ch) * resid_ld : nullptr);
+        float pv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pv[i] = x.pre[i * kBM + x.r];
+        tmem_st16(x.tpre + ch, pv);
+    }
+}
+
 template <int CH, bool kTP, bool kB>
 __device__ __forceinline__ void finish_tile(const TileCtx& x) {
     const FwdArgs& a = *x.a;
@@ -633,11 +661,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
             float v[CH];
             tmem_ld<CH>(x.taddr + ch, v);
             const int nc = min(CH, tp - ch);
-            if (x.n_contrib > 1) {
-                if (!x.has_pre || ch > 0) presum(x, ch);
-#pragma unroll
-                for (int i = 0; i < CH; ++i) v[i] += x.pre[i * kBM + r];
-            }
+            if (x.n_contrib > 1) add_presum(x, ch, nullptr, v);
             for (int rr = 0; rr < a.tp_world; ++rr) {
                 float* dst = x.peers->xch[rr] + (static_cast<long long>(a.tp_rank * nth + m) * 256 + ch) * kBM + r;
 #pragma unroll
@@ -677,11 +701,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         // residual to the presum (own + (presum + resid)) so the early finisher can do it before its
         // accumulator is ready — every path (row count, early or not) uses this one order
         const bool fold = !kTP && P.epi == kFeResid && x.n_contrib > 1;
-        if (x.n_contrib > 1 && !tp_resid) {
-            if (!x.has_pre || ch > 0) presum(x, ch, fold ? a.resid + static_cast<long long>(ch) * h + n : nullptr);
-#pragma unroll
-            for (int i = 0; i < CH; ++i) v[i] += x.pre[i * kBM + r];
-        }
+        if (x.n_contrib > 1 && !tp_resid) add_presum(x, ch, fold ? a.resid + static_cast<long long>(ch) * h + n : nullptr, v);
         if (et == 0) stamp(a, x.p, 9);
         if (P.epi == kFeResid) {  // resid += acc; xb = bf16(resid); per-tile sum of squares
             float* o = a.resid + static_cast<long long>(ch) * h + n;
@@ -849,7 +869,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x, G = gridDim.x;
-    const uint32_t ncols = static_cast<uint32_t>(a.nacc * a.acc_cols);
+    // TMEM: nacc accumulators (+ one presum region when 16 < tp <= 64: two co-resident CTAs stay <= 512
+    // columns; at tp = 16 the single chunk's presum stays in shared memory, measured faster for the draft)
+    const bool tpre_on = a.tp > 16 && a.tp <= 64;
+    const uint32_t tpre_col = static_cast<uint32_t>(a.nacc * a.acc_cols);
+    const uint32_t ncols = [&] {
+        const uint32_t used = tpre_col + (tpre_on ? static_cast<uint32_t>(a.acc_cols) : 0u);
+        uint32_t n = 32;
+        while (n < used) n <<= 1;
+        return n;
+    }();
 
     if (threadIdx.x == 0) {
         if constexpr (kB) {
@@ -924,9 +953,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             // 16, so every box lands inside the stage).  Rows >= T keep stale data that reaches only padded
             // columns.
             for (int i = 0; i < 5; ++i) tma_prefetch_desc(&a.wmaps[i]);
-            const int n16 = (T + 15) / 16;
-            const int xb_i = T <= 4 ? 0 : T <= 8 ? 1 : 2;  // single box (T <= 16): 4 << xb_i rows
-            const int x_rows_total = T <= 16 ? (4 << xb_i) : n16 * 16;
+            // DBL_FWD_DBG=1 (timing experiment, results invalid): load 16 activation rows whatever T is
+            const int Tx = a.dbg == 1 ? min(T, 16) : T;
+            const int n16 = (Tx + 15) / 16;
+            const int xb_i = Tx <= 4 ? 0 : Tx <= 8 ? 1 : 2;  // single box (T <= 16): 4 << xb_i rows
+            const int x_rows_total = Tx <= 16 ? (4 << xb_i) : n16 * 16;
             const uint32_t stage_tx = static_cast<uint32_t>(kABytes + x_rows_total * kBK * 2);
             for (int i = 0; i < 3; ++i)
                 for (int b = 0; b < 5; ++b) tma_prefetch_desc(&a.xmaps[i][b]);
@@ -937,7 +968,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
             auto issue_x = [&]() {  // the activation rows of unit x into stage xr
                 uint8_t* dst = sB + xr.st * bbytes;
                 const CUtensorMap* xm = a.xmaps[x.xmap];
-                if (T <= 16) {
+                if (Tx <= 16) {
                     tma_load_2d(dst, &xm[xb_i], &full[xr.st], x.kb * kBK, 0, kEvictLast);
                 } else {
                     const int q64 = n16 >> 2, rem = n16 & 3;
@@ -1159,14 +1190,21 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     const bool finisher = my == 0;
                     TileCtx tc{&a, &P, p, m, n_contrib, my, first, tile_u0, U, A, taddr, tp, T, start,
                                q, lane, et, r, rs, red, sval, sidx, tag, (tp_ep << 12) | static_cast<unsigned long long>(p + 1),
-                               false, sm.pre, &sm.peers, &sm.bt};
+                               false, sm.pre, &sm.peers, &sm.bt,
+                               tmem + tpre_col + (static_cast<uint32_t>(q * 32) << 16), false};
                     const bool early = finisher && n_contrib > 1;
-                    if (early) {  // the other contributors are (nearly always) done: sum them now (first
-                                  // 16-column chunk; finish_tile presums any further chunks itself)
+                    if (early) {  // the other contributors are (nearly always) done: sum them now, the
+                                  // residual folded in too (off the tail's chain) — every chunk into TMEM
+                                  // (tp <= 64), else the first chunk into sm.pre
                         wait_partials(tc);
-                        // into sm.pre (own thread's row only), the residual folded in too (off the tail's chain)
-                        presum(tc, 0, !kTP && P.epi == kFeResid ? a.resid + m * kBM + r : nullptr);
-                        tc.has_pre = true;
+                        const float* rz = !kTP && P.epi == kFeResid ? a.resid + m * kBM + r : nullptr;
+                        if (tpre_on) {
+                            presum_all_to_tmem(tc, rz, h);
+                            tc.pre_all = true;
+                        } else {
+                            presum(tc, 0, rz);
+                            tc.has_pre = true;
+                        }
                     }
                     mbar_wait_wd(&tfull[buf], static_cast<uint32_t>((it / a.nacc) & 1), a, 6, p);
                     tc_fence_after();

@@ -86,7 +86,7 @@ struct FwdArgs {
     CUtensorMap xmaps[3][5];  // xb, attn, act; boxes of 4, 8, 16, 32, 64 token rows
     const FwdPhase* ph;
     int n_ph;
-    int dbg;               // DBL_FWD_DBG (timing experiments only; results invalid): 1 no X loads, 2 no MMA
+    int dbg;               // DBL_FWD_DBG (experiments only; results invalid): 1 16 activation rows only, 3 watchdog test
     int tp, stages, nacc, acc_cols;
     LaneState* lane;
     const int32_t* buf;
