@@ -432,6 +432,17 @@ struct DoubleEngine {
             S.target = S.draft;
         if (dm.device() != tm.device() && tm.persistent_grids_on(dm.device()) > 1)
             throw_invalid("draft GPU hosts more than one target shard (at most two persistent forwards per GPU)");
+        // shared memory: the draft's and the target's forward CTAs co-reside on every SM of a shared GPU
+        if (&dm == &tm) {
+            dm.set_smem_budget(kFwdSmemSharedBudget);
+        } else if (tm.persistent_grids_on(dm.device()) > 0) {
+            dm.set_smem_budget(kFwdSmemDraftBudget);
+            tm.set_smem_budget(kFwdSmemBudget);
+        }
+    }
+    ~DoubleEngine() {
+        dm.set_smem_budget(kFwdSmemBudget);
+        tm.set_smem_budget(kFwdSmemBudget);
     }
     bool split() const { return S.dmain != S.main; }
     // the draft side's datastore for sequence q (see DoubleSeq::dst); DBL_STORE_MIRROR=1 forces a replica

@@ -638,7 +638,7 @@ __device__ __forceinline__ void add_presum(const TileCtx& x, int ch, const float
 }
 // early: every chunk's presum into TMEM (the accumulator is not ready yet; the partials are)
 __device__ __forceinline__ void presum_all_to_tmem(const TileCtx& x, const float* resid0, long long resid_ld) {
-    for (int ch = 0; ch < x.tp; ch += 16) {
+    for (int ch = 0; ch < (x.a->dbg == 5 ? 16 : x.tp); ch += 16) {
         presum(x, ch, resid0 ? resid0 + static_cast<long long>(ch) * resid_ld : nullptr);
         float pv[16];
 #pragma unroll
@@ -657,7 +657,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
     const bool tp_resid = kTP && P.epi == kFeResid;
     const int nth = h / kBM;
     if constexpr (kTP) if (tp_resid) {  // this rank's partial of tile m -> every rank's exchange slot [my rank][m]
-        for (int ch = 0; ch < tp; ch += CH) {
+        for (int ch = 0; ch < (a.dbg == 5 ? 16 : tp); ch += CH) {
             float v[CH];
             tmem_ld<CH>(x.taddr + ch, v);
             const int nc = min(CH, tp - ch);
@@ -682,7 +682,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         }
         named_bar_sync(1, 128);
     }
-    for (int ch = 0; ch < tp; ch += CH) {
+    for (int ch = 0; ch < (a.dbg == 5 ? 16 : tp); ch += CH) {
         float v[CH];
         const int nc = min(CH, tp - ch);
         if (kTP && tp_resid) {  // sum of the ranks' partials, rank order (identical on every rank)
@@ -1212,7 +1212,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     if (!finisher) {  // partial -> slot, then release the slot flag
                         const int slot = 2 * rg.ci + (u == rg.b0 ? 0 : 1);
                         float* Pp = a.ws + static_cast<long long>(slot) * tp * kBM;
-                        for (int ch = 0; ch < tp; ch += 16) {
+                        for (int ch = 0; ch < (a.dbg == 5 ? 16 : tp); ch += 16) {
                             float v[16];
                             tmem_ld16(taddr + ch, v);
 #pragma unroll
@@ -1336,21 +1336,30 @@ void fwd_prepare() {
                                         227 * 1024 - kFwdMiscBytes));
         CUDA_CHECK(cudaFuncSetAttribute(fwd_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         227 * 1024 - kFwdMiscBytes));
+        // the whole unified L1 as shared memory: a target CTA (~140 KB) and a draft CTA (~68 KB) must
+        // co-reside on every SM whichever launches first (the driver would otherwise size the carveout
+        // for the first kernel alone and the second persistent grid would wait for the first to finish)
+        for (auto k : {fwd_kernel<false, false>, fwd_kernel<true, false>, fwd_kernel<false, true>})
+            CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared));
     });
 }
 
-int fwd_smem_budget() {  // DBL_FWD_SMEM_KB overrides (A/B)
+int fwd_smem_budget(int budget) {  // DBL_FWD_SMEM_KB overrides (A/B)
     static const int kb = [] {
         const char* e = std::getenv("DBL_FWD_SMEM_KB");
         return e ? std::atoi(e) : 0;
     }();
-    return kb > 0 ? std::min(kb, 227) * 1024 : kFwdSmemBudget;
+    return kb > 0 ? std::min(kb, 227) * 1024 : budget;
 }
 
-int fwd_stages(int tp, size_t* smem) {
+int fwd_stages(int tp, int budget, size_t* smem) {
     const int stage = kABytes + tp * kBK * 2;
-    const int s = (fwd_smem_budget() - 1024 - kFwdMiscBytes) / stage;  // kFwdMiscBytes: the static FwdSmem
-    if (s < 2) throw_invalid("stream forward: token bucket too large for the shared-memory ring");
+    // kFwdMiscBytes: the static FwdSmem.  At least two stages even past the budget (a wide batched
+    // forward in the draft role then does not co-reside with the target: the launches serialize)
+    const int s = std::max(2, (fwd_smem_budget(budget) - 1024 - kFwdMiscBytes) / stage);
+    if (1024 + kFwdMiscBytes + 2 * stage > 227 * 1024)
+        throw_invalid("stream forward: token bucket too large for the shared-memory ring");
     const int stages = std::min(s, kFwdMaxStages);
     *smem = 1024 + static_cast<size_t>(stages) * stage;
     return stages;

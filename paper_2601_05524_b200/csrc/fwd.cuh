@@ -130,12 +130,12 @@ constexpr int kFwdThreads = 192;  // warp 0 TMA producer, warp 1 MMA, warps 2..5
 constexpr int kFwdMiscBytes = 16 * 1024;     // static shared state (barriers, reductions, attention);
                                              // <= 16 KiB keeps 2 ring stages at 256 token columns
 constexpr int kFwdMaxStages = 24;
-constexpr int kFwdSmemBudget = 113 * 1024;  // two CTAs per SM: a draft and a target forward co-reside
+// shared-memory budgets per forward CTA: model.cuh (kFwdSmem*Budget)
 constexpr int kFwdMinUnits = 4;             // smallest stream-K range worth a CTA (4 x 16 KiB)
 
 void fwd_prepare();  // kernel attributes (call once, outside graph capture)
 // stages for a token-column bucket; smem bytes returned through *smem
-int fwd_stages(int tp, size_t* smem);
+int fwd_stages(int tp, int budget, size_t* smem);
 
 void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s);
 

@@ -18,6 +18,14 @@ struct LaneCache {
 
 class Lane;
 
+// Shared memory per forward CTA.  Two CTAs co-reside on an SM (a DOUBLE round's draft and target
+// forwards, each a persistent grid): their sum must stay within the SM's 228 KB minus 1 KB per CTA.
+// The target streams most of the bytes and needs the deeper ring at > 16 token columns (measured: 4 ->
+// 7 stages at 32 columns saves 0.3 ms on Qwen3-14B), the latency-bound draft does not.
+constexpr int kFwdSmemBudget = 154 * 1024;       // a model's default (the target role)
+constexpr int kFwdSmemDraftBudget = 72 * 1024;   // the draft role beside a target (DoubleEngine)
+constexpr int kFwdSmemSharedBudget = 113 * 1024; // both roles on one model (self-drafting)
+
 // Optional per-GEMM CUDA-event timing of a model's forwards (bench roofline; off in the decode loop)
 struct GemmProfiler {
     std::vector<cudaEvent_t> ev;  // pairs (before, after) per GEMM launch
@@ -75,6 +83,8 @@ class Model {
     // persistent grids one forward places on GPU `dev` (tensor-parallel shards may span several GPUs)
     virtual int persistent_grids_on(int dev) const { return dev == device() ? persistent_grids() : 0; }
     virtual void set_profiler(GemmProfiler*) {}
+    // shared memory per forward CTA (persistent forwards: fwd.cuh kFwdSmem*Budget)
+    virtual void set_smem_budget(int /*bytes*/) {}
     virtual std::string kind() const = 0;
 };
 

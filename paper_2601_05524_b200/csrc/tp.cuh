@@ -44,6 +44,9 @@ class TpTransformer final : public Model {
         return k;
     }
     void set_profiler(GemmProfiler* p) override { shards_[0]->set_profiler(p); }
+    void set_smem_budget(int bytes) override {
+        for (auto& sh : shards_) sh->set_smem_budget(bytes);
+    }
     int world() const { return static_cast<int>(shards_.size()); }
     Transformer& shard(int r) { return *shards_[static_cast<size_t>(r)]; }
 

@@ -49,6 +49,7 @@ struct Transformer::Impl {
     DevBuf<__nv_bfloat16> w_qkv, w_o, w_gu, w_down;
     CUtensorMap t_qkv, t_o, t_gu, t_down, t_lm;
     GemmProfiler* prof = nullptr;
+    int smem_budget = kFwdSmemBudget;  // per forward CTA (fwd.cuh: the target / draft roles)
     // one process per shard (IPC): this rank's exchange buffers (model-level, exported once), every
     // rank's addresses (peers' opened from their IPC handles) and the model-level exchange-tag counter
     DevBuf<float> ipc_xch;
@@ -383,7 +384,7 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
                  const std::vector<Lane*>* batch = nullptr) {
     if (max_tokens < 1) max_tokens = 1;
     if (max_tokens > kMaxTp) throw_runtime("forward exceeds 256 token columns (decoder must chunk)");
-    const int tp = (max_tokens + 15) / 16 * 16;
+    int tp = (max_tokens + 15) / 16 * 16;
     TfCache& c = *static_cast<TfCache*>(cache);
     if (m.world > 1 && !c.peers.xch[m.world - 1]) throw_logic("tensor-parallel lane cache not linked to its peers");
     FwdArgs a{};
@@ -400,9 +401,10 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
         const char* e = std::getenv("DBL_FWD_DBG");
         return e ? std::atoi(e) : 0;
     }();
+    if (a.dbg == 4 || a.dbg == 5) tp = std::max(tp, 32);  // experiments: the 32-column machinery at <= 16 tokens (5: epilogues on the first 16 columns only)
     a.tp = tp;
     size_t smem = 0;
-    a.stages = fwd_stages(tp, &smem);
+    a.stages = fwd_stages(tp, m.smem_budget, &smem);
     a.acc_cols = tp <= 32 ? 32 : tp <= 64 ? 64 : tp <= 128 ? 128 : 256;
     a.nacc = tp <= 128 ? 2 : 1;
     a.lane = state;
@@ -480,6 +482,8 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
     }
 }
 }  // namespace
+
+void Transformer::set_smem_budget(int bytes) { impl_->smem_budget = bytes; }
 
 void Transformer::forward(Lane& lane, int max_tokens, cudaStream_t s) {
     run_forward(*impl_, device_, lane.state, lane.buf.p, lane.argmax.p, lane.cache.get(), max_tokens, nullptr, 0, s);
