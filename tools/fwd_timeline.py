@@ -34,10 +34,15 @@ n_ph, grid = C.c_int(), C.c_int()
 _capi.check(L.dbl_debug_fwd_trace(st.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(n_ph), C.byref(grid)))
 P, G = n_ph.value, grid.value
 st = st[:P * G * 16].reshape(P, G, 16).astype(np.int64)
+per_layer = (P - 3) // nl  # 5 (attention combined by its last item) or 6 (a separate combine phase)
 kinds, mb = ["embed"], [0.0]
 for _ in range(nl):
-    kinds += ["qkv", "attn", "combine", "o", "gate|up", "down"]
-    mb += [(nh + 2 * nkv) * hd * h * 2 / 1e6, 0.0, 0.0, h * nh * hd * 2 / 1e6, 2 * f * h * 2 / 1e6, h * f * 2 / 1e6]
+    if per_layer == 6:
+        kinds += ["qkv", "attn", "combine", "o", "gate|up", "down"]
+        mb += [(nh + 2 * nkv) * hd * h * 2 / 1e6, 0.0, 0.0, h * nh * hd * 2 / 1e6, 2 * f * h * 2 / 1e6, h * f * 2 / 1e6]
+    else:
+        kinds += ["qkv", "attn", "o", "gate|up", "down"]
+        mb += [(nh + 2 * nkv) * hd * h * 2 / 1e6, 0.0, h * nh * hd * 2 / 1e6, 2 * f * h * 2 / 1e6, h * f * 2 / 1e6]
 kinds += ["lm_head", "argmax"]
 mb += [V * h * 2 / 1e6, 0.0]
 assert len(kinds) == P, (len(kinds), P)
@@ -73,11 +78,11 @@ for k, (us, b) in tot.items():
 print(f"span {prev_done:.1f} us; weights {sum(mb):.0f} MB -> {sum(mb) * 1e6 / (prev_done * 1e3):.0f} GB/s")
 
 # ---- detail of one middle layer: per phase, percentiles over CTAs relative to the previous phase's end
-L0 = 1 + 6 * (nl // 2)
+L0 = 1 + per_layer * (nl // 2)
 print(f"\nlayer {nl // 2} detail (us after the previous phase's last signal; min/median/max over CTAs)")
 names = {1: "dep", 4: "mma0", 5: "mma1", 6: "epi1", 2: "sig"}
 prev = col(L0 - 1, 2, np.max)
-for p in range(L0, L0 + 6):
+for p in range(L0, L0 + per_layer):
     parts = []
     for k in (1, 4, 5, 6, 2):
         v = st[p, :, k][st[p, :, k] > 0]
@@ -100,7 +105,7 @@ for p in range(P):
         units[p], active[p], offset[p], kbs[p] = U, A, off, K // 64
         off = (off + A) % sms
 print("\nstragglers (epilogue end - last MMA, us): top CTAs per phase")
-for p in range(L0, L0 + 6):
+for p in range(L0, L0 + per_layer):
     if p not in units:
         continue
     U, A, o, KB = units[p], active[p], offset[p], kbs[p]
