@@ -21,9 +21,10 @@ class Lane;
 // Shared memory per forward CTA.  Two CTAs co-reside on an SM (a DOUBLE round's draft and target
 // forwards, each a persistent grid): their sum must stay within the SM's 228 KB minus 1 KB per CTA.
 // The target streams most of the bytes and needs the deeper ring at > 16 token columns (measured: 4 ->
-// 7 stages at 32 columns saves 0.3 ms on Qwen3-14B), the latency-bound draft does not.
-constexpr int kFwdSmemBudget = 154 * 1024;       // a model's default (the target role)
-constexpr int kFwdSmemDraftBudget = 72 * 1024;   // the draft role beside a target (DoubleEngine)
+// 6 stages at 32 columns saved 0.3 ms on Qwen3-14B at 16 tokens); the draft keeps 4 stages (3 cost it
+// +3 %, profiles/r2af_*).
+constexpr int kFwdSmemBudget = 136 * 1024;       // a model's default (the target role)
+constexpr int kFwdSmemDraftBudget = 90 * 1024;   // the draft role beside a target (DoubleEngine)
 constexpr int kFwdSmemSharedBudget = 113 * 1024; // both roles on one model (self-drafting)
 
 // Optional per-GEMM CUDA-event timing of a model's forwards (bench roofline; off in the decode loop)
