@@ -10,6 +10,7 @@
 // cursor updates, and starts the next round.  KV "rollback" is a length update: kv_len := LCP of what
 // the device processed and the new committed ⊕ speculative context.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -445,6 +446,49 @@ struct DoubleEngine {
         tm.set_smem_budget(kFwdSmemBudget);
     }
     bool split() const { return S.dmain != S.main; }
+
+    // DBL_ROUND_TIMELINE_FILE=path (+ DBL_ROUND_TIMELINE_N rounds, default 64): per round, the device
+    // intervals of the verify forward and of every draft segment (CUDA events, one GPU: one clock) and
+    // the host's finish_round time, appended as JSON lines — the PSD draft-while-verify overlap record
+    struct Timeline {
+        FILE* f = nullptr;
+        long left = 0, round = 0;
+        cudaEvent_t ev0 = nullptr, tf_acc = nullptr;
+        std::vector<cudaEvent_t> ds, de;
+        void init(int gamma) {
+            for (int j = static_cast<int>(ds.size()); j < gamma; ++j) {
+                cudaEvent_t a, b;
+                CUDA_CHECK(cudaEventCreate(&a));
+                CUDA_CHECK(cudaEventCreate(&b));
+                ds.push_back(a);
+                de.push_back(b);
+            }
+            if (!ev0) {
+                CUDA_CHECK(cudaEventCreate(&ev0));
+                CUDA_CHECK(cudaEventCreate(&tf_acc));
+            }
+        }
+        ~Timeline() {
+            if (f) std::fclose(f);
+            for (auto e : ds) cudaEventDestroy(e);
+            for (auto e : de) cudaEventDestroy(e);
+            if (ev0) cudaEventDestroy(ev0);
+            if (tf_acc) cudaEventDestroy(tf_acc);
+        }
+    } tl_;
+    bool timeline_on(int gamma) {
+        if (tl_.round == 0 && !tl_.f) {
+            const char* path = std::getenv("DBL_ROUND_TIMELINE_FILE");
+            if (path && *path && !split()) {
+                tl_.f = std::fopen(path, "a");
+                const char* n = std::getenv("DBL_ROUND_TIMELINE_N");
+                tl_.left = n ? std::atol(n) : 64;
+            }
+        }
+        if (!tl_.f || tl_.left <= 0) return false;
+        tl_.init(gamma);
+        return true;
+    }
     // the draft side's datastore for sequence q (see DoubleSeq::dst); DBL_STORE_MIRROR=1 forces a replica
     // on the same device (tests the replication path on one GPU)
     void bind_store(DoubleSeq& q, DeviceStore* st) const {
@@ -547,12 +591,16 @@ struct DoubleEngine {
             q.rr->draft_error = q.rr->target_error = 0;
             if (q.smp) launch_derive_rngs(q.smp->rng.p, q.smp->seed, static_cast<uint64_t>(q.round), S.main);
         }
+        const bool tlon = timeline_on(gamma);
+        const auto h0 = std::chrono::steady_clock::now();
+        if (tlon) CUDA_CHECK(cudaEventRecord(tl_.ev0, S.main));
         S.fork();
         // ---- draft worker: iterative_draft over committed ⊕ spec (pipeline.cpp:39-46)
         std::vector<Lane*> dls, tls;
         std::vector<int> bounds;
         DeviceGuard gd(dm.device());
         for (int j = 0; j < gamma; ++j) {
+            if (tlon) CUDA_CHECK(cudaEventRecord(tl_.ds[j], S.draft));
             dls.clear();
             bounds.clear();
             for (DoubleSeq* qp : act) {
@@ -580,6 +628,7 @@ struct DoubleEngine {
                 forward_set(dm, dls, bounds, S.draft);
                 for (DoubleSeq* qp : act) launch_draft_accept(*qp->dl, qp->rr_dev, j, S.draft);
             }
+            if (tlon) CUDA_CHECK(cudaEventRecord(tl_.de[j], S.draft));
         }
         // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
         DeviceGuard gt(tm.device());
@@ -613,8 +662,10 @@ struct DoubleEngine {
             CUDA_CHECK(cudaEventRecord(S.tf1, S.target));
             for (DoubleSeq* qp : act) launch_target_accept(*qp->tl, qp->nc, qp->rr_dev, S.target);
         }
+        if (tlon) CUDA_CHECK(cudaEventRecord(tl_.tf_acc, S.target));
         CUDA_CHECK(cudaStreamSynchronize(S.draft));
         CUDA_CHECK(cudaStreamSynchronize(S.target));
+        const auto h1 = std::chrono::steady_clock::now();
         {
             float ms = 0.f;
             CUDA_CHECK(cudaEventElapsedTime(&ms, S.tf0, S.tf1));
@@ -622,6 +673,27 @@ struct DoubleEngine {
             ++tfwd_n;
         }
         for (DoubleSeq* qp : act) finish(*qp, o);
+        if (tlon) {
+            const auto h2 = std::chrono::steady_clock::now();
+            auto us = [&](cudaEvent_t e) {
+                float ms = 0.f;
+                CUDA_CHECK(cudaEventElapsedTime(&ms, tl_.ev0, e));
+                return 1e3 * ms;
+            };
+            std::fprintf(tl_.f, "{\"round\":%ld,\"gamma\":%d,\"target_fwd\":[%.1f,%.1f],\"target_end\":%.1f,\"draft\":[",
+                         tl_.round, gamma, us(S.tf0), us(S.tf1), us(tl_.tf_acc));
+            for (int j = 0; j < gamma; ++j)
+                std::fprintf(tl_.f, "%s[%.1f,%.1f]", j ? "," : "", us(tl_.ds[j]), us(tl_.de[j]));
+            std::fprintf(tl_.f, "],\"host_wait_us\":%.1f,\"host_finish_us\":%.1f,\"target_rows\":%d}\n",
+                         std::chrono::duration<double, std::micro>(h1 - h0).count(),
+                         std::chrono::duration<double, std::micro>(h2 - h1).count(),
+                         act[0]->L + act[0]->rr->ext_c - (act[0]->nc - 1));
+            ++tl_.round;
+            if (--tl_.left == 0) {
+                std::fclose(tl_.f);
+                tl_.f = nullptr;
+            }
+        }
     }
 
     // finish_round (pipeline.cpp:91-206) + rollback(state, |committed|) (pipeline.cpp:15-30) + the KV

@@ -1418,7 +1418,11 @@ void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool coop = [] {  // DBL_FWD_COOP=0: plain launches (experiment)
+        const char* e = std::getenv("DBL_FWD_COOP");
+        return !(e && e[0] == '0');
+    }();
+    cfg.numAttrs = coop ? 1 : 0;
     if (a.batch.n > 0) {
         if (a.tp_world > 1) throw_invalid("batched forward: tensor-parallel lanes are not supported");
         CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<false, true>, a));
