@@ -624,26 +624,56 @@ __device__ __forceinline__ void presum(const TileCtx& x, int ch, const float* re
 
 // the presum of chunk ch (+ the folded residual) added into v: from TMEM (every chunk presummed early),
 // from `pre` (chunk 0 presummed early), or computed now
-__device__ __forceinline__ void add_presum(const TileCtx& x, int ch, const float* resid, float (&v)[16]) {
+template <int CH>
+__device__ __forceinline__ void add_presum(const TileCtx& x, int ch, const float* resid, float (&v)[CH]) {
     if (x.pre_all) {
-        float pv[16];
-        tmem_ld16(x.tpre + ch, pv);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += pv[i];
+        for (int k = 0; k < CH; k += 16) {
+            float pv[16];
+            tmem_ld16(x.tpre + ch + k, pv);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[k + i] += pv[i];
+        }
         return;
     }
-    if (!x.has_pre || ch > 0) presum(x, ch, resid);
+    if constexpr (CH == 16) {  // 32-column chunks only run with every presum in TMEM
+        if (!x.has_pre || ch > 0) presum(x, ch, resid);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] += x.pre[i * kBM + x.r];
+        for (int i = 0; i < 16; ++i) v[i] += x.pre[i * kBM + x.r];
+    }
 }
-// early: every chunk's presum into TMEM (the accumulator is not ready yet; the partials are)
+// early: every chunk's presum into TMEM (the accumulator is not ready yet; the partials are) — 32 columns
+// at a time, two contributors' loads in flight, accumulated in registers in contributor order (the same
+// order as presum: p_1 + p_2 + ... then + resid)
 __device__ __forceinline__ void presum_all_to_tmem(const TileCtx& x, const float* resid0, long long resid_ld) {
-    for (int ch = 0; ch < (x.a->dbg == 5 ? 16 : x.tp); ch += 16) {
-        presum(x, ch, resid0 ? resid0 + static_cast<long long>(ch) * resid_ld : nullptr);
-        float pv[16];
+    const FwdArgs& a = *x.a;
+    const int tp = x.tp;
+    for (int c0 = 0; c0 < ((a.dbg == 5 || a.dbg == 8) ? 16 : tp); c0 += 32) {
+        const int ncol = min(32, tp - c0);
+        float sacc[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pv[i] = x.pre[i * kBM + x.r];
-        tmem_st16(x.tpre + ch, pv);
+        for (int i = 0; i < 32; ++i) sacc[i] = 0.f;
+        for (int jb = 1; jb < x.n_contrib; jb += 2) {
+            float xs[2][32];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const bool load = jb + j < x.n_contrib;
+                const float* Pj = a.ws + static_cast<long long>(load ? slot_of(x, jb + j) : 0) * tp * kBM + c0 * kBM + x.r;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) xs[j][i] = (load && i < ncol) ? __ldcg(Pj + i * kBM) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                sacc[i] = jb == 1 ? xs[0][i] : sacc[i] + xs[0][i];
+                if (jb + 1 < x.n_contrib) sacc[i] += xs[1][i];
+            }
+        }
+        if (resid0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sacc[i] += i < ncol ? __ldcg(resid0 + static_cast<long long>(c0 + i) * resid_ld) : 0.f;
+        }
+        tmem_st16(x.tpre + c0, sacc);
+        if (ncol > 16) tmem_st16(x.tpre + c0 + 16, sacc + 16);
     }
 }
 
@@ -657,7 +687,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
     const bool tp_resid = kTP && P.epi == kFeResid;
     const int nth = h / kBM;
     if constexpr (kTP) if (tp_resid) {  // this rank's partial of tile m -> every rank's exchange slot [my rank][m]
-        for (int ch = 0; ch < (a.dbg == 5 ? 16 : tp); ch += CH) {
+        for (int ch = 0; ch < ((a.dbg == 5 || a.dbg == 7) ? 16 : tp); ch += CH) {
             float v[CH];
             tmem_ld<CH>(x.taddr + ch, v);
             const int nc = min(CH, tp - ch);
@@ -682,7 +712,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
         }
         named_bar_sync(1, 128);
     }
-    for (int ch = 0; ch < (a.dbg == 5 ? 16 : tp); ch += CH) {
+    for (int ch = 0; ch < ((a.dbg == 5 || a.dbg == 7) ? 16 : tp); ch += CH) {
         float v[CH];
         const int nc = min(CH, tp - ch);
         if (kTP && tp_resid) {  // sum of the ranks' partials, rank order (identical on every rank)
@@ -717,10 +747,27 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
                 }
                 sq[i] = i < nc ? nv * nv : 0.f;
             }
-            x.red[q * 32 + lane] = warp_colsum<CH>(sq, lane);
-            named_bar_sync(1, 128);
-            if (et < CH && ch + et < tp)
-                a.ssq[m * 256 + ch + et] = ((x.red[et] + x.red[32 + et]) + x.red[64 + et]) + x.red[96 + et];
+            if constexpr (CH == 32) {  // two 16-column halves: the CH = 16 summation order (batch invariance)
+                float lo[16], hi[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    lo[i] = sq[i];
+                    hi[i] = sq[16 + i];
+                }
+                x.red[q * 32 + lane] = warp_colsum<16>(lo, lane);
+                x.sval[q * 32 + lane] = warp_colsum<16>(hi, lane);
+                named_bar_sync(1, 128);
+                if (et < 32 && ch + et < tp) {
+                    const float* rb = et < 16 ? x.red : x.sval;
+                    const int c = et & 15;
+                    a.ssq[m * 256 + ch + et] = ((rb[c] + rb[32 + c]) + rb[64 + c]) + rb[96 + c];
+                }
+            } else {
+                x.red[q * 32 + lane] = warp_colsum<CH>(sq, lane);
+                named_bar_sync(1, 128);
+                if (et < CH && ch + et < tp)
+                    a.ssq[m * 256 + ch + et] = ((x.red[et] + x.red[32 + et]) + x.red[64 + et]) + x.red[96 + et];
+            }
             named_bar_sync(1, 128);
         } else if (P.epi == kFeSilu) {  // rows interleaved 16 gate | 16 up per warp
             const int f = m * 64 + q * 16 + lane;
@@ -731,7 +778,7 @@ __device__ __forceinline__ void finish_tile(const TileCtx& x) {
                 const float up = __shfl_down_sync(0xffffffffu, g, 16);
                 if (lane < 16 && i < nc) o[static_cast<long long>(i) * a.ffn_l] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * up);
             }
-        } else if (P.epi == kFeQkv) {  // rstd scale, q/k RMSNorm, RoPE, q -> qbuf, k/v -> paged KV cache
+        } else if (CH == 16 && P.epi == kFeQkv) {  // rstd scale, q/k RMSNorm, RoPE, q -> qbuf, k/v -> paged KV cache
             const int hd = a.hd, half = hd >> 1;
             const bool in_rows = n < P.n_out;  // warp-uniform (n_out % 64 == 0)
             const bool is_q = n < a.q_dim, is_k = !is_q && n < a.q_dim + a.kv_dim;
@@ -1212,7 +1259,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     if (!finisher) {  // partial -> slot, then release the slot flag
                         const int slot = 2 * rg.ci + (u == rg.b0 ? 0 : 1);
                         float* Pp = a.ws + static_cast<long long>(slot) * tp * kBM;
-                        for (int ch = 0; ch < (a.dbg == 5 ? 16 : tp); ch += 16) {
+                        for (int ch = 0; ch < ((a.dbg == 5 || a.dbg == 6) ? 16 : tp); ch += 16) {
                             float v[16];
                             tmem_ld16(taddr + ch, v);
 #pragma unroll
@@ -1223,7 +1270,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                     } else {
                         if (et == 0) stamp(a, p, 8);
                         if (n_contrib > 1 && !early) wait_partials(tc);
-                        finish_tile<16, kTP, kB>(tc);  // 16-column chunks
+                        // 32-column chunks for 16 < tp <= 64 (every presum is in TMEM) outside QKV (its RoPE /
+                        // head-norm epilogue keeps 16), else 16-column chunks
+                        if constexpr (!kTP) {  // (the exchange path keeps 16: 32 would spill there)
+                            if (tp > 16 && tp <= 64 && P.epi != kFeQkv) finish_tile<32, kTP, kB>(tc);
+                            else finish_tile<16, kTP, kB>(tc);
+                        } else {
+                            finish_tile<16, kTP, kB>(tc);
+                        }
                     }
                     if (et == 0 && finisher) stamp(a, p, 10);
                     tc_fence_before();

@@ -275,7 +275,11 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
                                     (m.h + 127) / 128});
     // CTAs of this model's forward: one per SM, or 1/k of the SMs when k tensor-parallel shards share
     // the GPU (every shard's grid must be resident at once)
-    const int sms = std::max(1, num_sms(device_) / std::max(1, shards_per_device_));
+    static const int grid_div = [] {  // DBL_FWD_GRID_DIV=k: a forward on 1/k of the SMs (experiment)
+        const char* e = std::getenv("DBL_FWD_GRID_DIV");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const int sms = std::max(1, num_sms(device_) / std::max(1, shards_per_device_) / grid_div);
     c.grid = sms;
     c.ws.ensure(sms, kMaxTp, max_tiles);
     // ---- the forward's phase list (fwd.cuh); tensor maps: W 0..4 = qkv, o, gate|up, down, lm head;
@@ -401,7 +405,7 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
         const char* e = std::getenv("DBL_FWD_DBG");
         return e ? std::atoi(e) : 0;
     }();
-    if (a.dbg == 4 || a.dbg == 5) tp = std::max(tp, 32);  // experiments: the 32-column machinery at <= 16 tokens (5: epilogues on the first 16 columns only)
+    if (a.dbg >= 4 && a.dbg <= 8) tp = std::max(tp, 32);  // experiments: the 32-column machinery at <= 16 tokens (5: epilogues on the first 16 columns only)
     a.tp = tp;
     size_t smem = 0;
     a.stages = fwd_stages(tp, m.smem_budget, &smem);
