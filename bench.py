@@ -342,7 +342,7 @@ def main():
     return run_bench(a, rank, world, local, wl, max_new, metric, base_cfg)
 
 
-def tp_children(a, rank, world, cmd=None, timeout=1500):
+def tp_children(a, rank, world, cmd=None, timeout=600):
     """Run this rank's tensor-parallel child (bench.py with DBL_TP_CHILD=rank,world,port) and agree
     across ranks: returns (rank 0's JSON line — "" on other ranks — or None if any rank failed, the
     first error)."""
