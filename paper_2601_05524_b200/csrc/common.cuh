@@ -57,7 +57,13 @@ struct DevBuf {
         if (count) CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
         n = count;
     }
-    void zero(cudaStream_t s = 0) { if (n) CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s)); }
+    // s == 0: completes before returning — the decode loop's streams are non-blocking, so an
+    // asynchronous legacy-stream memset could land after their first writes to this buffer
+    void zero(cudaStream_t s = 0) {
+        if (!n) return;
+        CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+        if (s == 0) CUDA_CHECK(cudaStreamSynchronize(0));
+    }
     void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
     size_t bytes() const { return n * sizeof(T); }
 };

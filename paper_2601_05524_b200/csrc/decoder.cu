@@ -42,7 +42,10 @@ Lane::Lane(Model& m, int cap) : model(m), capacity(cap) {
     argmax.alloc(cap);
     buf.zero();
     CUDA_CHECK(cudaMalloc(&state, sizeof(LaneState)));
-    CUDA_CHECK(cudaMemset(state, 0, sizeof(LaneState)));
+    CUDA_CHECK(cudaMemsetAsync(state, 0, sizeof(LaneState), 0));
+    // complete before the lane is used: its token uploads and kernels run on non-blocking streams that
+    // do not order after the legacy stream (an in-flight memset here once zeroed uploaded tokens)
+    CUDA_CHECK(cudaStreamSynchronize(0));
     cache = m.make_cache(cap);
 }
 Lane::~Lane() {
@@ -82,7 +85,13 @@ struct LaneIO {
     }
 };
 
-constexpr int kPrefillChunk = 256;
+constexpr int kPrefillChunkMax = 256;
+// DBL_PREFILL_CHUNK (experiments): a smaller prefill / long-forward piece
+const int kPrefillChunk = [] {
+    const char* e = std::getenv("DBL_PREFILL_CHUNK");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 && v <= kPrefillChunkMax ? v : kPrefillChunkMax;
+}();
 
 // advance the lane's KV to `upto` (positions [kv_len, upto) processed), in forward-sized chunks
 void catch_up(Lane& lane, int upto, cudaStream_t s) {
@@ -1466,6 +1475,14 @@ void forward_stateless(Model& m, const int32_t* ctx, int L, const int32_t* cands
     else if (out_logits)
         CUDA_CHECK(cudaMemcpyAsync(out_logits, lg.p, lg.bytes(), cudaMemcpyDeviceToHost, S.main));
     CUDA_CHECK(cudaStreamSynchronize(S.main));
+    if (const char* dbg = std::getenv("DBL_DEBUG_STATE_FILE")) {  // debugging: the lane's KV state per call
+        if (FILE* f = std::fopen(dbg, "a")) {
+            unsigned long long h = 0xcbf29ce484222325ull;
+            for (int i = 0; i <= c; ++i) h = (h ^ static_cast<uint32_t>(out_argmax[i])) * 0x100000001b3ull;
+            std::fprintf(f, "argmax=%016llx %s\n", h, m.debug_state_hash(lane, L - 1).c_str());
+            std::fclose(f);
+        }
+    }
     for (int i = 0; i <= c; ++i)
         if (out_argmax[i] < 0) throw_runtime("degenerate distribution");
     if (keep_dists) *keep_dists = std::move(dd);

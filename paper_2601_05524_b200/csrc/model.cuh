@@ -84,6 +84,8 @@ class Model {
     // persistent grids one forward places on GPU `dev` (tensor-parallel shards may span several GPUs)
     virtual int persistent_grids_on(int dev) const { return dev == device() ? persistent_grids() : 0; }
     virtual void set_profiler(GemmProfiler*) {}
+    // debugging: hashes of the lane's device state (KV per layer for positions < upto, scratch buffers)
+    virtual std::string debug_state_hash(Lane&, int /*upto*/) { return ""; }
     // shared memory per forward CTA (persistent forwards: fwd.cuh kFwdSmem*Budget)
     virtual void set_smem_budget(int /*bytes*/) {}
     virtual std::string kind() const = 0;

@@ -489,6 +489,49 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
 
 void Transformer::set_smem_budget(int bytes) { impl_->smem_budget = bytes; }
 
+std::string Transformer::debug_state_hash(Lane& lane, int upto) {
+    const Impl& m = *impl_;
+    TfCache& c = *static_cast<TfCache*>(lane.cache.get());
+    DeviceGuard g(device_);
+    CUDA_CHECK(cudaDeviceSynchronize());
+    auto fnv = [](const void* p, size_t n, unsigned long long h) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+        return h;
+    };
+    std::string out;
+    char buf[64];
+    const int pages = (upto + kPage - 1) / kPage;
+    std::vector<__nv_bfloat16> host(static_cast<size_t>(pages) * m.nkv * kPage * m.hd);
+    for (int l = 0; l < cfg_.n_layers; ++l)
+        for (int kv = 0; kv < 2; ++kv) {
+            const __nv_bfloat16* src = (kv ? c.vbuf.p : c.kbuf.p) + c.layer_stride * l;
+            CUDA_CHECK(cudaMemcpy(host.data(), src, host.size() * 2, cudaMemcpyDeviceToHost));
+            unsigned long long h = 0xcbf29ce484222325ull;
+            for (int pg = 0; pg < pages; ++pg)
+                for (int hh = 0; hh < m.nkv; ++hh)
+                    for (int ps = 0; ps < kPage; ++ps)
+                        if (pg * kPage + ps < upto)
+                            h = fnv(host.data() + ((static_cast<size_t>(pg) * m.nkv + hh) * kPage + ps) * m.hd, m.hd * 2, h);
+            std::snprintf(buf, sizeof buf, "%s%d=%016llx ", kv ? "v" : "k", l, h);
+            out += buf;
+            if (l == 0 && kv == 0) {  // layer 0's K per page (one prefill piece per page at DBL_PREFILL_CHUNK=64)
+                out += "[";
+                for (int pg = 0; pg < pages; ++pg) {
+                    unsigned long long hp = 0xcbf29ce484222325ull;
+                    for (int hh = 0; hh < m.nkv; ++hh)
+                        for (int ps = 0; ps < kPage; ++ps)
+                            if (pg * kPage + ps < upto)
+                                hp = fnv(host.data() + ((static_cast<size_t>(pg) * m.nkv + hh) * kPage + ps) * m.hd, m.hd * 2, hp);
+                    std::snprintf(buf, sizeof buf, "%04llx ", hp & 0xffff);
+                    out += buf;
+                }
+                out += "] ";
+            }
+        }
+    return out;
+}
+
 void Transformer::forward(Lane& lane, int max_tokens, cudaStream_t s) {
     run_forward(*impl_, device_, lane.state, lane.buf.p, lane.argmax.p, lane.cache.get(), max_tokens, nullptr, 0, s);
 }

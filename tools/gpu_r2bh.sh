@@ -1,0 +1,3 @@
+R=1500
+for cfg in "1152 1" "1152 2" "1088 4" "1152 4" "1152 3" "700 4"; do set -- $cfg; DBL_PREFILL_CHUNK=64 timeout 1200 python tools/determinism_stress.py qwen3-0.6b $1 $2 $R; done 2>&1 | grep -v variant > gpurun_out/r2bh.txt
+cat gpurun_out/r2bh.txt
