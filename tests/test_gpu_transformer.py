@@ -185,3 +185,21 @@ def test_watchdog_aborts_without_poisoning_the_context(dbl):
     assert dbl.forward_batch(m, ctx, cands) == want
     assert dbl.run(m, m, dbl.HierarchicalDatastore(3, 10), ctx, 16, dbl.PipelineOptions(gamma=2)).output == \
         dbl.run_vanilla_ar(m, ctx, 16).output
+
+
+def test_repeated_long_context_forwards_are_bitwise_identical(dbl):
+    """Determinism regression (the lossless identity needs it): identical long-context calls — a fresh
+    lane each, prefill in several pieces — return bitwise identical logits and argmax rows.  (A
+    legacy-stream memset racing the token upload once corrupted ~0.5 % of such calls;
+    tools/determinism_stress.py is the long version.)"""
+    import hashlib
+    cfg = dbl.transformer_config("qwen3-0.6b", seed=7, max_seq=1408, n_layers=2)
+    m = dbl.Transformer(cfg)
+    rnd = random.Random(5)
+    ctx = [rnd.randrange(cfg.vocab) for _ in range(1152)]
+    cands = [rnd.randrange(cfg.vocab) for _ in range(3)]
+    hs, rows = set(), set()
+    for _ in range(40):
+        hs.add(hashlib.sha256(np.ascontiguousarray(dbl.forward_logits(m, ctx, cands)).tobytes()).hexdigest())
+        rows.add(tuple(dbl.forward_batch(m, ctx, cands)))
+    assert len(hs) == 1 and len(rows) == 1, (len(hs), len(rows))
