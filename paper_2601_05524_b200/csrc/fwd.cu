@@ -153,9 +153,7 @@ struct Ring {  // ring slot + mbarrier parity of the next use
 // context's KV cache) would otherwise be fetched from DRAM at the moment they are needed — behind a
 // saturated weight stream, i.e. microseconds per dependent load.  They are warmed into L2 ahead of use
 // with bulk prefetches, split over `parts` issuers.
-__device__ int g_nowarm;  // DBL_FWD_DBG=10 (experiment): no L2 warming
 __device__ __forceinline__ void l2_warm(const void* base, long long bytes, int part, int parts) {
-    if (g_nowarm) return;
     constexpr long long kChunk = 16384;
     const long long n = (bytes + kChunk - 1) / kChunk;
     const uintptr_t b = reinterpret_cast<uintptr_t>(base) & ~uintptr_t(15);
@@ -959,7 +957,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         }
         *sep = *reinterpret_cast<volatile unsigned long long*>(a.epoch);
         g_wdtag = static_cast<int>(*sep & 0x3fffffffull) + 1;
-        if (c == 0) g_nowarm = a.dbg == 10;
         sm.tp_ep = a.tp_epoch ? *reinterpret_cast<volatile unsigned long long*>(a.tp_epoch) : *sep;
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
@@ -1149,7 +1146,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         const int h = a.h;
         int it = 0;
         auto signal = [&](int p) {  // this CTA's contribution to phase p is written
-            if (a.dbg == 11) __threadfence();  // experiment: every thread fences its own writes
             fence_proxy_async_global();
             named_bar_sync(1, 128);
             if (et == 0) {
@@ -1160,7 +1156,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
         auto acquire = [&](int p) {
             if (et == 0) wait_dep(a, p, ep, 5);
             named_bar_sync(1, 128);
-            if (a.dbg == 11) fence_acq_rel_gpu();  // experiment: every thread acquires
         };
         if constexpr (!kB) {  // warm L2: this forward's embedding rows and RoPE rows (tiny, cold, on the critical path)
             const int gt = c * 128 + et, GT = G * 128;
@@ -1244,7 +1239,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) fwd_kernel(const __grid_consta
                                q, lane, et, r, rs, red, sval, sidx, tag, (tp_ep << 12) | static_cast<unsigned long long>(p + 1),
                                false, sm.pre, &sm.peers, &sm.bt,
                                tmem + tpre_col + (static_cast<uint32_t>(q * 32) << 16), false};
-                    const bool early = finisher && n_contrib > 1 && a.dbg != 9;  // DBL_FWD_DBG=9: never early (experiment)
+                    const bool early = finisher && n_contrib > 1;
                     if (early) {  // the other contributors are (nearly always) done: sum them now, the
                                   // residual folded in too (off the tail's chain) — every chunk into TMEM
                                   // (tp <= 64), else the first chunk into sm.pre
