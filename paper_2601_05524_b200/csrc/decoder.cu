@@ -448,11 +448,27 @@ struct DoubleEngine {
         } else if (tm.persistent_grids_on(dm.device()) > 0) {
             dm.set_smem_budget(kFwdSmemDraftBudget);
             tm.set_smem_budget(kFwdSmemBudget);
+            colocated_ = true;
         }
     }
+    // The driver runs cooperative grids one at a time, so a co-located draft's forward and the verify
+    // forward would serialize (§7a).  A draft forward on half the SMs, launched plainly, runs beside the
+    // verify's grid (both always fit: 136 + 90 KB, 64 K registers per SM) — worth it while the draft
+    // chain fits under the verify (gamma <= 2: 150 -> 170 tok/s on configs[1]); longer chains keep the
+    // draft's full grid (each segment is then on the critical path).  DBL_DRAFT_GRID_DIV overrides.
+    void configure_draft(int gamma) {
+        if (!colocated_) return;
+        static const int env = [] {
+            const char* e = std::getenv("DBL_DRAFT_GRID_DIV");
+            return e ? std::max(1, std::atoi(e)) : 0;
+        }();
+        dm.set_draft_grid(env ? env : (gamma <= 2 ? 2 : 1));
+    }
+    bool colocated_ = false;
     ~DoubleEngine() {
         dm.set_smem_budget(kFwdSmemBudget);
         tm.set_smem_budget(kFwdSmemBudget);
+        dm.set_draft_grid(1);
     }
     bool split() const { return S.dmain != S.main; }
 
@@ -864,6 +880,7 @@ std::vector<RunOutput> run_double_multi(Model& dm, Model& tm, const std::vector<
     for (const auto& p : prompts) longest = std::max(longest, p.size());
     const int cap = static_cast<int>(longest) + max_new + 3 * gamma * (d + 1) + 3 * d + 64;
     DoubleEngine E(dm, tm);
+    E.configure_draft(gamma);
     Streams& S = E.S;
 
     std::vector<DoubleSeq> seqs(B);
@@ -1017,6 +1034,7 @@ Trace RoundSession::run_round(HostPipelineState& st, DeviceStore& store, const d
         const int cap = std::max(need, I.cap) + 256;
         I.q.reset();  // its lanes' caches go back to the models first
         I.q = std::make_unique<DoubleSeq>();
+        I.E.configure_draft(o.gamma);
         I.E.init_seq(*I.q, &store, cap, o);
         I.cap = cap;
         I.gamma = o.gamma;

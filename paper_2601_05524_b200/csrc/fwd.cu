@@ -1458,7 +1458,7 @@ void fwd_trace_read(unsigned long long* dst, long long cap, int* n_ph, int* grid
     CUDA_CHECK(cudaMemcpy(dst, t.buf.p, need * 8, cudaMemcpyDeviceToHost));
 }
 
-void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s) {
+void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s, bool coop_in) {
     // Cooperative launch: the forward's CTAs wait on each other (phase counters), so they must be
     // co-resident — gang scheduling guarantees it even when a draft forward or another shard's
     // forward shares the GPU (a partially resident persistent grid could otherwise spin forever).
@@ -1472,11 +1472,11 @@ void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    static const bool coop = [] {  // DBL_FWD_COOP=0: plain launches (experiment)
+    static const bool coop_env = [] {  // DBL_FWD_COOP=0: plain launches (experiment)
         const char* e = std::getenv("DBL_FWD_COOP");
         return !(e && e[0] == '0');
     }();
-    cfg.numAttrs = coop ? 1 : 0;
+    cfg.numAttrs = coop_env && coop_in ? 1 : 0;
     if (a.batch.n > 0) {
         if (a.tp_world > 1) throw_invalid("batched forward: tensor-parallel lanes are not supported");
         CUDA_CHECK(cudaLaunchKernelEx(&cfg, fwd_kernel<false, true>, a));

@@ -137,7 +137,7 @@ void fwd_prepare();  // kernel attributes (call once, outside graph capture)
 // stages for a token-column bucket; smem bytes returned through *smem
 int fwd_stages(int tp, int budget, size_t* smem);
 
-void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s);
+void fwd_launch(const FwdArgs& a, int grid, size_t smem, cudaStream_t s, bool coop = true);
 
 // DBL_FWD_TRACE=1: every forward records per-(phase, CTA) %globaltimer stamps — [0] first weight tile
 // issued, [1] activation dependency resolved (producer), [2] last contribution signalled, [3] epilogue

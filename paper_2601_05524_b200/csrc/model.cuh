@@ -88,6 +88,8 @@ class Model {
     virtual std::string debug_state_hash(Lane&, int /*upto*/) { return ""; }
     // shared memory per forward CTA (persistent forwards: fwd.cuh kFwdSmem*Budget)
     virtual void set_smem_budget(int /*bytes*/) {}
+    // the draft beside a target on one GPU: forwards on 1/div of the SMs, launched plainly (1 = own grid)
+    virtual void set_draft_grid(int /*div*/) {}
     virtual std::string kind() const = 0;
 };
 

@@ -50,6 +50,8 @@ struct Transformer::Impl {
     CUtensorMap t_qkv, t_o, t_gu, t_down, t_lm;
     GemmProfiler* prof = nullptr;
     int smem_budget = kFwdSmemBudget;  // per forward CTA (fwd.cuh: the target / draft roles)
+    int grid_div = 1;                  // draft beside a target: a forward on 1/grid_div of the SMs,
+    bool coop = true;                  // launched plainly so it runs beside the target's grid
     // one process per shard (IPC): this rank's exchange buffers (model-level, exported once), every
     // rank's addresses (peers' opened from their IPC handles) and the model-level exchange-tag counter
     DevBuf<float> ipc_xch;
@@ -81,6 +83,7 @@ struct TfCache final : LaneCache {
     TpPeers peers{};
     int n_ph = 0;
     int grid = 0;  // CTAs per forward (the phase table's split is built for this grid)
+    int grid_div = 1;
     GemmWorkspace ws;
     size_t layer_stride = 0;
 };
@@ -223,8 +226,10 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
     if (impl_->world == 1) {
         std::lock_guard<std::mutex> lk(pool_mu_);
         for (auto it = pool_.begin(); it != pool_.end(); ++it) {
-            const int cap = static_cast<TfCache*>(it->get())->capacity;
-            if (cap == capacity) {  // exact: batched forwards need every lane's KV at the same stride
+            const TfCache* pc = static_cast<TfCache*>(it->get());
+            // exact capacity (batched forwards need every lane's KV at the same stride) and the grid the
+            // phase table was split for
+            if (pc->capacity == capacity && pc->grid_div == impl_->grid_div) {
                 std::unique_ptr<LaneCache> c = std::move(*it);
                 pool_.erase(it);
                 return c;
@@ -275,12 +280,13 @@ std::unique_ptr<LaneCache> Transformer::make_cache(int capacity) {
                                     (m.h + 127) / 128});
     // CTAs of this model's forward: one per SM, or 1/k of the SMs when k tensor-parallel shards share
     // the GPU (every shard's grid must be resident at once)
-    static const int grid_div = [] {  // DBL_FWD_GRID_DIV=k: a forward on 1/k of the SMs (experiment)
+    static const int env_div = [] {  // DBL_FWD_GRID_DIV=k: every forward on 1/k of the SMs (experiment)
         const char* e = std::getenv("DBL_FWD_GRID_DIV");
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
-    const int sms = std::max(1, num_sms(device_) / std::max(1, shards_per_device_) / grid_div);
+    const int sms = std::max(1, num_sms(device_) / std::max(1, shards_per_device_) / env_div / impl_->grid_div);
     c.grid = sms;
+    c.grid_div = impl_->grid_div;
     c.ws.ensure(sms, kMaxTp, max_tiles);
     // ---- the forward's phase list (fwd.cuh); tensor maps: W 0..4 = qkv, o, gate|up, down, lm head;
     // X 0..2 = xb, attn, act
@@ -479,7 +485,7 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
     // vocab-parallel logits: this rank's columns of the caller's [rows][vocab] buffer
     if (logits) a.logits = logits + static_cast<size_t>(m.rank) * m.vocab_l;
     if (m.prof) m.prof->next(s);
-    fwd_launch(a, c.grid, smem, s);
+    fwd_launch(a, c.grid, smem, s, m.coop);
     if (m.prof) {
         m.prof->next(s);
         m.prof->bytes.push_back(static_cast<double>(Transformer::weight_bytes_of(m)));
@@ -488,6 +494,10 @@ void run_forward(Transformer::Impl& m, int device, LaneState* state, const int32
 }  // namespace
 
 void Transformer::set_smem_budget(int bytes) { impl_->smem_budget = bytes; }
+void Transformer::set_draft_grid(int div) {
+    impl_->grid_div = std::max(1, div);
+    impl_->coop = impl_->grid_div == 1;
+}
 
 std::string Transformer::debug_state_hash(Lane& lane, int upto) {
     const Impl& m = *impl_;

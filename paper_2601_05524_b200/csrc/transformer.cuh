@@ -27,6 +27,7 @@ class Transformer final : public Model {
     std::string kind() const override { return "transformer"; }
     int persistent_grids() const override { return 1; }
     void set_smem_budget(int bytes) override;
+    void set_draft_grid(int div) override;
     std::string debug_state_hash(Lane& lane, int upto) override;
     void set_profiler(GemmProfiler* p) override;
     void get_weight(const std::string& name, int layer, uint16_t* out, int64_t numel);
