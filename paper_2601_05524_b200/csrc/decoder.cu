@@ -1046,6 +1046,10 @@ Trace RoundSession::run_round(HostPipelineState& st, DeviceStore& store, const d
     DoubleSeq& q = *I.q;
     q.st = &store;
     q.dst = &store;  // one device (checked above): the draft side reads the same datastore
+    // the caller may have changed the datastore since the last round (API calls run on the legacy
+    // stream; the session's streams are non-blocking): order this round after that work
+    CUDA_CHECK(cudaEventRecord(I.E.S.ready, 0));
+    CUDA_CHECK(cudaStreamWaitEvent(I.E.S.main, I.E.S.ready, 0));
     q.committed = st.committed;
     q.spec = st.speculative;
     q.mode = st.mode;
