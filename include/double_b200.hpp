@@ -98,6 +98,20 @@ class HierarchicalDatastore {  // datastore.hpp:72-95
     int max_order, depth;
 
     void set_rejected_enabled(bool on) { check(dbl_store_set_rejected_enabled(h_, on ? 1 : 0)); }
+    // the device n-gram index over a layer's current sequences (build_prior builds the prior's); later
+    // inserts into the layer are scanned until the next build — lookups are identical either way
+    void build_index(int layer) { check(dbl_store_build_index(h_, layer)); }
+    int64_t index_entries(int layer) const {
+        int64_t v = 0;
+        check(dbl_store_index_entries(h_, layer, &v));
+        return v;
+    }
+    // device microseconds per lookup (back-to-back single-CTA lookups)
+    double profile_lookup(std::span<const TokenId> context, int d, int iters = 100) {
+        double us = 0;
+        check(dbl_store_profile_lookup(h_, context.data(), static_cast<int>(context.size()), d, iters, &us));
+        return us;
+    }
     LookupResult lookup(std::span<const TokenId> context, int d) const {  // datastore.cpp:82-132
         LookupResult r;
         r.candidates.resize(static_cast<size_t>(d > 0 ? d : 1));

@@ -98,6 +98,38 @@ int main() {
         CHECK(throws<std::invalid_argument>([&] { store.lookup(TokenSeq{}, 10); }));
         CHECK(store.stats().lookups == 2 && store.stats().fallback_hits == 1 && store.stats().misses == 1);
     }
+    {  // the device n-gram index (dbl_store_build_index): lookups identical to the scan, before and after
+       // more inserts (the appended tail is scanned), over a randomized store
+        std::mt19937_64 g(17);
+        HierarchicalDatastore scan(3, 10), idx(3, 10);
+        std::vector<TokenSeq> seqs;
+        for (int i = 0; i < 60; ++i) {
+            TokenSeq q;
+            for (int k = 0; k < 8 + static_cast<int>(g() % 40); ++k) q.push_back(static_cast<TokenId>(g() % 24));
+            seqs.push_back(q);
+        }
+        for (int i = 0; i < 40; ++i) {
+            scan.prior.insert(seqs[i], i);
+            idx.prior.insert(seqs[i], i);
+        }
+        idx.build_index(DBL_LAYER_PRIOR);
+        CHECK(idx.index_entries(DBL_LAYER_PRIOR) > 0 && scan.index_entries(DBL_LAYER_PRIOR) == 0);
+        for (int i = 40; i < 60; ++i) {  // an appended tail, and dynamic / rejected layers
+            const int layer = i % 3;
+            (layer == 0 ? scan.prior : layer == 1 ? scan.dynamic : scan.rejected).insert(seqs[i], i);
+            (layer == 0 ? idx.prior : layer == 1 ? idx.dynamic : idx.rejected).insert(seqs[i], i);
+        }
+        int same = 0;
+        for (int k = 0; k < 200; ++k) {
+            TokenSeq ctx;
+            for (int j = 0; j < 1 + static_cast<int>(g() % 6); ++j) ctx.push_back(static_cast<TokenId>(g() % 24));
+            const int d = 1 + static_cast<int>(g() % 10);
+            const LookupResult a = scan.lookup(ctx, d), b = idx.lookup(ctx, d);
+            same += a.candidates == b.candidates && a.source == b.source && a.matched_order == b.matched_order;
+        }
+        CHECK(same == 200);
+        CHECK(idx.profile_lookup(TokenSeq{1, 2, 3}, 10, 20) > 0.0);
+    }
     {  // :33-44 insert/occurrence_count, empty insert throws invalid_argument
         HierarchicalDatastore store(3, 10);
         store.prior.insert(TokenSeq{1, 2, 3, 4}, 0);
