@@ -1,6 +1,7 @@
 // Retrieval kernels (K1 lookup, K1b insert) and the DeviceStore host object.
 // Semantics: HierarchicalDatastore::lookup / NGramIndex::insert (datastore.cpp:9-132).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include <cub/cub.cuh>
@@ -715,7 +716,14 @@ void DeviceStore::load_layer(int l, int max_order, const int64_t* off, const int
     LayerDesc v = desc_of(h);
     set_layer_kernel<<<1, 1, 0, s>>>(desc_dev_, l, v, 0);
     CUDA_LAUNCH_CHECK();
-    build_index(l, s);  // synchronises s (the host vectors above are pageable sources)
+    // the index pays off past a few thousand tokens (a scan of a small prior is as fast as a probe, and
+    // building costs a sort and a host sync); DBL_STORE_INDEX_MIN overrides the threshold
+    static const int64_t index_min = [] {
+        const char* e = std::getenv("DBL_STORE_INDEX_MIN");
+        return e ? std::atoll(e) : 4096LL;
+    }();
+    if (nt >= index_min) build_index(l, s);  // synchronises s
+    else CUDA_CHECK(cudaStreamSynchronize(s));  // the host vectors above are pageable sources
 }
 
 void DeviceStore::lookup_lane(int32_t* buf, LaneState* lane, int d, cudaStream_t s) const {

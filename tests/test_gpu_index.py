@@ -50,15 +50,19 @@ def test_index_golden_vectors(dbl):
 def test_index_known_answers(dbl):
     # test_datastore.cpp:62-136 through an indexed prior
     st = dbl.HierarchicalDatastore(3, 10)
-    dbl.build_prior(st, [[1, 2, 3, 4, 5, 6]], 1)
+    dbl.build_prior(st, [[1, 2, 3, 4, 5, 6]], 1)  # small priors are scanned (index past 4,096 tokens)
+    assert st.prior.index_entries == 0
+    st.prior.build_index()
     assert st.prior.index_entries > 0
     r = st.lookup([9, 2, 3], 10)
     assert (r.candidates, r.source, r.matched_order) == ([4, 5, 6], "prior", 2)
     st = dbl.HierarchicalDatastore(3, 3)
     dbl.build_prior(st, [[1, 2, 3, 4, 5, 6, 7, 8]], 1)
+    st.prior.build_index()
     assert st.lookup([1, 2], 3).candidates == [3, 4, 5]
     st = dbl.HierarchicalDatastore(3, 10)
     dbl.build_prior(st, [[5, 6, 7, 1], [7, 2, 3]], 2)  # higher order beats layer / recency
+    st.prior.build_index()
     st.dynamic.insert([1, 2, 3, 9], 5)
     r = st.lookup([7, 2, 3], 10)  # (7,2,3) and the prior's (2,3) end their sequence: avail 0, skipped
     assert (r.candidates, r.source, r.matched_order) == ([9], "dynamic", 2)
