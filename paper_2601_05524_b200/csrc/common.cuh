@@ -3,6 +3,7 @@
 // capi.cu converts it to a status + thread-local message.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; the ranges cost nothing unless a profiler is attached
 
 #include <cstdint>
 #include <stdexcept>
@@ -110,6 +111,15 @@ struct DeviceGuard {
         if (prev != dev) CUDA_CHECK(cudaSetDevice(dev));
     }
     ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// NVTX range over a host scope (nsys / ncu --nvtx show the decode loop's stages: "dbl.round",
+// "dbl.draft", "dbl.target", "dbl.wait", "dbl.finish_round", "dbl.ar_block", ...)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 void require_device(int device);  // throws DBL_CUDA_ERROR unless an sm_100 device is usable

@@ -599,6 +599,7 @@ struct DoubleEngine {
     // run_round (pipeline.cpp:223-262) for every sequence in `act`: each gets one Trace appended to
     // q.res.traces and its PipelineState advanced; lanes are left holding committed ⊕ speculative.
     void round(const std::vector<DoubleSeq*>& act, const dbl_pipeline_options& o) {
+        NvtxRange nv_round("dbl.round");
         const int d = o.depth, gamma = o.gamma;
         const int c_max = o.draft_retrieval ? d : 0, tc_max = o.target_retrieval ? d : 0;
         for (DoubleSeq* qp : act) {
@@ -624,6 +625,7 @@ struct DoubleEngine {
         std::vector<Lane*> dls, tls;
         std::vector<int> bounds;
         DeviceGuard gd(dm.device());
+        auto nv_draft = std::make_unique<NvtxRange>("dbl.draft");
         for (int j = 0; j < gamma; ++j) {
             if (tlon) CUDA_CHECK(cudaEventRecord(tl_.ds[j], S.draft));
             dls.clear();
@@ -655,8 +657,10 @@ struct DoubleEngine {
             }
             if (tlon) CUDA_CHECK(cudaEventRecord(tl_.de[j], S.draft));
         }
+        nv_draft.reset();
         // ---- target worker: lookup + one batched verify forward (pipeline.cpp:48-70)
         DeviceGuard gt(tm.device());
+        auto nv_target = std::make_unique<NvtxRange>("dbl.target");
         bounds.clear();
         for (DoubleSeq* qp : act) {
             DoubleSeq& q = *qp;
@@ -688,8 +692,12 @@ struct DoubleEngine {
             for (DoubleSeq* qp : act) launch_target_accept(*qp->tl, qp->nc, qp->rr_dev, S.target);
         }
         if (tlon) CUDA_CHECK(cudaEventRecord(tl_.tf_acc, S.target));
-        CUDA_CHECK(cudaStreamSynchronize(S.draft));
-        CUDA_CHECK(cudaStreamSynchronize(S.target));
+        nv_target.reset();
+        {
+            NvtxRange nv_wait("dbl.wait");
+            CUDA_CHECK(cudaStreamSynchronize(S.draft));
+            CUDA_CHECK(cudaStreamSynchronize(S.target));
+        }
         const auto h1 = std::chrono::steady_clock::now();
         {
             float ms = 0.f;
@@ -697,7 +705,10 @@ struct DoubleEngine {
             tfwd_ms += ms;
             ++tfwd_n;
         }
-        for (DoubleSeq* qp : act) finish(*qp, o);
+        {
+            NvtxRange nv_fin("dbl.finish_round");
+            for (DoubleSeq* qp : act) finish(*qp, o);
+        }
         if (tlon) {
             const auto h2 = std::chrono::steady_clock::now();
             auto us = [&](cudaEvent_t e) {
@@ -1153,6 +1164,7 @@ RunOutput run_ar(Model& tm, const int32_t* prompt, int n_prompt, int max_new, do
     int produced = 0;
     bool done = max_new == 0;
     while (!done) {
+        NvtxRange nv_blk("dbl.ar_block");
         const int n = std::min(kBlock, max_new - produced);
         for (int i = 0; i < n; ++i) {
             if (smp) {
