@@ -180,6 +180,12 @@ int dbl_last_run_jsonl(char* buf, int64_t cap, int64_t* len);
 int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
                int64_t jsonl_cap, int64_t* jsonl_len);
+/* Sampled decoding (temperature > 0) at wide vocabularies: by default rows of more than 4,096 entries
+ * use fixed-order parallel reductions and fp32 tempering (same law, deterministic); with exact
+ * sampling on, every row takes the reference's sequential fp64 sums / scan and fp64 pow
+ * (model.cpp:55-68, 83-97; verification.cpp:25-58) — decisions bit-identical to the reference at any
+ * vocabulary, ~0.5 ms of single-thread fp64 work per 150k-entry row.  Applies to every visible device. */
+int dbl_set_exact_sampling(int on);
 /* run_vanilla_ar with a SamplerConfig (harness.cpp:233-258): temperature 0 = dbl_run_ar; > 0 samples
  * each token with Rng(splitmix64(seed ^ 0x6172000000000000)) exactly as the reference */
 int dbl_run_ar_sampled(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,

@@ -500,6 +500,9 @@ inline std::vector<std::vector<double>> forward_batch(const Model& m, std::span<
     return rows;
 }
 
+// sampled decoding at wide vocabularies on the reference-exact path (dbl_set_exact_sampling)
+inline void set_exact_sampling(bool on = true) { check(dbl_set_exact_sampling(on ? 1 : 0)); }
+
 // run_vanilla_ar (harness.cpp:233-258)
 inline RunResult run_vanilla_ar(const Model& target, const TokenSeq& prompt, int max_new_tokens, double t_target = 1.0,
                                 const SamplerConfig& sampler = {}) {

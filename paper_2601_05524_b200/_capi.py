@@ -107,6 +107,7 @@ PROTOTYPES = {
     "dbl_transformer_get_weight": [VP, C.c_char_p, C.c_int, U16P, C.c_int64],
     "dbl_run": [VP, VP, VP, I32P, C.c_int, C.c_int, C.POINTER(PipelineOptions), I32P, C.c_int,
                 C.POINTER(C.c_int), C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
+    "dbl_set_exact_sampling": [C.c_int],
     "dbl_run_ar": [VP, I32P, C.c_int, C.c_int, C.c_double, I32P, C.c_int, C.POINTER(C.c_int),
                    C.POINTER(RunMetrics), C.c_char_p, C.c_int64, I64P],
     "dbl_run_ar_sampled": [VP, I32P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64, I32P, C.c_int,

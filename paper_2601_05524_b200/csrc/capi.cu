@@ -14,6 +14,7 @@
 #include "fwd.cuh"
 #include "verify.cuh"
 #include "gemm.cuh"
+#include "sampling.cuh"
 #include "lane.cuh"
 #include "tf_kernels.cuh"
 #include <cuda_bf16.h>
@@ -714,6 +715,10 @@ int dbl_last_run_jsonl(char* buf, int64_t cap, int64_t* len) {
         }
     });
 }
+int dbl_set_exact_sampling(int on) {
+    return guarded([&] { dbl::set_exact_sampling(on != 0); });
+}
+
 int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_new, double t_target,
                int32_t* out, int cap, int* n_out, dbl_run_metrics* metrics, char* jsonl,
                int64_t jsonl_cap, int64_t* jsonl_len) {

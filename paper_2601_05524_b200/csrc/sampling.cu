@@ -6,10 +6,10 @@
 //   * elementwise work (tempered's pow / normalise, residual max(0, p - q)) is spread over the block
 //     — identical per element to the reference's loop;
 //   * sums and the inverse-CDF scan follow the reference's sequential order on one thread when the
-//     vocabulary is small (<= kExactVocab, e.g. the table models of config 1), so every decision and
-//     token is bit-identical to the reference; wide vocabularies (transformers, no reference to be
-//     bit-identical to) use coalesced fixed-order reductions, a two-level warp-segment scan and fp32
-//     tempering (pow via exp2/log2) — deterministic, same law, ~1.2 MB rows at block bandwidth;
+//     vocabulary is small (<= kExactVocab, e.g. the table models of config 1) or exact sampling is on
+//     (dbl_set_exact_sampling), so every decision and token is bit-identical to the reference; by
+//     default wide vocabularies use coalesced fixed-order reductions, a two-level warp-segment scan
+//     and fp32 tempering (pow via exp2/log2) — deterministic, same law, ~1.2 MB rows at block bandwidth;
 //   * every uniform() is drawn by thread 0 from the lane's mt19937_64 state, staged in shared memory
 //     for the kernel's lifetime, in exactly the reference's draw order.
 #include "rng.cuh"
@@ -21,6 +21,11 @@ namespace {
 
 constexpr int kNT = 1024;
 constexpr int kExactVocab = 4096;
+// reference-exact sampling at every vocabulary size (dbl_set_exact_sampling): the sequential sums,
+// scan and fp64 pow of the small-vocabulary path for wide rows too — bit-identical decisions with the
+// reference at e.g. V = 151,936, at ~0.5 ms of single-thread fp64 work per row
+__device__ int g_exact_sampling = 0;
+__device__ __forceinline__ bool exact_path(int n) { return n <= kExactVocab || g_exact_sampling != 0; }
 
 struct Blk {
     double red[kNT];
@@ -40,7 +45,7 @@ __device__ __forceinline__ double blk_bcast(Blk& sh, double v, bool from0) {
 // sum of w[0, n) in the reference's order (n <= kExactVocab) or a fixed chunked tree
 __device__ double blk_sum(Blk& sh, const double* w, int n) {
     const int t = threadIdx.x;
-    if (n <= kExactVocab) {
+    if (exact_path(n)) {
         if (t == 0) {
             double a = 0.0;
             for (int i = 0; i < n; ++i) a += w[i];
@@ -67,7 +72,7 @@ __device__ double blk_sum(Blk& sh, const double* w, int n) {
 // positive entry whose running sum exceeds u, else the last positive entry (rounding slack), else -1
 __device__ int blk_pick(Blk& sh, const double* w, int n, double u) {
     const int t = threadIdx.x;
-    if (n <= kExactVocab) {
+    if (exact_path(n)) {
         if (t == 0) {
             double acc = 0.0;
             int last = -1, r = -2;
@@ -153,7 +158,7 @@ __device__ bool blk_tempered(Blk& sh, const double* dist, double* out, int n, do
         return true;
     }
     const double inv = 1.0 / T;
-    if (n <= kExactVocab) {
+    if (exact_path(n)) {
         for (int i = threadIdx.x; i < n; i += kNT) out[i] = dist[i] > 0.0 ? pow(dist[i], inv) : 0.0;
     } else {  // fp32 pow (exp2 . log2): rows of 1e5+ entries at block rate; no reference to match here
         const float invf = static_cast<float>(inv);
@@ -470,6 +475,18 @@ void launch_ar_sample(Lane& lane, const double* dist, DevRng* rng, double temper
     ar_sample_kernel<<<1, kNT, 0, s>>>(dist, lane.buf.p, lane.state, lane.model.vocab(), rng, temperature, scratch,
                                        out_host, i);
     CUDA_LAUNCH_CHECK();
+}
+
+void set_exact_sampling(bool on) {
+    int n = 0, cur = 0;
+    CUDA_CHECK(cudaGetDeviceCount(&n));
+    CUDA_CHECK(cudaGetDevice(&cur));
+    const int v = on ? 1 : 0;
+    for (int d = 0; d < n; ++d) {  // every visible device's copy of the module flag
+        CUDA_CHECK(cudaSetDevice(d));
+        CUDA_CHECK(cudaMemcpyToSymbol(g_exact_sampling, &v, sizeof(int)));
+    }
+    CUDA_CHECK(cudaSetDevice(cur));
 }
 
 }  // namespace dbl

@@ -11,6 +11,8 @@ namespace dbl {
 // lane error codes written by the sampled kernels (LaneState::error / RoundResult::*_error)
 enum SampleErr : int { kSampDegenerate = 1, kSampCapacity = 2, kSampInvalid = 3, kSampResidualZero = 4 };
 [[noreturn]] void raise_sample_error(int code);
+// wide vocabularies on the reference-exact path (sequential fp64 sums and scan, fp64 pow) on every device
+void set_exact_sampling(bool on);
 
 // fp32 logits rows -> fp64 softmax rows of positions [row0, L+c) of `lane`; logits row of position p is
 // p - start (single-lane forward) or *row_base + p (batched forward)

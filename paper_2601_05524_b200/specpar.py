@@ -31,7 +31,7 @@ from ._capi import (DoubleError, InvalidArgument, LogicError, PipelineOptions as
 SOURCES = ["prior", "dynamic", "rejected", "context", "miss"]
 PRIOR, DYNAMIC, REJECTED = 0, 1, 2
 
-__all__ = ["NGramIndex", "HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
+__all__ = ["set_exact_sampling", "NGramIndex", "HierarchicalDatastore", "LookupResult", "LookupStats", "TableModel", "Transformer", "TpTransformer",
            "PipelineOptions", "RunResult", "forward_batch", "forward_logits", "forward_dists", "run",
            "run_vanilla_ar", "run_vanilla_ar_batch", "run_batch", "link_tp_processes",
            "run_serial_sd", "build_prior", "last_run_log", "DoubleError", "InvalidArgument", "LogicError",
@@ -603,6 +603,12 @@ def last_run_log() -> np.ndarray:
     buf = np.zeros(max(n.value, 1), np.int32)
     check(lib().dbl_last_run_log(_p32(buf), len(buf), C.byref(n)))
     return buf[:n.value]
+
+
+def set_exact_sampling(on: bool = True):
+    """Sampled decoding at wide vocabularies on the reference-exact path (sequential fp64 sums and
+    scan, fp64 pow — include/double_b200.h: dbl_set_exact_sampling); every visible device."""
+    check(lib().dbl_set_exact_sampling(1 if on else 0))
 
 
 def run_vanilla_ar(target: _Model, prompt, max_new_tokens: int, t_target: float = 1.0,

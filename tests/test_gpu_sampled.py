@@ -6,7 +6,8 @@
 * 30 randomized Double configurations at temperature 1 (+ their sampled AR streams), same bar;
 * transformers: the device loop against the reference's own loop (oracle/_ref) driven by the same
   model's distribution rows through a proxy-model callback — tokens, traces and metrics identical,
-  for a vocabulary on the exact (sequential-sum) path and one on the wide (chunked-sum) path;
+  for a vocabulary on the exact (sequential-sum) path and one on the wide (chunked-sum) path, and at
+  Qwen3's V = 151,936 with exact sampling on (the reference's sequential sums at every width);
 * same seed -> same stream, different seeds -> different streams."""
 import hashlib
 import json
@@ -136,6 +137,43 @@ def test_transformer_sampled_equals_reference_loop(dbl, reference, vocab, temper
         assert r.output == want, method
         assert r.jsonl == wjs, method
         assert _metrics(r) == wm, method
+
+
+@pytest.mark.parametrize("temperature", [0.8])
+def test_transformer_sampled_exact_at_real_vocab(dbl, reference, temperature):
+    """Exact sampling (dbl_set_exact_sampling) at Qwen3's vocabulary, V = 151,936: every row takes the
+    reference's sequential fp64 sums / scan and fp64 pow (model.cpp:55-97, verification.cpp:25-58), so
+    the device loop equals the reference's own loop over the same rows by construction — tokens, traces
+    and metrics — not only when no draw lands near a threshold."""
+    from oracle.pyoracle import make_probs_callback
+    vocab = 151936
+    tgt = dbl.Transformer(dbl.transformer_config("tiny-qwen", seed=43, vocab=vocab, init_std=0.08))
+    drf = dbl.Transformer(dbl.transformer_config("tiny-qwen-draft", seed=44, vocab=vocab, init_std=0.08))
+    prior = _prior(vocab, 9)
+    prompt = prior[0][:12]
+    tcb = make_probs_callback(lambda ctx, c: dbl.forward_dists(tgt, ctx, c), vocab)
+    dcb = make_probs_callback(lambda ctx, c: dbl.forward_dists(drf, ctx, c), vocab)
+    n = 24
+    dbl.set_exact_sampling(True)
+    try:
+        for method, gamma in (("double", 3), ("vanilla_ar", 1), ("sd", 2)):
+            seed = 2000 + gamma
+            want, wjs, wm = reference.run_callback_probs(vocab, dcb, tcb, prior, prompt, n, temperature, seed,
+                                                         method=method, gamma=gamma, depth=6)
+            st = dbl.HierarchicalDatastore(3, 6)
+            dbl.build_prior(st, prior, len(prior))
+            opts = dbl.PipelineOptions(gamma=gamma, depth=6, temperature=temperature, rng_seed=seed)
+            if method == "vanilla_ar":
+                r = dbl.run_vanilla_ar(tgt, prompt, n, temperature=temperature, rng_seed=seed)
+            elif method == "double":
+                r = dbl.run(drf, tgt, st, prompt, n, opts)
+            else:
+                r = dbl.run_serial_sd(drf, tgt, st, prompt, n, opts)
+            assert r.output == want, method
+            assert r.jsonl == wjs, method
+            assert _metrics(r) == wm, method
+    finally:
+        dbl.set_exact_sampling(False)
 
 
 def test_sampled_streams_follow_the_seed(dbl):
