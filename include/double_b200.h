@@ -184,7 +184,8 @@ int dbl_run_ar(dbl_model_t target, const int32_t* prompt, int n_prompt, int max_
  * use fixed-order parallel reductions and fp32 tempering (same law, deterministic); with exact
  * sampling on, every row takes the reference's sequential fp64 sums / scan and fp64 pow
  * (model.cpp:55-68, 83-97; verification.cpp:25-58) — decisions bit-identical to the reference at any
- * vocabulary, ~0.5 ms of single-thread fp64 work per 150k-entry row.  Applies to every visible device. */
+ * vocabulary, ~0.5 ms of single-thread fp64 work per 150k-entry row.  Applies to every visible device;
+ * set it between runs (a decode in flight on another thread may see either setting). */
 int dbl_set_exact_sampling(int on);
 /* run_vanilla_ar with a SamplerConfig (harness.cpp:233-258): temperature 0 = dbl_run_ar; > 0 samples
  * each token with Rng(splitmix64(seed ^ 0x6172000000000000)) exactly as the reference */
